@@ -1,0 +1,148 @@
+"""Pins for the CPU oracle (oracle/solver.py) against what mathematics fixes.
+
+* Chebyshev: the residual after a degree-d Jacobi-preconditioned Chebyshev
+  iteration equals the closed-form scaled Chebyshev polynomial
+  T_d((theta - lambda)/delta) / T_d(theta/delta) applied in the eigenbasis of
+  D^-1/2 S D^-1/2 (numpy.polynomial.chebyshev, not the recurrence).
+* GMRES: after j steps (no restart) the residual is the brute-force minimum
+  over the explicit Krylov space (least squares); restarted GMRES / FGMRES
+  agree with LAPACK LU to 1e-8 (O9); identity -> 1 iteration; exact diagonal
+  preconditioner on a diagonal system -> 1 iteration.
+* PCG: agrees with a dense solve; Jacobi on a diagonal matrix -> 1 iteration.
+* Block-Reg velocity block: the Woodbury form equals the dense inverse of
+  diag(M) + B^T (eps W)^-1 B.
+* Exact Block-Schur on the K = I cube with the sin source converges in 2
+  iterations (the right-hand side is an eigenvector).
+"""
+import numpy as np
+import pytest
+import scipy.sparse as sp
+from numpy.polynomial import chebyshev as npcheb
+
+from oracle import solver as O
+from vemgen import configs
+
+RNG = np.random.default_rng(77)
+
+
+def _spd(n, cond=50.0):
+    Q, _ = np.linalg.qr(RNG.normal(size=(n, n)))
+    lam = np.geomspace(1.0, cond, n)
+    return (Q * lam) @ Q.T
+
+
+@pytest.mark.parametrize("degree", [1, 2, 5, 16])
+def test_chebyshev_closed_form(degree):
+    n = 40
+    S = _spd(n) + np.diag(RNG.uniform(1, 5, n))
+    d = np.diag(S).copy()
+    Dh = np.diag(1 / np.sqrt(d))
+    lam, U = np.linalg.eigh(Dh @ S @ Dh)
+    lmax, ratio = 1.05 * lam.max(), 30.0
+    v = RNG.normal(size=n)
+    x = O.chebyshev(sp.csr_matrix(S), 1 / d, v, degree, lmax, ratio)
+    a, b = lmax / ratio, lmax
+    theta, delta = (a + b) / 2, (b - a) / 2
+    cd = np.zeros(degree + 1)
+    cd[-1] = 1.0
+    rho = npcheb.chebval((theta - lam) / delta, cd) / npcheb.chebval(theta / delta, cd)
+    # r = D^1/2 U rho(L) U^T D^-1/2 v
+    r_ref = np.sqrt(d) * (U @ (rho * (U.T @ (v / np.sqrt(d)))))
+    r = v - S @ x
+    assert np.abs(r - r_ref).max() < 1e-12 * np.abs(v).max()
+
+
+def test_chebyshev_linear():
+    S = sp.csr_matrix(_spd(30) + 3 * np.eye(30))
+    d = S.diagonal()
+    a, b = RNG.normal(size=30), RNG.normal(size=30)
+    f = lambda v: O.chebyshev(S, 1 / d, v, 16, 2.0, 30.0)  # noqa: E731
+    assert np.abs(f(2 * a - 3 * b) - (2 * f(a) - 3 * f(b))).max() < 1e-13 * np.abs(f(a)).max() * 10
+
+
+@pytest.mark.parametrize("j", [1, 3, 7])
+@pytest.mark.parametrize("flexible", [False, True])
+def test_gmres_minimal_residual_bruteforce(j, flexible):
+    n = 25
+    A = RNG.normal(size=(n, n)) + 6 * np.eye(n)
+    Pm = np.diag(RNG.uniform(0.5, 2.0, n))
+    b = RNG.normal(size=n)
+    res = O.gmres(lambda x: A @ x, lambda v: Pm @ v, b, rtol=1e-30, restart=50, maxit=j,
+                  flexible=flexible)
+    assert res.iterations == j
+    AP = A @ Pm
+    Kr = [b]
+    for _ in range(j - 1):
+        Kr.append(AP @ Kr[-1])
+    Kr = np.stack(Kr, 1)
+    Qk, _ = np.linalg.qr(Kr)
+    y, *_ = np.linalg.lstsq(AP @ Qk, b, rcond=None)
+    r_ref = np.linalg.norm(b - AP @ Qk @ y)
+    r = np.linalg.norm(b - A @ res.x)
+    assert abs(r - r_ref) <= 1e-10 * np.linalg.norm(b)
+
+
+def test_gmres_identity_and_diagonal_one_iteration():
+    b = RNG.normal(size=50)
+    r = O.gmres(lambda x: x, lambda v: v, b, 1e-12, 30)
+    assert r.iterations == 1 and r.converged
+    dg = RNG.uniform(1, 10, 50)
+    r = O.gmres(lambda x: dg * x, lambda v: v / dg, b, 1e-12, 30)
+    assert r.iterations == 1 and r.converged and np.abs(r.x - b / dg).max() < 1e-12
+
+
+@pytest.mark.parametrize("kind", [O.PRECOND_BLOCK_SCHUR, O.PRECOND_BLOCK_REG])
+def test_gmres_vs_lu_c1(kind):
+    s = configs.CONFIGS["C1"].build()
+    xd = O.dense_solve(s.M, s.B, s.rhs)
+    r = O.solve(s.M, s.B, s.rhs, kind, 1e-10, 30, eps=configs.eps_for(s))
+    assert r.converged and r.rel_residual_true <= 1e-10
+    assert np.abs(r.x - xd).max() <= 1e-8 * np.abs(xd).max()
+
+
+def test_gmres_vs_lu_k1_tets():
+    s = configs.CONFIGS["C2s"].build()
+    xd = O.dense_solve(s.M, s.B, s.rhs)
+    r = O.solve(s.M, s.B, s.rhs, O.PRECOND_BLOCK_SCHUR, 1e-10, 30)
+    assert r.converged
+    nu = s.layout.n_u
+    for sl in (slice(0, nu), slice(nu, None)):
+        assert np.abs(r.x[sl] - xd[sl]).max() <= 1e-8 * np.abs(xd[sl]).max()
+
+
+def test_exact_schur_eigenvector_case():
+    s = configs.CONFIGS["C1"].build()
+    r = O.solve(s.M, s.B, s.rhs, O.PRECOND_BLOCK_SCHUR, 1e-10, 30, exact_schur=True)
+    assert r.converged and r.iterations == 2
+
+
+def test_pcg_dense_and_diagonal():
+    A = _spd(60, 1e3)
+    b = RNG.normal(size=60)
+    x, its, ok = O.pcg(sp.csr_matrix(A), 1 / np.diag(A), b, 1e-12, 1000)
+    assert ok and np.abs(x - np.linalg.solve(A, b)).max() < 1e-9 * np.abs(x).max()
+    dg = RNG.uniform(1, 100, 60)
+    x, its, ok = O.pcg(sp.diags(dg).tocsr(), 1 / dg, b, 1e-12, 10)
+    assert ok and its == 1
+
+
+def test_woodbury_block_reg_velocity_block():
+    s = configs.CONFIGS["C1"].build()
+    eps = configs.eps_for(s)
+    P = O.Preconditioner(O.PRECOND_BLOCK_REG, s.M, s.B, eps=eps, inner_rtol=1e-14, inner_maxit=5000)
+    nu = s.layout.n_u
+    D = np.diag(s.M.diagonal())
+    Bd = s.B.toarray()
+    ref = np.linalg.inv(D + Bd.T @ Bd / eps)
+    v = RNG.normal(size=s.n)
+    z = P.apply(v)
+    zu_ref = ref @ v[:nu]
+    assert np.abs(z[:nu] - zu_ref).max() < 1e-7 * np.abs(zu_ref).max()
+    assert np.abs(z[nu:] - v[nu:] / eps).max() == 0.0
+
+
+def test_spmv_definition():
+    s = configs.CONFIGS["C1"].build()
+    x = RNG.normal(size=s.n)
+    A = sp.bmat([[s.M, s.B.T], [s.B, None]]).toarray()
+    assert np.abs(O.spmv_saddle(s.M, s.B, x) - A @ x).max() < 1e-13 * np.abs(A @ x).max()

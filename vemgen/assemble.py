@@ -1,0 +1,262 @@
+"""Global assembly of the mixed-VEM saddle-point system.
+
+    [ M  B^T ] [u]   [g]
+    [ B   0  ] [p] = [f]
+
+* M  = sum_P a_{h,P}: consistency nu int Pi v . Pi w plus the dofi-dofi
+  stabilisation s_P = nu(x_P)|P| sum dof_i dof_i, with
+  nu = K^{-1} (reading R4); for a diagonal tensor K the consistency is
+  componentwise and s_P = |P| tr(K^{-1})/3.
+* B  = -|P| DivMatrix per cell, pressure unknowns = moments (readings R6, R7):
+  row alpha of B u = f states div u_h = Pi^0_k f on every cell (P:58,
+  P:805-820).
+* g  = -sum_{f in boundary} sigma_f int_f g_D v.n_f (pressure Dirichlet data,
+  reading R5); f_P = -|P| Hp^{-1} (int_P f m_a)_a.
+
+Global numbering (O5): face DOF  face*n_f + beta,
+                       interior  N_F*n_f + cell*n_i + i,
+                       pressure  cell*n_p + alpha.
+Local matrix entries |a| <= 1e-14 max|template| are dropped before assembly
+(reading R11).
+"""
+from __future__ import annotations
+
+from dataclasses import dataclass, field
+
+import numpy as np
+import scipy.sparse as sp
+
+from . import poly
+from .local import local_operators, volume_rule
+from .quad import gauss_legendre_01, tet_rule, triangle_rule, parallelogram_rule
+
+DROP_TOL = 1e-14
+
+
+@dataclass
+class Layout:
+    k: int
+    n_face_dof: int
+    n_int_dof: int
+    n_p_dof: int
+    n_faces: int
+    n_elems: int
+
+    @property
+    def n_u(self) -> int:
+        return self.n_faces * self.n_face_dof + self.n_elems * self.n_int_dof
+
+    @property
+    def n_p(self) -> int:
+        return self.n_elems * self.n_p_dof
+
+
+@dataclass
+class System:
+    M: sp.csr_matrix
+    B: sp.csr_matrix
+    g: np.ndarray
+    f: np.ndarray
+    layout: Layout
+    mesh: object
+    k: int
+    local: list = field(default_factory=list)  # per class: (class, ops)
+
+    @property
+    def rhs(self) -> np.ndarray:
+        return np.concatenate([self.g, self.f])
+
+    @property
+    def n(self) -> int:
+        return self.layout.n_u + self.layout.n_p
+
+
+def _drop(T):
+    T = np.array(T, copy=True)
+    mx = np.abs(T).reshape(T.shape[0], -1).max(axis=1)
+    T[np.abs(T) <= DROP_TOL * mx.reshape((-1,) + (1,) * (T.ndim - 1))] = 0.0
+    return T
+
+
+def sin_source(x):
+    """f = 3 pi^2 prod sin(pi x_d): the source of p = prod sin(pi x_d), K = I."""
+    return 3 * np.pi ** 2 * np.prod(np.sin(np.pi * x), axis=-1)
+
+
+def exact_p(x):
+    return np.prod(np.sin(np.pi * x), axis=-1)
+
+
+def exact_u(x, K=None):
+    """u = -K grad p (reading R4); K diagonal (3,) or None."""
+    s, c = np.sin(np.pi * x), np.cos(np.pi * x)
+    gp = np.pi * np.stack([c[..., 0] * s[..., 1] * s[..., 2], s[..., 0] * c[..., 1] * s[..., 2],
+                           s[..., 0] * s[..., 1] * c[..., 2]], axis=-1)
+    return -gp if K is None else -gp * K
+
+
+def _box_source_moments(lo, hi, xP, hP, k, nq=16):
+    """int over the union of boxes of f m_a for f = 3pi^2 prod sin(pi x_d),
+    separable in 1D (lo, hi (E, nb, 3)) -> (E, n_k)."""
+    x, w = gauss_legendre_01(nq)
+    E, nb = lo.shape[:2]
+    alphas = poly.multi_indices_3d(k)
+    out = np.zeros((E, len(alphas)))
+    for b in range(nb):
+        I = []
+        for d in range(3):
+            a, bb = lo[:, b, d], hi[:, b, d]
+            pts = a[:, None] + x[None, :] * (bb - a)[:, None]
+            ww = w[None, :] * (bb - a)[:, None]
+            t = (pts - xP[:, d, None]) / hP[:, None]
+            base = ww * np.sin(np.pi * pts)
+            I.append(np.stack([(base * t ** p).sum(1) for p in range(k + 1)], 1))
+        for i, (a1, a2, a3) in enumerate(alphas):
+            out[:, i] += I[0][:, a1] * I[1][:, a2] * I[2][:, a3]
+    return 3 * np.pi ** 2 * out
+
+
+def source_moments(cls, k, source=None, chunk=200000):
+    """F (E, n_k) = int_P f m_a for every cell of the class."""
+    if source is None and cls.vol_kind == "boxes":
+        return _box_source_moments(cls.box_lo, cls.box_hi, cls.centroid, cls.h, k)
+    src = source or sin_source
+    out = []
+    E = cls.centroid.shape[0]
+    for s0 in range(0, E, chunk):
+        sl = slice(s0, min(E, s0 + chunk))
+        g = dict(vol_kind=cls.vol_kind)
+        if cls.vol_kind == "boxes":
+            g["box_lo"], g["box_hi"] = cls.box_lo[sl], cls.box_hi[sl]
+        else:
+            g["tet_verts"] = cls.tet_verts[sl]
+        pts, w = volume_rule(g, 2 * k + 8)
+        m = poly.eval_monomials_3d((pts - cls.centroid[sl, None, :]) / cls.h[sl, None, None], k)
+        out.append(np.einsum("eq,eq,eqa->ea", w, src(pts), m))
+    return np.concatenate(out, axis=0)
+
+
+def boundary_term(mesh, k, gD):
+    """g_(f,beta) = -sigma_f sum_gamma CF[gamma, beta] int_f g_D m^f_gamma on
+    boundary faces (natural pressure BC).  Returns (dof ids, values)."""
+    fg = mesh.boundary_geom
+    nf = poly.dim_pk_2d(k)
+    q = 2 * k + 8
+    if fg.kind == "para":
+        fp, fw = parallelogram_rule(fg.v0, fg.v1, fg.v2, q)
+    else:
+        fp, fw = triangle_rule(fg.v0, fg.v1, fg.v2, q)
+    from .local import face_coords
+    mf = poly.eval_monomials_2d(face_coords(fg, fp), k)
+    Hf = np.einsum("eq,eqa,eqb->eab", fw, mf, mf)
+    CF = fg.area[:, None, None] * np.linalg.inv(Hf)
+    G = np.einsum("eq,eq,eqa->ea", fw, gD(fp), mf)
+    val = -mesh.boundary_sign[:, None] * np.einsum("eab,ea->eb", CF, G)
+    dofs = mesh.boundary_faces[:, None] * nf + np.arange(nf)[None, :]
+    return dofs.reshape(-1), val.reshape(-1)
+
+
+def build_system(mesh, k: int, source=None, gD=None, keep_local=False) -> System:
+    """Assemble M, B, g, f for mesh at order k (RT-type, reading R1)."""
+    nf = poly.dim_pk_2d(k)
+    nk = poly.dim_pk_3d(k)
+    n_int = (nk - 1) + poly.dim_gperp(k)
+    lay = Layout(k, nf, n_int, nk, mesh.n_faces, mesh.n_cells)
+    Nu, Np = lay.n_u, lay.n_p
+    mr, mc, mv, br, bc, bv = [], [], [], [], [], []
+    f = np.zeros(Np)
+    local_keep = []
+    for cls in mesh.classes:
+        E = cls.cell_ids.shape[0]
+        ops = local_operators(cls.rep(), k)
+        nloc = ops["nloc"]
+        fd = (cls.face_ids[:, :, None] * nf + np.arange(nf)[None, None, :]).reshape(E, -1)
+        idofs = mesh.n_faces * nf + cls.cell_ids[:, None] * n_int + np.arange(n_int)[None, :]
+        L = np.concatenate([fd, idofs], axis=1)
+        assert L.shape[1] == nloc
+        P = cls.cell_ids[:, None] * nk + np.arange(nk)[None, :]
+        Kc = mesh.K[cls.cell_ids]
+        invK = 1.0 / Kc
+        sP = cls.vol * invK.mean(axis=1)
+        A = np.stack([_drop(ops["A"][:, c]) for c in range(3)], axis=1)
+        S = _drop(ops["S"])
+        Bt = _drop(-ops["vol"][:, None, None] * ops["Div"])
+        if cls.congruent:
+            mask = (A[0] != 0).any(axis=0) | (S[0] != 0)
+            ii, jj = np.nonzero(mask)
+            vals = (invK[:, 0, None] * A[0, 0][ii, jj] + invK[:, 1, None] * A[0, 1][ii, jj]
+                    + invK[:, 2, None] * A[0, 2][ii, jj] + sP[:, None] * S[0][ii, jj])
+            mr.append(L[:, ii].reshape(-1)); mc.append(L[:, jj].reshape(-1)); mv.append(vals.reshape(-1))
+            bi, bj = np.nonzero(Bt[0])
+            br.append(P[:, bi].reshape(-1)); bc.append(L[:, bj].reshape(-1))
+            bv.append(np.broadcast_to(Bt[0][bi, bj], (E, bi.size)).reshape(-1))
+        else:
+            Ml = np.einsum("ec,ecij->eij", invK, A) + sP[:, None, None] * S
+            nz = Ml != 0
+            mr.append(np.broadcast_to(L[:, :, None], Ml.shape)[nz])
+            mc.append(np.broadcast_to(L[:, None, :], Ml.shape)[nz])
+            mv.append(Ml[nz])
+            nzb = Bt != 0
+            br.append(np.broadcast_to(P[:, :, None], Bt.shape)[nzb])
+            bc.append(np.broadcast_to(L[:, None, :], Bt.shape)[nzb])
+            bv.append(Bt[nzb])
+        F = source_moments(cls, k, source)
+        Hinv = np.linalg.inv(ops["Hp"])
+        fP = -cls.vol[:, None] * np.einsum("eab,eb->ea", np.broadcast_to(Hinv, (E, nk, nk)), F)
+        f[P.reshape(-1)] = fP.reshape(-1)
+        if keep_local:
+            local_keep.append((cls, ops, L, P))
+    M = _to_csr(np.concatenate(mr), np.concatenate(mc), np.concatenate(mv), Nu, Nu)
+    B = _to_csr(np.concatenate(br), np.concatenate(bc), np.concatenate(bv), Np, Nu)
+    g = np.zeros(Nu)
+    if gD is not None:
+        dofs, vals = boundary_term(mesh, k, gD)
+        np.add.at(g, dofs, vals)
+    return System(M, B, g, f, lay, mesh, k, local_keep)
+
+
+def _to_csr(r, c, v, nr, nc):
+    A = sp.coo_matrix((v, (r.astype(np.int64), c.astype(np.int64))), shape=(nr, nc)).tocsr()
+    A.sum_duplicates()
+    A.sort_indices()
+    return A
+
+
+def pressure_coeffs(system: System, p_mom: np.ndarray):
+    """Monomial coefficients of p_h from moment unknowns: q = |P| Hp^{-1} mu."""
+    out = []
+    for cls, ops, L, P in system.local:
+        E = cls.cell_ids.shape[0]
+        Hinv = np.broadcast_to(np.linalg.inv(ops["Hp"]), (E,) + ops["Hp"].shape[1:])
+        out.append((cls, cls.vol[:, None] * np.einsum("eab,eb->ea", Hinv, p_mom[P])))
+    return out
+
+
+def l2_errors(system: System, u: np.ndarray, p: np.ndarray, K=None):
+    """Relative errors e_u = ||u - Pi^0_k u_h|| / ||u||, e_p = ||p - p_h|| / ||p||
+    (with Pi^0_k u_h for the velocity)."""
+    k = system.k
+    nk = poly.dim_pk_3d(k)
+    eu2 = nu2 = ep2 = np2 = 0.0
+    for cls, ops, L, P in system.local:
+        E = cls.cell_ids.shape[0]
+        g = dict(vol_kind=cls.vol_kind)
+        if cls.vol_kind == "boxes":
+            g["box_lo"], g["box_hi"] = cls.box_lo, cls.box_hi
+        else:
+            g["tet_verts"] = cls.tet_verts
+        pts, w = volume_rule(g, 2 * k + 8)
+        m = poly.eval_monomials_3d((pts - cls.centroid[:, None, :]) / cls.h[:, None, None], k)
+        Pi = np.broadcast_to(ops["Pi"], (E,) + ops["Pi"].shape[1:])
+        cu = np.einsum("eil,el->ei", Pi, u[L])                     # (E, 3 nk)
+        uh = np.stack([np.einsum("eqa,ea->eq", m, cu[:, c * nk:(c + 1) * nk]) for c in range(3)], -1)
+        Hinv = np.broadcast_to(np.linalg.inv(ops["Hp"]), (E, nk, nk))
+        cp = cls.vol[:, None] * np.einsum("eab,eb->ea", Hinv, p[P])
+        ph = np.einsum("eqa,ea->eq", m, cp)
+        ue = exact_u(pts, K)
+        pe = exact_p(pts)
+        eu2 += float(np.einsum("eq,eqd->", w, (ue - uh) ** 2))
+        nu2 += float(np.einsum("eq,eqd->", w, ue ** 2))
+        ep2 += float(np.einsum("eq,eq->", w, (pe - ph) ** 2))
+        np2 += float(np.einsum("eq,eq->", w, pe ** 2))
+    return np.sqrt(eu2 / nu2), np.sqrt(ep2 / np2)
