@@ -1,0 +1,180 @@
+/*
+ * vem_mixed.h — C ABI of the B200 (sm_100a) block-preconditioned GMRES solver
+ * for the mixed virtual element saddle-point system
+ *
+ *        [ M  B^T ] [u]   [g]
+ *        [ B   0  ] [p] = [f]                         PAPER.md P:952-961 (C = 0)
+ *
+ * produced by the order-k mixed VEM of PAPER.md §4 (M = velocity mass matrix,
+ * eqn a_{h,P}; B = discrete divergence).
+ *
+ * The solve is right-preconditioned GMRES(m) (FGMRES(m) for Block-Reg), the
+ * Krylov method of P:962, with the two block-diagonal preconditioners of
+ * P:963-985:
+ *   Block-Schur: B_1 = diag(M); B_2 = S = -B diag(M)^-1 B^T, whose
+ *     inverse is applied by a fixed-degree Jacobi-preconditioned Chebyshev
+ *     iteration on S_D = B diag(M)^-1 B^T (reading R15; the paper
+ *     uses an exact MUMPS solve).
+ *   Block-Reg: B_2^-1 = (eps W)^-1; B_1^-1 = (diag(M) + B^T (eps W)^-1 B)^-1
+ *     applied by the Woodbury identity with an inner Jacobi-PCG on
+ *     S_D + eps W (reading R16; the paper uses GAMG on A + B^T W^-1 B).
+ *
+ * Everything runs in FP64 on the CUDA device; there is no CPU fallback.  A
+ * host-side CSR input is copied to the device during upload; every later step
+ * (format build, S_D product, preconditioners, Arnoldi, Givens, restarts)
+ * runs in this library's kernels.
+ *
+ * Status codes (int return): see VEM_* below; vem_status_string() names them,
+ * vem_last_error() returns the last detailed message of a context.
+ */
+#ifndef VEM_MIXED_H
+#define VEM_MIXED_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+enum {
+  VEM_OK = 0,
+  VEM_NOT_CONVERGED = 1,   /* maxit reached: the last iterate is written, report filled */
+  VEM_BREAKDOWN = 2,       /* Arnoldi breakdown at the first step of a cycle            */
+  VEM_ERR_INVALID = -1,    /* NULL / size mismatch / unsorted or out-of-range indices / eps<=0   */
+  VEM_ERR_DIAG_M = -2,     /* non-positive diag(M)                                       */
+  VEM_ERR_DIAG_S = -3,     /* non-positive diag(S_D) (B rank deficient)                          */
+  VEM_ERR_CUDA = -4,       /* CUDA error or out of device memory                                 */
+  VEM_ERR_PRECOND = -5,    /* unsupported precond_kind                                           */
+  VEM_ERR_INNER = -6       /* Block-Reg inner PCG did not reach inner_rtol in inner_maxit        */
+};
+
+enum { VEM_PRECOND_NONE = 0, VEM_PRECOND_BLOCK_SCHUR = 1, VEM_PRECOND_BLOCK_REG = 2 };
+
+typedef struct vem_ctx vem_ctx;    /* opaque; owns every device buffer it allocates */
+
+/* Host CSR matrix, caller-owned, read during upload only.  Rows sorted by
+ * column, no duplicates, 0-based.  indptr has n_rows + 1 entries. */
+typedef struct {
+  int64_t n_rows, n_cols, nnz;
+  const int64_t *indptr;
+  const int32_t *indices;
+  const double *values;
+} vem_csr;
+
+/* DOF layout of the assembled system: velocity =
+ * [n_faces * n_face_dof face moments | n_elems * n_int_dof interior moments],
+ * pressure = n_elems * n_p_dof moments.  Used for validation and reporting. */
+typedef struct {
+  int32_t k, n_face_dof, n_int_dof, n_p_dof;
+  int64_t n_faces, n_elems;
+} vem_layout;
+
+typedef struct {
+  int32_t restart;        /* m, GMRES(m) restart length (default 30)                      */
+  int32_t cheb_degree;    /* d, Chebyshev degree of the Block-Schur B_2 apply (default 16) */
+  double  cheb_ratio;     /* lambda_max / lambda_min of the Chebyshev interval (default 30) */
+  double  inner_rtol;     /* Block-Reg inner PCG relative tolerance (default 1e-10)        */
+  int32_t inner_maxit;    /* Block-Reg inner PCG iteration cap (default 10000)             */
+  int32_t use_graphs;     /* 1: replay GMRES cycles / PCG chunks as CUDA graphs (default)  */
+  int32_t timing;         /* 1: time every kernel launch with CUDA events (stats below)    */
+  int32_t pcg_chunk;      /* PCG steps per host convergence poll (default 16)              */
+} vem_opts;
+
+typedef struct {
+  int32_t status;                 /* same value as the return code                       */
+  int32_t iterations;             /* total Arnoldi steps                          */
+  int32_t restarts;
+  int32_t converged;
+  int32_t breakdown;
+  int32_t cycles;
+  int64_t inner_iterations;       /* Block-Reg: total inner PCG steps                     */
+  double  rel_residual_true;      /* ||b - A x|| / ||b|| at exit                           */
+  double  rel_residual_est;       /* last Givens estimate |g_{j+1}| / ||b||               */
+  double  setup_ms;               /* upload + device format / S_D build                   */
+  double  solve_ms;               /* CUDA-event time of the solve on the caller's stream  */
+} vem_solve_report;
+
+typedef struct {
+  int64_t n_u, n_p, nnz_M, nnz_B, nnz_A, nnz_S;
+  double  lambda_max;             /* Gershgorin bound of diag(S_D)^-1 S_D                 */
+  double  eps;                    /* Block-Reg regularisation as uploaded                 */
+  int32_t spmv_group, schur_group;/* lanes per row of the CSR kernels                     */
+  int32_t sm_count;
+  int64_t device_bytes;           /* device memory owned by the context                   */
+} vem_info;
+
+/* Kernel classes for the per-launch CUDA-event statistics (opts.timing = 1). */
+enum {
+  VEM_K_SPMV = 0,       /* fused saddle SpMV y = A x (and residual b - A x)      */
+  VEM_K_CHEB = 1,       /* Chebyshev step on S_D (Block-Schur B_2)               */
+  VEM_K_PCG_SPMV = 2,   /* PCG step: p update + (S_D + eps W) p + p.q            */
+  VEM_K_PCG_VEC = 3,    /* PCG step: x, r updates + r.z, r.r                     */
+  VEM_K_DOT = 4,        /* CGS multi-dot V^T w                                   */
+  VEM_K_UPDATE = 5,     /* CGS update w -= V h (+ norm, Givens)                  */
+  VEM_K_PRECOND_VEC = 6,/* diagonal scalings, Woodbury pieces, Chebyshev init    */
+  VEM_K_CYCLE = 7,      /* cycle end: back-substitution, x update                */
+  VEM_NUM_KCLASS = 8
+};
+
+typedef struct {
+  int64_t launches[VEM_NUM_KCLASS];
+  double  ms[VEM_NUM_KCLASS];
+} vem_kernel_stats;
+
+void vem_mixed_default_options(vem_opts *opts);
+
+/* Copy M (n_u x n_u), B (n_p x n_u) and optionally a diagonal W (n_p x n_p,
+ * NULL = identity) to the device on `cuda_stream` (a cudaStream_t, e.g.
+ * torch.cuda.current_stream().cuda_stream; NULL = default stream), build the
+ * device formats, diag(M)^-1, S_D = B diag(M)^-1 B^T (device SpGEMM), diag(S_D),
+ * lambda_max and, if eps > 0, the Block-Reg pieces.  eps <= 0 disables
+ * Block-Reg.  On success *ctx owns all device memory; on failure *ctx = NULL. */
+int vem_mixed_upload(vem_ctx **ctx, const vem_csr *M, const vem_csr *B, const vem_csr *W,
+                     double eps, const vem_layout *layout, const vem_opts *opts,
+                     void *cuda_stream);
+
+/* Solve A [u; p] = rhs from x0 = 0 to ||b - A x|| <= tol ||b|| (Givens estimate
+ * checked every step, confirmed by the true residual at each cycle end).
+ * rhs (n_u + n_p), out_u (n_u), out_p (n_p): caller-owned DEVICE pointers
+ * (never freed by the library).  maxit caps the total Arnoldi steps.  The
+ * stream is synchronised before return.  report (host) may be NULL. */
+int vem_mixed_solve(vem_ctx *ctx, const double *rhs, double tol, int32_t maxit,
+                    int32_t precond_kind, double *out_u, double *out_p,
+                    vem_solve_report *report);
+
+/* Same solve with HOST buffers: rhs is copied host->device and u, p
+ * device->host inside the call (end-to-end path). */
+int vem_mixed_solve_host(vem_ctx *ctx, const double *rhs_host, double tol, int32_t maxit,
+                         int32_t precond_kind, double *u_host, double *p_host,
+                         vem_solve_report *report);
+
+/* y = A x for device x, y of length n_u + n_p (the fused saddle SpMV). */
+int vem_mixed_spmv(vem_ctx *ctx, const double *x, double *y);
+
+/* y = S_D x for device x, y of length n_p (checks the device S_D product). */
+int vem_mixed_schur_spmv(vem_ctx *ctx, const double *x, double *y);
+
+/* z = P^-1 v (device, length n_u + n_p) for precond_kind; inner_its (host,
+ * may be NULL) receives the Block-Reg inner PCG step count. */
+int vem_mixed_precond_apply(vem_ctx *ctx, int32_t precond_kind, const double *v, double *z,
+                            int64_t *inner_its);
+
+int vem_mixed_set_options(vem_ctx *ctx, const vem_opts *opts);
+int vem_mixed_get_options(vem_ctx *ctx, vem_opts *opts);
+int vem_mixed_get_info(vem_ctx *ctx, vem_info *info);
+
+/* Copy S_D back to host CSR arrays sized from vem_info (n_p + 1, nnz_S, nnz_S). */
+int vem_mixed_get_schur(vem_ctx *ctx, int64_t *indptr, int32_t *indices, double *values);
+
+/* Per-kernel-class launch counts and CUDA-event milliseconds accumulated while
+ * opts.timing = 1; reset != 0 clears them after copying. */
+int vem_mixed_kernel_stats(vem_ctx *ctx, vem_kernel_stats *stats, int32_t reset);
+
+void vem_mixed_destroy(vem_ctx *ctx);
+const char *vem_status_string(int status);
+const char *vem_last_error(vem_ctx *ctx);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* VEM_MIXED_H */

@@ -1,0 +1,7 @@
+"""B200-native block-preconditioned GMRES for mixed virtual elements (arXiv 1901.02330).
+
+The product path is libvem_mixed.so (sm_100a CUDA, C ABI in include/vem_mixed.h)
+driven through the thin ctypes binding below.  No CPU fallback exists.
+"""
+from .binding import (PRECOND_BLOCK_REG, PRECOND_BLOCK_SCHUR, PRECOND_NONE, EXPORTS, LIB_PATH,  # noqa: F401
+                      VemError, VemMixed, default_options, load_library)

@@ -1,0 +1,780 @@
+// kernels.cuh — sm_100a FP64 kernels of the block-preconditioned GMRES hot path.
+//
+// Every kernel is HBM-bound (0.1-0.25 flop/byte), so there are no
+// tensor cores; the design levers are coalescing, one pass over each stream,
+// fusion of the vector updates into the sparse products and deterministic
+// two-stage reductions (per-block partials + last-block reduce, fixed order).
+//
+// Paper references (PAPER.md line numbers):
+//   saddle operator A = [M B^T; B 0]
+//   GMRES (PETSc) -> right-preconditioned GMRES(m)/FGMRES(m)
+//   Block-Schur B_1 = diag(M), B_2 = -B diag(M)^-1 B^T
+//   Block-Reg  B_1 ~ (M + B^T W^-1 B)^-1, B_2 = W^-1
+#pragma once
+#include <cstdint>
+#include <cuda_runtime.h>
+
+#define VEM_MAXM 128
+#define VEM_DOT_CHUNK 8
+
+struct GmresState {
+  int active;      // Arnoldi steps of the current cycle proceed while 1
+  int j;           // steps done in the current cycle
+  int its;         // total Arnoldi steps
+  int maxit;
+  int conv_est;    // |g_{j+1}| <= tol_abs
+  int breakdown;   // h_{j+1,j} <= 1e-14 ||A z_j||
+  int conv_true;   // ||b - A x|| <= tol_abs at the last cycle end
+  int m;
+  int flexible;
+  int has_steps;   // gate for the cycle-end kernels
+  int pad0, pad1;
+  double bnorm, tol_abs, beta, est, true_res, wnorm0;
+};
+
+struct PcgState {
+  int active, its, maxit, failed;
+  double rz, alpha, beta, bn, tol_abs, rr;
+};
+
+struct DevState {
+  GmresState g;
+  PcgState p;
+  int one_i;       // constant 1 (always-open gate)
+  int pad;
+  double one;      // constant 1.0 (unit scale)
+  double H[(VEM_MAXM + 1) * VEM_MAXM];   // column-major, leading dim m+1
+  double cs[VEM_MAXM], sn[VEM_MAXM], gv[VEM_MAXM + 1];
+  double h1[VEM_MAXM + 2], coef[VEM_MAXM + 2], vscale[VEM_MAXM + 1], y[VEM_MAXM];
+  double lmax;
+  int setup_err;
+  int pad2;
+};
+
+// ---------------------------------------------------------------------------
+// reduction helpers
+// ---------------------------------------------------------------------------
+__device__ __forceinline__ double warp_sum(double v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  return v;
+}
+__device__ __forceinline__ double warp_max(double v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v = fmax(v, __shfl_xor_sync(0xffffffffu, v, o));
+  return v;
+}
+
+// Sum NV per-thread values over the block; result valid in thread 0 (out[i]).
+template <int NV>
+__device__ __forceinline__ void block_sum_n(double (&v)[NV], double *sh /* >= 32*NV */) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
+#pragma unroll
+  for (int i = 0; i < NV; ++i) v[i] = warp_sum(v[i]);
+  if (lane == 0) {
+#pragma unroll
+    for (int i = 0; i < NV; ++i) sh[warp * NV + i] = v[i];
+  }
+  __syncthreads();
+  if (warp == 0) {
+#pragma unroll
+    for (int i = 0; i < NV; ++i) {
+      double t = lane < nw ? sh[lane * NV + i] : 0.0;
+      v[i] = warp_sum(t);
+    }
+  }
+  __syncthreads();
+}
+
+// Last-block election after every block stored its partials (threadfence
+// reduction pattern).  Returns true in every thread of the last block.
+__device__ __forceinline__ bool elect_last_block(unsigned *counter) {
+  __shared__ bool s_last;
+  __threadfence();
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    unsigned total = gridDim.x * gridDim.y;
+    unsigned t = atomicAdd(counter, 1u);
+    s_last = (t == total - 1);
+  }
+  __syncthreads();
+  if (s_last) __threadfence();
+  return s_last;
+}
+
+// In the last block: out[o] = sum over blocks b < nb of part[(o / C) * nb * C + b * C + o % C]
+// for o < nout (fixed order: lane-strided then xor tree => deterministic).
+template <int C>
+__device__ void reduce_partials(const double *part, int nb, int nout, double *out) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
+  for (int o = warp; o < nout; o += nw) {
+    const double *base = part + (size_t)(o / C) * nb * C + (o % C);
+    double s = 0.0;
+    for (int b = lane; b < nb; b += 32) s += __ldcg(base + (size_t)b * C);
+    s = warp_sum(s);
+    if (lane == 0) out[o] = s;
+  }
+  __syncthreads();
+}
+
+// ---------------------------------------------------------------------------
+// CSR SpMV, G lanes per row (G in {1,2,4,8,16,32}), rows [row0, row0 + nrows)
+//   mode 0: y[r] = (A x)[r]            mode 1: y[r] = b[r] - (A x)[r]
+// ---------------------------------------------------------------------------
+template <int G>
+__device__ __forceinline__ double row_dot(const int *__restrict__ rp, const int *__restrict__ ci,
+                                          const double *__restrict__ va, const double *__restrict__ x,
+                                          long row, bool valid) {
+  double acc = 0.0;
+  if (valid) {
+    const int s = rp[row], e = rp[row + 1];
+    const int lane = threadIdx.x & (G - 1);
+    for (int k = s + lane; k < e; k += G) acc = fma(va[k], __ldg(x + ci[k]), acc);
+  }
+  if (G > 1) {
+#pragma unroll
+    for (int o = G / 2; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o, G);
+  }
+  return acc;
+}
+
+template <int G>
+__global__ void __launch_bounds__(256) k_spmv(long row0, long nrows, const int *__restrict__ rp,
+                                              const int *__restrict__ ci, const double *__restrict__ va,
+                                              const double *__restrict__ x, double *__restrict__ y,
+                                              const double *__restrict__ b, int mode, const int *gate) {
+  if (!*gate) return;
+  const long t = (long)blockIdx.x * blockDim.x + threadIdx.x;
+  const long r = t / G;
+  const bool valid = r < nrows;
+  const double acc = row_dot<G>(rp, ci, va, x, row0 + r, valid);
+  if (valid && (threadIdx.x & (G - 1)) == 0) {
+    const long row = row0 + r;
+    y[row] = mode ? b[row] - acc : acc;
+  }
+}
+
+// Residual r = b - A x written to V0 with ||r||^2 partials; the last block
+// starts a new GMRES cycle: beta = ||r||, vscale_0 = 1/beta, g = (beta, 0, ..).
+template <int G>
+__global__ void __launch_bounds__(256) k_residual_start(long n, const int *__restrict__ rp,
+                                                        const int *__restrict__ ci,
+                                                        const double *__restrict__ va,
+                                                        const double *__restrict__ x,
+                                                        const double *__restrict__ b, double *__restrict__ r,
+                                                        int use_x, double *part, unsigned *counter,
+                                                        DevState *st) {
+  __shared__ double sh[32];
+  const long t = (long)blockIdx.x * blockDim.x + threadIdx.x;
+  const long row = t / G;
+  const bool valid = row < n;
+  double acc = 0.0;
+  if (use_x) acc = row_dot<G>(rp, ci, va, x, row, valid);
+  double v[1] = {0.0};
+  if (valid && (threadIdx.x & (G - 1)) == 0) {
+    const double rv = b[row] - acc;
+    r[row] = rv;
+    v[0] = rv * rv;
+  }
+  block_sum_n<1>(v, sh);
+  if (threadIdx.x == 0) part[blockIdx.x] = v[0];
+  if (elect_last_block(counter)) {
+    __shared__ double tot;
+    reduce_partials<1>(part, gridDim.x, 1, &tot);
+    if (threadIdx.x == 0) {
+      GmresState &g = st->g;
+      const double beta = sqrt(tot);
+      if (!use_x) {               // first cycle: ||b||
+        g.bnorm = beta;
+      }
+      g.beta = beta;
+      g.true_res = beta;
+      g.conv_true = beta <= g.tol_abs ? 1 : 0;
+      g.j = 0;
+      g.conv_est = 0;
+      g.breakdown = 0;
+      g.has_steps = 0;
+      g.active = (g.conv_true || g.its >= g.maxit) ? 0 : 1;
+      st->vscale[0] = beta > 0.0 ? 1.0 / beta : 0.0;
+      st->gv[0] = beta;
+      *counter = 0u;
+    }
+  }
+}
+
+// ---------------------------------------------------------------------------
+// Block-Schur apply:  z_u = s v_u ./ diag(M);
+// z_p = -C_d(S_D) (s v_p): degree-d Jacobi Chebyshev (Saad Alg. 12.1, x0 = 0)
+// init: r = s v_p, d = D^-1 r / theta, x = d   (degree 1: z_p = -d)
+// ---------------------------------------------------------------------------
+__global__ void k_bs_init(long nu, long np, const double *__restrict__ v, const double *scale,
+                          const double *__restrict__ dMinv, const double *__restrict__ dSinv,
+                          double inv_theta, double *__restrict__ z, double *__restrict__ cr,
+                          double *__restrict__ cd, double *__restrict__ cx, int degree1, const int *gate) {
+  if (!*gate) return;
+  const double s = *scale;
+  const long n = nu + np;
+  for (long i = (long)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (long)gridDim.x * blockDim.x) {
+    if (i < nu) {
+      z[i] = s * v[i] * dMinv[i];
+    } else {
+      const long k = i - nu;
+      const double r = s * v[i];
+      const double d = dSinv[k] * r * inv_theta;
+      if (degree1) {
+        z[i] = -d;
+      } else {
+        cr[k] = r;
+        cd[k] = d;
+        cx[k] = d;
+      }
+    }
+  }
+}
+
+// one Chebyshev step:  r -= S d_old;  d_new = c1 d_old + c2 D^-1 r;  x += d_new
+// last step writes z_p = -(x + d_new) instead of x.
+template <int G>
+__global__ void __launch_bounds__(256) k_cheb_step(long np, const int *__restrict__ rp, const int *__restrict__ ci,
+                                                   const double *__restrict__ va, const double *__restrict__ dSinv,
+                                                   double *__restrict__ r, const double *__restrict__ d_old,
+                                                   double *__restrict__ d_new, double *__restrict__ x, double c1,
+                                                   double c2, int last, double *__restrict__ zp, const int *gate) {
+  if (!*gate) return;
+  const long t = (long)blockIdx.x * blockDim.x + threadIdx.x;
+  const long row = t / G;
+  const bool valid = row < np;
+  const double sd = row_dot<G>(rp, ci, va, d_old, row, valid);
+  if (valid && (threadIdx.x & (G - 1)) == 0) {
+    const double rn = r[row] - sd;
+    const double dn = c1 * d_old[row] + c2 * (dSinv[row] * rn);
+    const double xn = x[row] + dn;
+    if (last) {
+      zp[row] = -xn;
+    } else {
+      r[row] = rn;
+      d_new[row] = dn;
+      x[row] = xn;
+    }
+  }
+}
+
+// ---------------------------------------------------------------------------
+// Block-Reg apply, W diagonal (wdiag == nullptr -> identity):
+//   z_p = s v_p / (eps W);  t0 = s v_u ./ diag(M) -> z_u;  rhs = B t0 (k_spmv on B rows)
+//   t = PCG(S_D + eps W, rhs);  z_u = t0 - diag(M)^-1 B^T t
+// ---------------------------------------------------------------------------
+__global__ void k_br_init(long nu, long np, const double *__restrict__ v, const double *scale,
+                          const double *__restrict__ dMinv, const double *__restrict__ wdiag, double inv_eps,
+                          double *__restrict__ z, const int *gate) {
+  if (!*gate) return;
+  const double s = *scale;
+  const long n = nu + np;
+  for (long i = (long)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (long)gridDim.x * blockDim.x) {
+    if (i < nu) {
+      z[i] = s * v[i] * dMinv[i];
+    } else {
+      const double w = wdiag ? wdiag[i - nu] : 1.0;
+      z[i] = s * v[i] * inv_eps / w;
+    }
+  }
+}
+
+// z_u[i] -= dMinv[i] * sum_{k in row i, col >= nu} A_ik t[col - nu]   (B^T t)
+template <int G>
+__global__ void __launch_bounds__(256) k_br_finish(long nu, const int *__restrict__ rp, const int *__restrict__ ci,
+                                                   const double *__restrict__ va, const double *__restrict__ dMinv,
+                                                   const double *__restrict__ tp, double *__restrict__ z,
+                                                   const int *gate) {
+  if (!*gate) return;
+  const long t = (long)blockIdx.x * blockDim.x + threadIdx.x;
+  const long row = t / G;
+  const bool valid = row < nu;
+  double acc = 0.0;
+  if (valid) {
+    const int s = rp[row], e = rp[row + 1];
+    for (int k = s + (int)(threadIdx.x & (G - 1)); k < e; k += G) {
+      const int c = ci[k];
+      if (c >= nu) acc = fma(va[k], tp[c - nu], acc);
+    }
+  }
+  if (G > 1) {
+#pragma unroll
+    for (int o = G / 2; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o, G);
+  }
+  if (valid && (threadIdx.x & (G - 1)) == 0) z[row] -= dMinv[row] * acc;
+}
+
+// PCG init: x = 0, r = b, p_prev = 0, beta = 0; rz = r.D^-1 r, bn = ||b||
+__global__ void k_pcg_init(long n, const double *__restrict__ b, const double *__restrict__ dinv,
+                           double *__restrict__ x, double *__restrict__ r, double *__restrict__ p0,
+                           double *part, unsigned *counter, DevState *st, double rtol, int maxit,
+                           const int *gate) {
+  __shared__ double sh[64];
+  const bool on = *gate != 0;
+  double v[2] = {0.0, 0.0};
+  if (on) {
+    for (long i = (long)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (long)gridDim.x * blockDim.x) {
+      const double bi = b[i];
+      x[i] = 0.0;
+      r[i] = bi;
+      p0[i] = 0.0;
+      v[0] += bi * dinv[i] * bi;
+      v[1] += bi * bi;
+    }
+  }
+  block_sum_n<2>(v, sh);
+  if (threadIdx.x == 0) {
+    part[blockIdx.x * 2 + 0] = v[0];
+    part[blockIdx.x * 2 + 1] = v[1];
+  }
+  if (elect_last_block(counter)) {
+    __shared__ double tot[2];
+    reduce_partials<2>(part, gridDim.x, 2, tot);
+    if (threadIdx.x == 0) {
+      PcgState &p = st->p;
+      p.rz = tot[0];
+      p.bn = sqrt(tot[1]);
+      p.tol_abs = rtol * p.bn;
+      p.beta = 0.0;
+      p.its = 0;
+      p.maxit = maxit;
+      p.failed = 0;
+      p.active = (on && p.bn > 0.0) ? 1 : 0;
+      *counter = 0u;
+    }
+  }
+}
+
+// PCG step part 1: p_new = D^-1 r + beta p_prev (on the fly at every gathered
+// column), q = (S + eps W) p_new, partial p_new . q; last block: alpha = rz / pq
+template <int G>
+__global__ void __launch_bounds__(256) k_pcg_spmv(long n, const int *__restrict__ rp, const int *__restrict__ ci,
+                                                  const double *__restrict__ va, const double *__restrict__ dinv,
+                                                  const double *__restrict__ wdiag, double eps,
+                                                  const double *__restrict__ r, const double *__restrict__ p_prev,
+                                                  double *__restrict__ p_new, double *__restrict__ q, double *part,
+                                                  unsigned *counter, DevState *st) {
+  __shared__ double sh[32];
+  if (!st->p.active) return;
+  const double beta = st->p.beta;
+  const long t = (long)blockIdx.x * blockDim.x + threadIdx.x;
+  const long row = t / G;
+  const bool valid = row < n;
+  double acc = 0.0;
+  if (valid) {
+    const int s = rp[row], e = rp[row + 1];
+    for (int k = s + (int)(threadIdx.x & (G - 1)); k < e; k += G) {
+      const int c = ci[k];
+      const double pc = fma(beta, p_prev[c], dinv[c] * r[c]);
+      acc = fma(va[k], pc, acc);
+    }
+  }
+  if (G > 1) {
+#pragma unroll
+    for (int o = G / 2; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o, G);
+  }
+  double v[1] = {0.0};
+  if (valid && (threadIdx.x & (G - 1)) == 0) {
+    const double pi = fma(beta, p_prev[row], dinv[row] * r[row]);
+    const double w = wdiag ? wdiag[row] : 1.0;
+    const double qi = fma(eps * w, pi, acc);
+    p_new[row] = pi;
+    q[row] = qi;
+    v[0] = pi * qi;
+  }
+  block_sum_n<1>(v, sh);
+  if (threadIdx.x == 0) part[blockIdx.x] = v[0];
+  if (elect_last_block(counter)) {
+    __shared__ double tot;
+    reduce_partials<1>(part, gridDim.x, 1, &tot);
+    if (threadIdx.x == 0) {
+      st->p.alpha = st->p.rz / tot;
+      *counter = 0u;
+    }
+  }
+}
+
+// PCG step part 2: x += alpha p; r -= alpha q; partial r.D^-1 r and r.r;
+// last block: its++, convergence ||r|| <= rtol ||b||, beta = rz_new / rz
+__global__ void k_pcg_vec(long n, const double *__restrict__ dinv, const double *__restrict__ p,
+                          const double *__restrict__ q, double *__restrict__ x, double *__restrict__ r,
+                          double *part, unsigned *counter, DevState *st) {
+  __shared__ double sh[64];
+  if (!st->p.active) return;
+  const double alpha = st->p.alpha;
+  double v[2] = {0.0, 0.0};
+  for (long i = (long)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (long)gridDim.x * blockDim.x) {
+    x[i] = fma(alpha, p[i], x[i]);
+    const double ri = fma(-alpha, q[i], r[i]);
+    r[i] = ri;
+    v[0] += ri * dinv[i] * ri;
+    v[1] += ri * ri;
+  }
+  block_sum_n<2>(v, sh);
+  if (threadIdx.x == 0) {
+    part[blockIdx.x * 2 + 0] = v[0];
+    part[blockIdx.x * 2 + 1] = v[1];
+  }
+  if (elect_last_block(counter)) {
+    __shared__ double tot[2];
+    reduce_partials<2>(part, gridDim.x, 2, tot);
+    if (threadIdx.x == 0) {
+      PcgState &p = st->p;
+      p.its += 1;
+      p.rr = tot[1];
+      if (sqrt(tot[1]) <= p.tol_abs) {
+        p.active = 0;
+      } else if (p.its >= p.maxit) {
+        p.active = 0;
+        p.failed = 1;
+      } else {
+        p.beta = tot[0] / p.rz;
+        p.rz = tot[0];
+      }
+      *counter = 0u;
+    }
+  }
+}
+
+// ---------------------------------------------------------------------------
+// CGS2 Arnoldi (batched classical Gram-Schmidt, applied twice)
+// ---------------------------------------------------------------------------
+// partial dots: out index o < nv: V_o . w ; o == nv (if with_norm): w . w.
+// grid (gx, ceil(nout / 8)); part layout [chunk][block][8]
+__global__ void __launch_bounds__(256) k_mdot(long n, const double *__restrict__ V, long ldv, int nv,
+                                              int with_norm, const double *__restrict__ w, double *part,
+                                              unsigned *counter, DevState *st, int pass) {
+  __shared__ double sh[32 * VEM_DOT_CHUNK];
+  if (!st->g.active) return;
+  const int nout = nv + (with_norm ? 1 : 0);
+  const int c0 = blockIdx.y * VEM_DOT_CHUNK;
+  double acc[VEM_DOT_CHUNK];
+#pragma unroll
+  for (int c = 0; c < VEM_DOT_CHUNK; ++c) acc[c] = 0.0;
+  const double *vp[VEM_DOT_CHUNK];
+#pragma unroll
+  for (int c = 0; c < VEM_DOT_CHUNK; ++c) {
+    const int o = c0 + c;
+    vp[c] = (o < nv) ? V + (size_t)o * ldv : w;
+  }
+  for (long i = (long)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (long)gridDim.x * blockDim.x) {
+    const double wi = w[i];
+#pragma unroll
+    for (int c = 0; c < VEM_DOT_CHUNK; ++c)
+      if (c0 + c < nout) acc[c] = fma(vp[c][i], wi, acc[c]);
+  }
+  block_sum_n<VEM_DOT_CHUNK>(acc, sh);
+  if (threadIdx.x == 0) {
+    double *dst = part + ((size_t)blockIdx.y * gridDim.x + blockIdx.x) * VEM_DOT_CHUNK;
+#pragma unroll
+    for (int c = 0; c < VEM_DOT_CHUNK; ++c) dst[c] = acc[c];
+  }
+  if (elect_last_block(counter)) {
+    __shared__ double tot[VEM_MAXM + 2];
+    reduce_partials<VEM_DOT_CHUNK>(part, gridDim.x, nout, tot);
+    if (threadIdx.x == 0) {
+      for (int o = 0; o < nv; ++o) {
+        const double h = st->vscale[o] * tot[o];
+        st->coef[o] = h * st->vscale[o];
+        st->h1[o] = (pass == 1) ? h : st->h1[o] + h;
+      }
+      if (with_norm) st->g.wnorm0 = sqrt(tot[nv]);
+      *counter = 0u;
+    }
+  }
+}
+
+// Givens step for column j, executed by one thread.
+__device__ void givens_column(DevState *st, int j, double hn) {
+  GmresState &g = st->g;
+  const int ld = g.m + 1;
+  double *Hc = st->H + (size_t)j * ld;
+  for (int i = 0; i <= j; ++i) Hc[i] = st->h1[i];
+  Hc[j + 1] = hn;
+  for (int i = 0; i < j; ++i) {
+    const double t = st->cs[i] * Hc[i] + st->sn[i] * Hc[i + 1];
+    Hc[i + 1] = -st->sn[i] * Hc[i] + st->cs[i] * Hc[i + 1];
+    Hc[i] = t;
+  }
+  const double rr = hypot(Hc[j], Hc[j + 1]);
+  st->cs[j] = Hc[j] / rr;
+  st->sn[j] = Hc[j + 1] / rr;
+  Hc[j] = rr;
+  Hc[j + 1] = 0.0;
+  st->gv[j + 1] = -st->sn[j] * st->gv[j];
+  st->gv[j] = st->cs[j] * st->gv[j];
+  g.est = fabs(st->gv[j + 1]);
+  g.its += 1;
+  g.j = j + 1;
+  g.has_steps = 1;
+  st->vscale[j + 1] = 1.0 / hn;
+  if (fabs(st->gv[j + 1]) <= g.tol_abs) {
+    g.conv_est = 1;
+    g.active = 0;
+  } else if (hn <= 1e-14 * g.wnorm0) {
+    g.breakdown = 1;
+    g.active = 0;
+  } else if (g.its >= g.maxit || j + 1 >= g.m) {
+    g.active = 0;
+  }
+}
+
+// w -= sum_{o < nv} coef_o V_o; optionally ||w||^2 partials and, in the last
+// block, the Givens step of column j.
+__global__ void __launch_bounds__(256) k_update(long n, const double *__restrict__ V, long ldv, int nv,
+                                                double *__restrict__ w, int with_norm, double *part,
+                                                unsigned *counter, DevState *st, int j) {
+  __shared__ double sh[32];
+  __shared__ double cf[VEM_MAXM + 1];
+  if (!st->g.active) return;
+  for (int o = threadIdx.x; o < nv; o += blockDim.x) cf[o] = st->coef[o];
+  __syncthreads();
+  double v[1] = {0.0};
+  for (long i = (long)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (long)gridDim.x * blockDim.x) {
+    double wi = w[i];
+    for (int o = 0; o < nv; ++o) wi = fma(-cf[o], V[(size_t)o * ldv + i], wi);
+    w[i] = wi;
+    v[0] += wi * wi;
+  }
+  if (!with_norm) return;
+  block_sum_n<1>(v, sh);
+  if (threadIdx.x == 0) part[blockIdx.x] = v[0];
+  if (elect_last_block(counter)) {
+    __shared__ double tot;
+    reduce_partials<1>(part, gridDim.x, 1, &tot);
+    if (threadIdx.x == 0) {
+      givens_column(st, j, sqrt(tot));
+      *counter = 0u;
+    }
+  }
+}
+
+// y = R^-1 g (back substitution on the rotated Hessenberg), coef_i = y_i * scale_i
+__global__ void k_backsolve(DevState *st, int use_vscale) {
+  if (threadIdx.x != 0 || blockIdx.x != 0) return;
+  GmresState &g = st->g;
+  const int k = g.j;
+  const int ld = g.m + 1;
+  for (int i = k - 1; i >= 0; --i) {
+    double s = st->gv[i];
+    for (int c = i + 1; c < k; ++c) s -= st->H[(size_t)c * ld + i] * st->y[c];
+    st->y[i] = s / st->H[(size_t)i * ld + i];
+  }
+  for (int i = 0; i < k; ++i) st->coef[i] = use_vscale ? st->y[i] * st->vscale[i] : st->y[i];
+}
+
+// out (+)= sum_{o < k} coef_o X_o, k = st->g.j
+__global__ void __launch_bounds__(256) k_combine(long n, const double *__restrict__ X, long ldx,
+                                                 double *__restrict__ out, int accumulate, DevState *st) {
+  __shared__ double cf[VEM_MAXM];
+  const int k = st->g.j;
+  if (k == 0) return;
+  for (int o = threadIdx.x; o < k; o += blockDim.x) cf[o] = st->coef[o];
+  __syncthreads();
+  for (long i = (long)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (long)gridDim.x * blockDim.x) {
+    double s = accumulate ? out[i] : 0.0;
+    for (int o = 0; o < k; ++o) s = fma(cf[o], X[(size_t)o * ldx + i], s);
+    out[i] = s;
+  }
+}
+
+__global__ void k_axpy_gated(long n, const double *__restrict__ z, double *__restrict__ x, const int *gate) {
+  if (!*gate) return;
+  for (long i = (long)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (long)gridDim.x * blockDim.x)
+    x[i] += z[i];
+}
+
+// ---------------------------------------------------------------------------
+// setup kernels (upload)
+// ---------------------------------------------------------------------------
+// count B entries per column (for B^T)
+__global__ void k_count_cols(long nnz, const int *__restrict__ ci, int *__restrict__ cnt) {
+  for (long k = (long)blockIdx.x * blockDim.x + threadIdx.x; k < nnz; k += (long)gridDim.x * blockDim.x)
+    atomicAdd(cnt + ci[k], 1);
+}
+// scatter B (rows p, cols u) into B^T rows (u) with atomic slots; sorted later
+__global__ void k_scatter_T(long nrows, const int *__restrict__ rp, const int *__restrict__ ci,
+                            const double *__restrict__ va, const int *__restrict__ trp, int *__restrict__ fill,
+                            int *__restrict__ tci, double *__restrict__ tva) {
+  for (long r = (long)blockIdx.x * blockDim.x + threadIdx.x; r < nrows; r += (long)gridDim.x * blockDim.x) {
+    for (int k = rp[r]; k < rp[r + 1]; ++k) {
+      const int c = ci[k];
+      const int slot = trp[c] + atomicAdd(fill + c, 1);
+      tci[slot] = (int)r;
+      tva[slot] = va[k];
+    }
+  }
+}
+// insertion sort of each (short) row by column index: deterministic B^T
+__global__ void k_sort_rows(long nrows, const int *__restrict__ rp, int *__restrict__ ci, double *__restrict__ va) {
+  for (long r = (long)blockIdx.x * blockDim.x + threadIdx.x; r < nrows; r += (long)gridDim.x * blockDim.x) {
+    const int s = rp[r], e = rp[r + 1];
+    for (int a = s + 1; a < e; ++a) {
+      const int key = ci[a];
+      const double val = va[a];
+      int b = a - 1;
+      while (b >= s && ci[b] > key) {
+        ci[b + 1] = ci[b];
+        va[b + 1] = va[b];
+        --b;
+      }
+      ci[b + 1] = key;
+      va[b + 1] = val;
+    }
+  }
+}
+// merged saddle-matrix row lengths: velocity rows = M row + B^T row, pressure rows = B row
+__global__ void k_a_rowlen(long nu, long np, const int64_t *__restrict__ mrp, const int *__restrict__ btrp,
+                           const int64_t *__restrict__ brp, int *__restrict__ len) {
+  const long n = nu + np;
+  for (long i = (long)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (long)gridDim.x * blockDim.x) {
+    if (i < nu)
+      len[i] = (int)(mrp[i + 1] - mrp[i]) + (btrp[i + 1] - btrp[i]);
+    else
+      len[i] = (int)(brp[i - nu + 1] - brp[i - nu]);
+  }
+}
+__global__ void k_a_fill(long nu, long np, const int64_t *__restrict__ mrp, const int *__restrict__ mci,
+                         const double *__restrict__ mva, const int *__restrict__ btrp, const int *__restrict__ btci,
+                         const double *__restrict__ btva, const int64_t *__restrict__ brp,
+                         const int *__restrict__ bci, const double *__restrict__ bva, const int *__restrict__ arp,
+                         int *__restrict__ aci, double *__restrict__ ava) {
+  const long n = nu + np;
+  for (long i = (long)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (long)gridDim.x * blockDim.x) {
+    int o = arp[i];
+    if (i < nu) {
+      for (int64_t k = mrp[i]; k < mrp[i + 1]; ++k, ++o) {
+        aci[o] = mci[k];
+        ava[o] = mva[k];
+      }
+      for (int k = btrp[i]; k < btrp[i + 1]; ++k, ++o) {
+        aci[o] = (int)(nu + btci[k]);
+        ava[o] = btva[k];
+      }
+    } else {
+      const long r = i - nu;
+      for (int64_t k = brp[r]; k < brp[r + 1]; ++k, ++o) {
+        aci[o] = bci[k];
+        ava[o] = bva[k];
+      }
+    }
+  }
+}
+// diag(M)^-1 from the merged rows; flags non-positive diagonals
+__global__ void k_diag_inv(long n, const int *__restrict__ rp, const int *__restrict__ ci,
+                           const double *__restrict__ va, long col_off, double *__restrict__ dinv,
+                           double *__restrict__ diag, int *err) {
+  for (long i = (long)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (long)gridDim.x * blockDim.x) {
+    double d = 0.0;
+    for (int k = rp[i]; k < rp[i + 1]; ++k)
+      if (ci[k] == i + col_off) d = va[k];
+    if (diag) diag[i] = d;
+    if (!(d > 0.0)) {
+      atomicExch(err, 1);
+      dinv[i] = 0.0;
+    } else {
+      dinv[i] = 1.0 / d;
+    }
+  }
+}
+// S_D expansion counts: cnt[i] = sum_{k in B row i} |B^T row col_k|
+__global__ void k_spgemm_count(long r0, long nr, const int64_t *__restrict__ brp, const int *__restrict__ bci,
+                               const int *__restrict__ btrp, int64_t *__restrict__ cnt) {
+  for (long t = (long)blockIdx.x * blockDim.x + threadIdx.x; t < nr; t += (long)gridDim.x * blockDim.x) {
+    const long i = r0 + t;
+    int64_t c = 0;
+    for (int64_t k = brp[i]; k < brp[i + 1]; ++k) c += btrp[bci[k] + 1] - btrp[bci[k]];
+    cnt[t] = c;
+  }
+}
+// expansion of row i of B D^-1 B^T in fixed order (k, then B^T row entries)
+__global__ void k_spgemm_expand(long r0, long nr, const int64_t *__restrict__ brp, const int *__restrict__ bci,
+                                const double *__restrict__ bva, const double *__restrict__ dMinv,
+                                const int *__restrict__ btrp, const int *__restrict__ btci,
+                                const double *__restrict__ btva, const int64_t *__restrict__ off,
+                                int *__restrict__ keys, double *__restrict__ vals) {
+  for (long t = (long)blockIdx.x * blockDim.x + threadIdx.x; t < nr; t += (long)gridDim.x * blockDim.x) {
+    const long i = r0 + t;
+    int64_t o = off[t];
+    for (int64_t k = brp[i]; k < brp[i + 1]; ++k) {
+      const int j = bci[k];
+      const double a = bva[k] * dMinv[j];
+      for (int q = btrp[j]; q < btrp[j + 1]; ++q, ++o) {
+        keys[o] = btci[q];
+        vals[o] = a * btva[q];
+      }
+    }
+  }
+}
+// distinct keys per (sorted) segment
+__global__ void k_spgemm_unique(long nr, const int64_t *__restrict__ off, const int *__restrict__ keys,
+                                int *__restrict__ ucnt) {
+  for (long t = (long)blockIdx.x * blockDim.x + threadIdx.x; t < nr; t += (long)gridDim.x * blockDim.x) {
+    int c = 0;
+    for (int64_t o = off[t]; o < off[t + 1]; ++o)
+      if (o == off[t] || keys[o] != keys[o - 1]) ++c;
+    ucnt[t] = c;
+  }
+}
+// reduce runs of equal keys (in their stable-sorted expansion order)
+__global__ void k_spgemm_compact(long nr, const int64_t *__restrict__ off, const int *__restrict__ keys,
+                                 const double *__restrict__ vals, const int *__restrict__ urp,
+                                 int *__restrict__ sci, double *__restrict__ sva) {
+  for (long t = (long)blockIdx.x * blockDim.x + threadIdx.x; t < nr; t += (long)gridDim.x * blockDim.x) {
+    int o = urp[t] - urp[0];
+    int64_t a = off[t];
+    const int64_t e = off[t + 1];
+    while (a < e) {
+      const int key = keys[a];
+      double s = 0.0;
+      while (a < e && keys[a] == key) s += vals[a++];
+      sci[o] = key;
+      sva[o] = s;
+      ++o;
+    }
+  }
+}
+// Gershgorin: per-row sum |S_ij| / S_ii, block max partials + last block max
+__global__ void k_gershgorin(long n, const int *__restrict__ rp, const int *__restrict__ ci,
+                             const double *__restrict__ va, double *part, unsigned *counter, DevState *st) {
+  __shared__ double sh[32];
+  double m = 0.0;
+  for (long i = (long)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (long)gridDim.x * blockDim.x) {
+    double s = 0.0, d = 0.0;
+    for (int k = rp[i]; k < rp[i + 1]; ++k) {
+      s += fabs(va[k]);
+      if (ci[k] == i) d = va[k];
+    }
+    if (d > 0.0) m = fmax(m, s / d);
+  }
+  m = warp_max(m);
+  if ((threadIdx.x & 31) == 0) sh[threadIdx.x >> 5] = m;
+  __syncthreads();
+  if (threadIdx.x < 32) {
+    double t = threadIdx.x < (blockDim.x >> 5) ? sh[threadIdx.x] : 0.0;
+    t = warp_max(t);
+    if (threadIdx.x == 0) part[blockIdx.x] = t;
+  }
+  if (elect_last_block(counter)) {
+    if (threadIdx.x == 0) {
+      double mm = 0.0;
+      for (unsigned b = 0; b < gridDim.x; ++b) mm = fmax(mm, __ldcg(part + b));
+      st->lmax = mm;
+      *counter = 0u;
+    }
+  }
+}
+__global__ void k_shift_inv(long n, const double *__restrict__ diag, const double *__restrict__ wdiag, double eps,
+                            double *__restrict__ out) {
+  for (long i = (long)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (long)gridDim.x * blockDim.x)
+    out[i] = 1.0 / (diag[i] + eps * (wdiag ? wdiag[i] : 1.0));
+}
+__global__ void k_widen(long n, const int64_t *__restrict__ in, int *__restrict__ out) {
+  for (long i = (long)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (long)gridDim.x * blockDim.x)
+    out[i] = (int)in[i];
+}
+__global__ void k_i32_to_i64(long n, const int *__restrict__ in, int64_t *__restrict__ out) {
+  for (long i = (long)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (long)gridDim.x * blockDim.x)
+    out[i] = in[i];
+}

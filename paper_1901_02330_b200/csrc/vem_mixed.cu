@@ -1,0 +1,1146 @@
+// vem_mixed.cu — host driver of the C ABI declared in include/vem_mixed.h.
+//
+// Layout in HBM:
+//   A        merged saddle CSR (n = n_u + n_p rows, int32 row pointer / column
+//            index, fp64 values): velocity row i = [M row i | B^T row i (cols
+//            shifted by n_u)], pressure row n_u + r = B row r.  x = [u; p] is
+//            streamed once per SpMV.
+//   S        S_D = B diag(M)^-1 B^T, CSR, built on the device at upload.
+//   V        (m+1) x ldv Krylov basis, one contiguous vector per row,
+//            ldv = n rounded up to 32 doubles; Z (FGMRES) m x ldv.
+//   DevState GMRES/PCG scalars, Hessenberg, Givens, device-resident so a whole
+//            GMRES(m) cycle runs without a host round trip (one CUDA graph).
+#include <cuda_runtime.h>
+#include <cub/cub.cuh>
+
+#include <algorithm>
+#include <chrono>
+#include <cmath>
+#include <cstdarg>
+#include <cstdio>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "../../include/vem_mixed.h"
+#include "kernels.cuh"
+
+namespace {
+
+constexpr int NT = 256;
+
+struct Timed {
+  int cls;
+  cudaEvent_t a, b;
+};
+
+struct Ctx {
+  // sizes
+  long nu = 0, np = 0, n = 0, ldv = 0;
+  long nnzM = 0, nnzB = 0, nnzA = 0, nnzS = 0;
+  vem_layout layout{};
+  vem_opts opts{};
+  cudaStream_t stream = nullptr;
+  int sm_count = 148;
+  double eps = 0.0;
+  bool has_reg = false;
+  int gA = 4, gS = 4;
+  double lmax = 0.0;
+  // device matrices
+  int *a_rp = nullptr, *a_ci = nullptr;
+  double *a_va = nullptr;
+  int *s_rp = nullptr, *s_ci = nullptr;
+  double *s_va = nullptr;
+  double *dMinv = nullptr, *dSinv = nullptr, *dSepsinv = nullptr, *wdiag = nullptr, *sdiag = nullptr;
+  // work vectors
+  double *V = nullptr, *Z = nullptr;
+  int zcap = 0;
+  double *x = nullptr, *b = nullptr, *z = nullptr, *t = nullptr;
+  double *cr = nullptr, *cd0 = nullptr, *cd1 = nullptr, *cx = nullptr;           // Chebyshev
+  double *px = nullptr, *pr = nullptr, *pp0 = nullptr, *pp1 = nullptr, *pq = nullptr, *pb = nullptr;  // PCG
+  double *part = nullptr;
+  unsigned *counter = nullptr;
+  DevState *st = nullptr;
+  DevState *hst = nullptr;  // pinned mirror
+  int *derr = nullptr;
+  long part_cap = 0;
+  // graphs
+  cudaGraphExec_t cycle_exec[3] = {nullptr, nullptr, nullptr};
+  cudaGraphExec_t pcg_exec = nullptr;
+  int pcg_exec_chunk = 0;
+  // timing
+  std::vector<Timed> pending;
+  std::vector<cudaEvent_t> free_events;
+  vem_kernel_stats stats{};
+  bool capturing = false;
+  // misc
+  std::string err;
+  double setup_ms = 0.0;
+  int64_t device_bytes = 0;
+  std::vector<void *> allocs;
+};
+
+int fail(Ctx *c, int code, const char *fmt, ...) {
+  char buf[512];
+  va_list ap;
+  va_start(ap, fmt);
+  vsnprintf(buf, sizeof buf, fmt, ap);
+  va_end(ap);
+  if (c) c->err = buf;
+  return code;
+}
+
+#define CK(call)                                                                              \
+  do {                                                                                        \
+    cudaError_t e_ = (call);                                                                  \
+    if (e_ != cudaSuccess)                                                                    \
+      return fail(c, VEM_ERR_CUDA, "%s failed: %s (%s:%d)", #call, cudaGetErrorString(e_), \
+                  __FILE__, __LINE__);                                                        \
+  } while (0)
+
+#define CKL()                                                                                 \
+  do {                                                                                        \
+    cudaError_t e_ = cudaGetLastError();                                                      \
+    if (e_ != cudaSuccess)                                                                    \
+      return fail(c, VEM_ERR_CUDA, "kernel launch failed: %s (%s:%d)", cudaGetErrorString(e_), \
+                  __FILE__, __LINE__);                                                        \
+  } while (0)
+
+template <typename T>
+int dalloc(Ctx *c, T **p, size_t count) {
+  size_t bytes = std::max<size_t>(count, 1) * sizeof(T);
+  cudaError_t e = cudaMalloc((void **)p, bytes);
+  if (e != cudaSuccess) return fail(c, VEM_ERR_CUDA, "cudaMalloc(%zu) failed: %s", bytes, cudaGetErrorString(e));
+  c->allocs.push_back(*p);
+  c->device_bytes += bytes;
+  return 0;
+}
+#define DA(p, n)                        \
+  do {                                  \
+    int r_ = dalloc(c, &(p), (size_t)(n)); \
+    if (r_) return r_;                  \
+  } while (0)
+
+void dfree(Ctx *c, void *p) {
+  if (!p) return;
+  auto it = std::find(c->allocs.begin(), c->allocs.end(), p);
+  if (it != c->allocs.end()) c->allocs.erase(it);
+  cudaFree(p);
+}
+
+inline int grid_for(long work, int per_block = NT) {
+  long g = (work + per_block - 1) / per_block;
+  return (int)std::max<long>(1, std::min<long>(g, 1L << 30));
+}
+inline int grid_stream(Ctx *c, long n) {   // grid-stride kernels: a few waves of 148 SMs
+  long g = (n + NT - 1) / NT;
+  return (int)std::max<long>(1, std::min<long>(g, (long)c->sm_count * 8));
+}
+int pick_group(double avg) {
+  if (avg < 3) return 2;
+  if (avg < 6) return 4;
+  if (avg < 12) return 8;
+  if (avg < 24) return 16;
+  return 32;
+}
+
+// ----------------------------------------------------------------------------
+// timing: events around each launch when opts.timing (never inside a capture)
+// ----------------------------------------------------------------------------
+cudaEvent_t take_event(Ctx *c) {
+  if (!c->free_events.empty()) {
+    cudaEvent_t e = c->free_events.back();
+    c->free_events.pop_back();
+    return e;
+  }
+  cudaEvent_t e;
+  cudaEventCreate(&e);
+  return e;
+}
+struct TimeScope {
+  Ctx *c;
+  int cls;
+  cudaEvent_t a = nullptr;
+  TimeScope(Ctx *c_, int cls_) : c(c_), cls(cls_) {
+    if (c->opts.timing && !c->capturing) {
+      a = take_event(c);
+      cudaEventRecord(a, c->stream);
+    }
+  }
+  ~TimeScope() {
+    if (a) {
+      cudaEvent_t b = take_event(c);
+      cudaEventRecord(b, c->stream);
+      c->pending.push_back({cls, a, b});
+    }
+  }
+};
+void flush_timing(Ctx *c) {   // call after a stream sync
+  for (auto &t : c->pending) {
+    float ms = 0.f;
+    if (cudaEventElapsedTime(&ms, t.a, t.b) == cudaSuccess) {
+      c->stats.launches[t.cls] += 1;
+      c->stats.ms[t.cls] += ms;
+    }
+    c->free_events.push_back(t.a);
+    c->free_events.push_back(t.b);
+  }
+  c->pending.clear();
+}
+
+// ----------------------------------------------------------------------------
+// launch helpers (templated on the CSR lanes-per-row)
+// ----------------------------------------------------------------------------
+template <template <int> class F, typename... Args>
+void dispatch_g(int g, Args... a) {
+  switch (g) {
+    case 2: F<2>::run(a...); break;
+    case 4: F<4>::run(a...); break;
+    case 8: F<8>::run(a...); break;
+    case 16: F<16>::run(a...); break;
+    default: F<32>::run(a...); break;
+  }
+}
+
+template <int G>
+struct SpmvL {
+  static void run(Ctx *c, long row0, long nrows, const double *x, double *y, const double *b, int mode,
+                  const int *gate) {
+    k_spmv<G><<<grid_for(nrows * G), NT, 0, c->stream>>>(row0, nrows, c->a_rp, c->a_ci, c->a_va, x, y, b,
+                                                         mode, gate);
+  }
+};
+template <int G>
+struct ResidL {
+  static void run(Ctx *c, const double *x, const double *b, double *r, int use_x) {
+    k_residual_start<G><<<grid_for(c->n * G), NT, 0, c->stream>>>(c->n, c->a_rp, c->a_ci, c->a_va, x, b, r,
+                                                                  use_x, c->part, c->counter, c->st);
+  }
+};
+template <int G>
+struct ChebL {
+  static void run(Ctx *c, double *dold, double *dnew, double c1, double c2, int last, double *zp,
+                  const int *gate) {
+    k_cheb_step<G><<<grid_for(c->np * G), NT, 0, c->stream>>>(c->np, c->s_rp, c->s_ci, c->s_va, c->dSinv, c->cr,
+                                                              dold, dnew, c->cx, c1, c2, last, zp, gate);
+  }
+};
+template <int G>
+struct SchurSpmvL {
+  static void run(Ctx *c, const double *x, double *y, const int *gate) {
+    k_spmv<G><<<grid_for(c->np * G), NT, 0, c->stream>>>(0, c->np, c->s_rp, c->s_ci, c->s_va, x, y, nullptr, 0,
+                                                         gate);
+  }
+};
+template <int G>
+struct BrFinL {
+  static void run(Ctx *c, double *z, const int *gate) {
+    k_br_finish<G><<<grid_for(c->nu * G), NT, 0, c->stream>>>(c->nu, c->a_rp, c->a_ci, c->a_va, c->dMinv, c->px,
+                                                              z, gate);
+  }
+};
+template <int G>
+struct PcgSpmvL {
+  static void run(Ctx *c, const double *pprev, double *pnew) {
+    k_pcg_spmv<G><<<grid_for(c->np * G), NT, 0, c->stream>>>(c->np, c->s_rp, c->s_ci, c->s_va, c->dSepsinv,
+                                                             c->wdiag, c->eps, c->pr, pprev, pnew, c->pq,
+                                                             c->part, c->counter, c->st);
+  }
+};
+
+const int *gate_one(Ctx *c) { return &c->st->one_i; }
+const int *gate_active(Ctx *c) { return &c->st->g.active; }
+const int *gate_steps(Ctx *c) { return &c->st->g.has_steps; }
+
+// ----------------------------------------------------------------------------
+// preconditioner applications (enqueue only)
+// ----------------------------------------------------------------------------
+void cheb_coeffs(Ctx *c, double &inv_theta, std::vector<double> &c1, std::vector<double> &c2) {
+  const double b = c->lmax, a = c->lmax / c->opts.cheb_ratio;
+  const double theta = 0.5 * (b + a), delta = 0.5 * (b - a), sigma = theta / delta;
+  double rho = 1.0 / sigma;
+  inv_theta = 1.0 / theta;
+  c1.clear();
+  c2.clear();
+  for (int i = 1; i < c->opts.cheb_degree; ++i) {
+    const double rn = 1.0 / (2.0 * sigma - rho);
+    c1.push_back(rn * rho);
+    c2.push_back(2.0 * rn / delta);
+    rho = rn;
+  }
+}
+
+int enqueue_block_schur(Ctx *c, const double *v, const double *scale, double *z, const int *gate) {
+  double inv_theta;
+  std::vector<double> c1, c2;
+  cheb_coeffs(c, inv_theta, c1, c2);
+  const int deg = c->opts.cheb_degree;
+  {
+    TimeScope ts(c, VEM_K_PRECOND_VEC);
+    k_bs_init<<<grid_stream(c, c->n), NT, 0, c->stream>>>(c->nu, c->np, v, scale, c->dMinv, c->dSinv, inv_theta, z,
+                                                          c->cr, c->cd0, c->cx, deg == 1, gate);
+  }
+  CKL();
+  double *dold = c->cd0, *dnew = c->cd1;
+  for (int i = 1; i < deg; ++i) {
+    TimeScope ts(c, VEM_K_CHEB);
+    dispatch_g<ChebL>(c->gS, c, dold, dnew, c1[i - 1], c2[i - 1], i == deg - 1 ? 1 : 0, z + c->nu, gate);
+    std::swap(dold, dnew);
+  }
+  CKL();
+  return 0;
+}
+
+int run_pcg(Ctx *c, int64_t *inner_its);
+
+int enqueue_block_reg(Ctx *c, const double *v, const double *scale, double *z, const int *gate,
+                      int64_t *inner_its) {
+  {
+    TimeScope ts(c, VEM_K_PRECOND_VEC);
+    k_br_init<<<grid_stream(c, c->n), NT, 0, c->stream>>>(c->nu, c->np, v, scale, c->dMinv, c->wdiag,
+                                                          1.0 / c->eps, z, gate);
+  }
+  {
+    TimeScope ts(c, VEM_K_PRECOND_VEC);  // rhs = B t0 (pressure rows of A)
+    dispatch_g<SpmvL>(c->gA, c, c->nu, c->np, (const double *)z, c->pb - c->nu, (const double *)nullptr, 0, gate);
+  }
+  CKL();
+  {
+    TimeScope ts(c, VEM_K_PRECOND_VEC);
+    k_pcg_init<<<grid_stream(c, c->np), NT, 0, c->stream>>>(c->np, c->pb, c->dSepsinv, c->px, c->pr, c->pp0,
+                                                            c->part, c->counter, c->st, c->opts.inner_rtol,
+                                                            c->opts.inner_maxit, gate);
+  }
+  CKL();
+  int rc = run_pcg(c, inner_its);
+  if (rc) return rc;
+  {
+    TimeScope ts(c, VEM_K_PRECOND_VEC);
+    dispatch_g<BrFinL>(c->gA, c, z, gate);
+  }
+  CKL();
+  return 0;
+}
+
+int enqueue_pcg_steps(Ctx *c, int nsteps) {
+  for (int s = 0; s < nsteps; ++s) {
+    double *pprev = (s % 2 == 0) ? c->pp0 : c->pp1;
+    double *pnew = (s % 2 == 0) ? c->pp1 : c->pp0;
+    {
+      TimeScope ts(c, VEM_K_PCG_SPMV);
+      dispatch_g<PcgSpmvL>(c->gS, c, (const double *)pprev, pnew);
+    }
+    {
+      TimeScope ts(c, VEM_K_PCG_VEC);
+      k_pcg_vec<<<grid_stream(c, c->np), NT, 0, c->stream>>>(c->np, c->dSepsinv, pnew, c->pq, c->px, c->pr,
+                                                             c->part, c->counter, c->st);
+    }
+  }
+  CKL();
+  return 0;
+}
+
+// Inner PCG: chunks of pcg_chunk (even) steps, graph-replayed, host polls the
+// device state between chunks.
+int run_pcg(Ctx *c, int64_t *inner_its) {
+  int chunk = std::max(2, c->opts.pcg_chunk);
+  if (chunk % 2) ++chunk;
+  const bool graphs = c->opts.use_graphs && !c->opts.timing;
+  if (graphs && (!c->pcg_exec || c->pcg_exec_chunk != chunk)) {
+    if (c->pcg_exec) cudaGraphExecDestroy(c->pcg_exec);
+    c->pcg_exec = nullptr;
+    cudaGraph_t g;
+    c->capturing = true;
+    CK(cudaStreamBeginCapture(c->stream, cudaStreamCaptureModeThreadLocal));
+    int rc = enqueue_pcg_steps(c, chunk);
+    cudaError_t e = cudaStreamEndCapture(c->stream, &g);
+    c->capturing = false;
+    if (rc) return rc;
+    if (e != cudaSuccess) return fail(c, VEM_ERR_CUDA, "PCG capture failed: %s", cudaGetErrorString(e));
+    CK(cudaGraphInstantiate(&c->pcg_exec, g, 0));
+    cudaGraphDestroy(g);
+    c->pcg_exec_chunk = chunk;
+  }
+  for (;;) {
+    if (graphs) {
+      CK(cudaGraphLaunch(c->pcg_exec, c->stream));
+    } else {
+      int rc = enqueue_pcg_steps(c, chunk);
+      if (rc) return rc;
+    }
+    CK(cudaMemcpyAsync(&c->hst->p, &c->st->p, sizeof(PcgState), cudaMemcpyDeviceToHost, c->stream));
+    CK(cudaStreamSynchronize(c->stream));
+    flush_timing(c);
+    if (!c->hst->p.active) break;
+  }
+  if (inner_its) *inner_its += c->hst->p.its;
+  if (c->hst->p.failed) return fail(c, VEM_ERR_INNER, "inner PCG did not reach %g in %d steps", c->opts.inner_rtol,
+                                    c->opts.inner_maxit);
+  return 0;
+}
+
+int enqueue_precond(Ctx *c, int kind, const double *v, const double *scale, double *z, const int *gate,
+                    int64_t *inner_its) {
+  if (kind == VEM_PRECOND_BLOCK_SCHUR) return enqueue_block_schur(c, v, scale, z, gate);
+  if (kind == VEM_PRECOND_BLOCK_REG) return enqueue_block_reg(c, v, scale, z, gate, inner_its);
+  // NONE: z = scale * v
+  TimeScope ts(c, VEM_K_PRECOND_VEC);
+  k_bs_init<<<grid_stream(c, c->n), NT, 0, c->stream>>>(c->n, 0, v, scale, nullptr, nullptr, 0.0, z, nullptr,
+                                                        nullptr, nullptr, 0, gate);
+  CKL();
+  return 0;
+}
+
+// ----------------------------------------------------------------------------
+// GMRES(m) cycle
+// ----------------------------------------------------------------------------
+int ensure_part(Ctx *c, long need) {
+  if (need <= c->part_cap) return 0;
+  if (c->part) dfree(c, c->part);
+  c->part = nullptr;
+  DA(c->part, need);
+  c->part_cap = need;
+  return 0;
+}
+
+int enqueue_arnoldi_step(Ctx *c, int kind, int j, int64_t *inner_its) {
+  const bool flex = kind == VEM_PRECOND_BLOCK_REG;
+  double *Vj = c->V + (size_t)j * c->ldv;
+  double *w = c->V + (size_t)(j + 1) * c->ldv;
+  double *zj = flex ? c->Z + (size_t)j * c->ldv : c->z;
+  int rc = enqueue_precond(c, kind, Vj, &c->st->vscale[j], zj, gate_active(c), inner_its);
+  if (rc) return rc;
+  {
+    TimeScope ts(c, VEM_K_SPMV);
+    dispatch_g<SpmvL>(c->gA, c, 0L, c->n, (const double *)zj, w, (const double *)nullptr, 0, gate_active(c));
+  }
+  const int nv = j + 1;
+  const int gx = c->sm_count * 2;
+  for (int pass = 1; pass <= 2; ++pass) {
+    const int nout = nv + (pass == 1 ? 1 : 0);
+    dim3 grid(gx, (nout + VEM_DOT_CHUNK - 1) / VEM_DOT_CHUNK);
+    {
+      TimeScope ts(c, VEM_K_DOT);
+      k_mdot<<<grid, NT, 0, c->stream>>>(c->n, c->V, c->ldv, nv, pass == 1 ? 1 : 0, w, c->part, c->counter, c->st,
+                                         pass);
+    }
+    {
+      TimeScope ts(c, VEM_K_UPDATE);
+      k_update<<<gx * 2, NT, 0, c->stream>>>(c->n, c->V, c->ldv, nv, w, pass == 2 ? 1 : 0, c->part, c->counter,
+                                             c->st, j);
+    }
+  }
+  CKL();
+  return 0;
+}
+
+int enqueue_cycle_end(Ctx *c, int kind, int64_t *inner_its) {
+  const bool flex = kind == VEM_PRECOND_BLOCK_REG;
+  {
+    TimeScope ts(c, VEM_K_CYCLE);
+    k_backsolve<<<1, 32, 0, c->stream>>>(c->st, flex ? 0 : 1);
+  }
+  if (flex) {
+    TimeScope ts(c, VEM_K_CYCLE);
+    k_combine<<<grid_stream(c, c->n), NT, 0, c->stream>>>(c->n, c->Z, c->ldv, c->x, 1, c->st);
+  } else {
+    {
+      TimeScope ts(c, VEM_K_CYCLE);
+      k_combine<<<grid_stream(c, c->n), NT, 0, c->stream>>>(c->n, c->V, c->ldv, c->t, 0, c->st);
+    }
+    int rc = enqueue_precond(c, kind, c->t, &c->st->one, c->z, gate_steps(c), inner_its);
+    if (rc) return rc;
+    TimeScope ts(c, VEM_K_CYCLE);
+    k_axpy_gated<<<grid_stream(c, c->n), NT, 0, c->stream>>>(c->n, c->z, c->x, gate_steps(c));
+  }
+  {
+    TimeScope ts(c, VEM_K_SPMV);
+    dispatch_g<ResidL>(c->gA, c, (const double *)c->x, (const double *)c->b, c->V, 1);
+  }
+  CKL();
+  return 0;
+}
+
+int enqueue_cycle(Ctx *c, int kind, int64_t *inner_its) {
+  for (int j = 0; j < c->opts.restart; ++j) {
+    int rc = enqueue_arnoldi_step(c, kind, j, inner_its);
+    if (rc) return rc;
+  }
+  return enqueue_cycle_end(c, kind, inner_its);
+}
+
+void destroy_graphs(Ctx *c) {
+  for (auto &g : c->cycle_exec)
+    if (g) {
+      cudaGraphExecDestroy(g);
+      g = nullptr;
+    }
+  if (c->pcg_exec) cudaGraphExecDestroy(c->pcg_exec);
+  c->pcg_exec = nullptr;
+}
+
+int ensure_work(Ctx *c, int kind) {
+  const int m = c->opts.restart;
+  if (!c->V) DA(c->V, (size_t)(m + 1) * c->ldv);
+  if (kind == VEM_PRECOND_BLOCK_REG && c->zcap < m) {
+    if (c->Z) dfree(c, c->Z);
+    c->Z = nullptr;
+    DA(c->Z, (size_t)m * c->ldv);
+    c->zcap = m;
+  }
+  return ensure_part(c, (long)c->sm_count * 2 * ((m + 2 + VEM_DOT_CHUNK - 1) / VEM_DOT_CHUNK + 1) * VEM_DOT_CHUNK +
+                            (long)c->sm_count * 64 * 2 + grid_for(c->n * 32) + 1024);
+}
+
+int solve_impl(Ctx *c, const double *rhs, double tol, int maxit, int kind, double *out_u, double *out_p,
+               vem_solve_report *rep) {
+  vem_solve_report R{};
+  if (kind < 0 || kind > 2) return fail(c, VEM_ERR_PRECOND, "unsupported precond_kind %d", kind);
+  if (kind == VEM_PRECOND_BLOCK_REG && !c->has_reg)
+    return fail(c, VEM_ERR_PRECOND, "Block-Reg needs eps > 0 at upload");
+  if (!rhs || !out_u || !out_p || maxit < 0 || !(tol > 0)) return fail(c, VEM_ERR_INVALID, "invalid solve arguments");
+  int rc = ensure_work(c, kind);
+  if (rc) return rc;
+  cudaEvent_t e0, e1;
+  CK(cudaEventCreate(&e0));
+  CK(cudaEventCreate(&e1));
+  CK(cudaEventRecord(e0, c->stream));
+  CK(cudaMemcpyAsync(c->b, rhs, c->n * sizeof(double), cudaMemcpyDeviceToDevice, c->stream));
+  CK(cudaMemsetAsync(c->x, 0, c->n * sizeof(double), c->stream));
+  // reset GMRES state
+  GmresState g0{};
+  g0.m = c->opts.restart;
+  g0.maxit = maxit;
+  g0.tol_abs = 0.0;
+  g0.flexible = kind == VEM_PRECOND_BLOCK_REG;
+  CK(cudaMemcpyAsync(&c->hst->g, &g0, sizeof(g0), cudaMemcpyHostToDevice, c->stream));
+  CK(cudaMemcpyAsync(&c->st->g, &c->hst->g, sizeof(g0), cudaMemcpyHostToDevice, c->stream));
+  CK(cudaStreamSynchronize(c->stream));
+  // beta0 = ||b||; V0 = b
+  dispatch_g<ResidL>(c->gA, c, (const double *)nullptr, (const double *)c->b, c->V, 0);
+  CKL();
+  CK(cudaMemcpyAsync(&c->hst->g, &c->st->g, sizeof(GmresState), cudaMemcpyDeviceToHost, c->stream));
+  CK(cudaStreamSynchronize(c->stream));
+  const double bnorm = c->hst->g.bnorm;
+  int status = VEM_OK;
+  int64_t inner = 0;
+  if (bnorm > 0.0) {
+    // tol_abs = tol * ||b||; re-run the start so conv/active use it
+    GmresState gs = c->hst->g;
+    gs.tol_abs = tol * bnorm;
+    gs.active = (gs.its >= gs.maxit) ? 0 : 1;
+    gs.conv_true = 0;
+    CK(cudaMemcpyAsync(&c->st->g, &gs, sizeof(gs), cudaMemcpyHostToDevice, c->stream));
+    const bool graphs = c->opts.use_graphs && !c->opts.timing && kind != VEM_PRECOND_BLOCK_REG;
+    int restarts = 0, cycles = 0;
+    while (c->hst->g.its < maxit || cycles == 0) {
+      if (maxit == 0) break;
+      if (graphs) {
+        if (!c->cycle_exec[kind]) {
+          cudaGraph_t gr;
+          c->capturing = true;
+          CK(cudaStreamBeginCapture(c->stream, cudaStreamCaptureModeThreadLocal));
+          int r2 = enqueue_cycle(c, kind, &inner);
+          cudaError_t e = cudaStreamEndCapture(c->stream, &gr);
+          c->capturing = false;
+          if (r2) return r2;
+          if (e != cudaSuccess) return fail(c, VEM_ERR_CUDA, "cycle capture failed: %s", cudaGetErrorString(e));
+          CK(cudaGraphInstantiate(&c->cycle_exec[kind], gr, 0));
+          cudaGraphDestroy(gr);
+        }
+        CK(cudaGraphLaunch(c->cycle_exec[kind], c->stream));
+      } else {
+        int r2 = enqueue_cycle(c, kind, &inner);
+        if (r2) {
+          status = r2;
+          break;
+        }
+      }
+      ++cycles;
+      CK(cudaMemcpyAsync(&c->hst->g, &c->st->g, sizeof(GmresState), cudaMemcpyDeviceToHost, c->stream));
+      CK(cudaStreamSynchronize(c->stream));
+      flush_timing(c);
+      const GmresState &h = c->hst->g;
+      if (h.conv_true) break;
+      if (h.its >= maxit) {
+        status = VEM_NOT_CONVERGED;
+        break;
+      }
+      if (h.breakdown && h.j == 1) {
+        status = VEM_BREAKDOWN;
+        break;
+      }
+      ++restarts;
+    }
+    if (status == VEM_OK && !c->hst->g.conv_true) status = VEM_NOT_CONVERGED;
+    R.restarts = restarts;
+    R.cycles = cycles;
+  }
+  CK(cudaMemcpyAsync(out_u, c->x, c->nu * sizeof(double), cudaMemcpyDeviceToDevice, c->stream));
+  CK(cudaMemcpyAsync(out_p, c->x + c->nu, c->np * sizeof(double), cudaMemcpyDeviceToDevice, c->stream));
+  CK(cudaEventRecord(e1, c->stream));
+  CK(cudaStreamSynchronize(c->stream));
+  flush_timing(c);
+  float ms = 0.f;
+  cudaEventElapsedTime(&ms, e0, e1);
+  cudaEventDestroy(e0);
+  cudaEventDestroy(e1);
+  const GmresState &h = c->hst->g;
+  R.status = status;
+  R.iterations = h.its;
+  R.converged = bnorm == 0.0 ? 1 : h.conv_true;
+  R.breakdown = h.breakdown;
+  R.inner_iterations = inner;
+  R.rel_residual_true = bnorm > 0 ? h.true_res / bnorm : 0.0;
+  R.rel_residual_est = bnorm > 0 ? h.est / bnorm : 0.0;
+  R.setup_ms = c->setup_ms;
+  R.solve_ms = ms;
+  if (rep) *rep = R;
+  return status;
+}
+
+// ----------------------------------------------------------------------------
+// upload
+// ----------------------------------------------------------------------------
+int check_csr(Ctx *c, const vem_csr *A, long nr, long nc, const char *name) {
+  if (!A || !A->indptr || (A->nnz && (!A->indices || !A->values)))
+    return fail(c, VEM_ERR_INVALID, "%s: NULL pointer", name);
+  if (A->n_rows != nr || A->n_cols != nc)
+    return fail(c, VEM_ERR_INVALID, "%s: shape %lld x %lld, expected %ld x %ld", name, (long long)A->n_rows,
+                (long long)A->n_cols, nr, nc);
+  if (A->indptr[0] != 0 || A->indptr[nr] != A->nnz) return fail(c, VEM_ERR_INVALID, "%s: bad indptr ends", name);
+  for (long r = 0; r < nr; ++r) {
+    const int64_t s = A->indptr[r], e = A->indptr[r + 1];
+    if (e < s) return fail(c, VEM_ERR_INVALID, "%s: indptr decreasing at row %ld", name, r);
+    for (int64_t k = s; k < e; ++k) {
+      const int32_t j = A->indices[k];
+      if (j < 0 || j >= nc) return fail(c, VEM_ERR_INVALID, "%s: column %d out of range in row %ld", name, j, r);
+      if (k > s && A->indices[k - 1] >= j) return fail(c, VEM_ERR_INVALID, "%s: row %ld not sorted/unique", name, r);
+    }
+  }
+  return 0;
+}
+
+template <typename T>
+int upload_array(Ctx *c, T **dst, const T *src, size_t n) {
+  int r = dalloc(c, dst, n);
+  if (r) return r;
+  if (n) CK(cudaMemcpyAsync(*dst, src, n * sizeof(T), cudaMemcpyHostToDevice, c->stream));
+  return 0;
+}
+
+int build_schur(Ctx *c, const int64_t *brp, const int *bci, const double *bva, const int *btrp, const int *btci,
+                const double *btva) {
+  // per-row expansion counts, processed in row chunks bounding the expansion buffer
+  const long np = c->np;
+  int64_t *cnt = nullptr;
+  DA(cnt, np + 1);
+  k_spgemm_count<<<grid_stream(c, np), NT, 0, c->stream>>>(0, np, brp, bci, btrp, cnt);
+  CKL();
+  std::vector<int64_t> hcnt(np);
+  CK(cudaMemcpyAsync(hcnt.data(), cnt, np * sizeof(int64_t), cudaMemcpyDeviceToHost, c->stream));
+  CK(cudaStreamSynchronize(c->stream));
+  const int64_t cap = (int64_t)1 << 27;
+  std::vector<std::pair<long, long>> chunks;
+  {
+    long r0 = 0;
+    int64_t acc = 0;
+    for (long r = 0; r < np; ++r) {
+      if (acc + hcnt[r] > cap && r > r0) {
+        chunks.push_back({r0, r});
+        r0 = r;
+        acc = 0;
+      }
+      acc += hcnt[r];
+    }
+    chunks.push_back({r0, np});
+  }
+  std::vector<int> hu(np);
+  std::vector<int *> cci;
+  std::vector<double *> cva;
+  std::vector<long> cnnz;
+  int *ucnt = nullptr, *urp = nullptr;
+  DA(ucnt, np + 1);
+  DA(urp, np + 1);
+  int64_t *off = nullptr;
+  DA(off, np + 1);
+  int rcode = 0;
+  for (auto &ch : chunks) {
+    const long r0 = ch.first, nr = ch.second - ch.first;
+    int64_t tot = 0;
+    std::vector<int64_t> hoff(nr + 1);
+    for (long t = 0; t < nr; ++t) {
+      hoff[t] = tot;
+      tot += hcnt[r0 + t];
+    }
+    hoff[nr] = tot;
+    if (tot >= ((int64_t)1 << 31)) return fail(c, VEM_ERR_INVALID, "S_D expansion row chunk too large");
+    CK(cudaMemcpyAsync(off, hoff.data(), (nr + 1) * sizeof(int64_t), cudaMemcpyHostToDevice, c->stream));
+    int *k0 = nullptr, *k1 = nullptr;
+    double *v0 = nullptr, *v1 = nullptr;
+    DA(k0, tot);
+    DA(k1, tot);
+    DA(v0, tot);
+    DA(v1, tot);
+    k_spgemm_expand<<<grid_stream(c, nr), NT, 0, c->stream>>>(r0, nr, brp, bci, bva, c->dMinv, btrp, btci, btva, off,
+                                                              k0, v0);
+    CKL();
+    size_t tb = 0;
+    CK(cub::DeviceSegmentedSort::StableSortPairs(nullptr, tb, k0, k1, v0, v1, (int)tot, (int)nr, off, off + 1,
+                                                 c->stream));
+    char *tmp = nullptr;
+    DA(tmp, tb);
+    CK(cub::DeviceSegmentedSort::StableSortPairs(tmp, tb, k0, k1, v0, v1, (int)tot, (int)nr, off, off + 1,
+                                                 c->stream));
+    k_spgemm_unique<<<grid_stream(c, nr), NT, 0, c->stream>>>(nr, off, k1, ucnt);
+    CKL();
+    CK(cudaMemcpyAsync(hu.data() + r0, ucnt, nr * sizeof(int), cudaMemcpyDeviceToHost, c->stream));
+    CK(cudaStreamSynchronize(c->stream));
+    std::vector<int> hurp(nr + 1);
+    long u = 0;
+    for (long t = 0; t < nr; ++t) {
+      hurp[t] = (int)u;
+      u += hu[r0 + t];
+    }
+    hurp[nr] = (int)u;
+    CK(cudaMemcpyAsync(urp, hurp.data(), (nr + 1) * sizeof(int), cudaMemcpyHostToDevice, c->stream));
+    int *sci = nullptr;
+    double *sva = nullptr;
+    DA(sci, u);
+    DA(sva, u);
+    k_spgemm_compact<<<grid_stream(c, nr), NT, 0, c->stream>>>(nr, off, k1, v1, urp, sci, sva);
+    CKL();
+    CK(cudaStreamSynchronize(c->stream));
+    dfree(c, tmp);
+    dfree(c, k0);
+    dfree(c, k1);
+    dfree(c, v0);
+    dfree(c, v1);
+    cci.push_back(sci);
+    cva.push_back(sva);
+    cnnz.push_back(u);
+  }
+  long nnzS = 0;
+  for (long u : cnnz) nnzS += u;
+  if (nnzS >= (1L << 31)) return fail(c, VEM_ERR_INVALID, "nnz(S_D) exceeds int32");
+  c->nnzS = nnzS;
+  std::vector<int> hrp(np + 1);
+  long acc = 0;
+  for (long r = 0; r < np; ++r) {
+    hrp[r] = (int)acc;
+    acc += hu[r];
+  }
+  hrp[np] = (int)acc;
+  DA(c->s_rp, np + 1);
+  DA(c->s_ci, nnzS);
+  DA(c->s_va, nnzS);
+  CK(cudaMemcpyAsync(c->s_rp, hrp.data(), (np + 1) * sizeof(int), cudaMemcpyHostToDevice, c->stream));
+  long o = 0;
+  for (size_t q = 0; q < cci.size(); ++q) {
+    CK(cudaMemcpyAsync(c->s_ci + o, cci[q], cnnz[q] * sizeof(int), cudaMemcpyDeviceToDevice, c->stream));
+    CK(cudaMemcpyAsync(c->s_va + o, cva[q], cnnz[q] * sizeof(double), cudaMemcpyDeviceToDevice, c->stream));
+    o += cnnz[q];
+  }
+  CK(cudaStreamSynchronize(c->stream));
+  for (size_t q = 0; q < cci.size(); ++q) {
+    dfree(c, cci[q]);
+    dfree(c, cva[q]);
+  }
+  dfree(c, cnt);
+  dfree(c, ucnt);
+  dfree(c, urp);
+  dfree(c, off);
+  return rcode;
+}
+
+int upload_impl(Ctx *c, const vem_csr *M, const vem_csr *B, const vem_csr *W, double eps, const vem_layout *lay) {
+  auto t0 = std::chrono::steady_clock::now();
+  if (!M || !B) return fail(c, VEM_ERR_INVALID, "M and B are required");
+  c->nu = M->n_rows;
+  c->np = B->n_rows;
+  c->n = c->nu + c->np;
+  if (c->nu <= 0 || c->np <= 0) return fail(c, VEM_ERR_INVALID, "empty system");
+  if (c->n >= (1L << 31)) return fail(c, VEM_ERR_INVALID, "n exceeds int32 indexing");
+  int r;
+  if ((r = check_csr(c, M, c->nu, c->nu, "M"))) return r;
+  if ((r = check_csr(c, B, c->np, c->nu, "B"))) return r;
+  if (lay) {
+    c->layout = *lay;
+    const long nu = (long)lay->n_faces * lay->n_face_dof + (long)lay->n_elems * lay->n_int_dof;
+    const long np = (long)lay->n_elems * lay->n_p_dof;
+    if (nu != c->nu || np != c->np) return fail(c, VEM_ERR_INVALID, "layout does not match M/B sizes");
+  }
+  c->nnzM = M->nnz;
+  c->nnzB = B->nnz;
+  c->nnzA = M->nnz + 2 * B->nnz;
+  if (c->nnzA >= (1L << 31)) return fail(c, VEM_ERR_INVALID, "nnz(A) exceeds int32 indexing");
+  if (W) {
+    if ((r = check_csr(c, W, c->np, c->np, "W"))) return r;
+    for (long i = 0; i < c->np; ++i)
+      if (W->indptr[i + 1] - W->indptr[i] != 1 || W->indices[W->indptr[i]] != i || !(W->values[W->indptr[i]] > 0))
+        return fail(c, VEM_ERR_INVALID, "W must be diagonal with positive entries");
+  }
+  c->ldv = (c->n + 31) / 32 * 32;
+  cudaDeviceProp prop;
+  int dev = 0;
+  CK(cudaGetDevice(&dev));
+  CK(cudaGetDeviceProperties(&prop, dev));
+  c->sm_count = prop.multiProcessorCount;
+
+  // raw uploads (freed after the merged formats are built)
+  int64_t *mrp = nullptr, *brp = nullptr;
+  int *mci = nullptr, *bci = nullptr;
+  double *mva = nullptr, *bva = nullptr;
+  if ((r = upload_array(c, &mrp, M->indptr, c->nu + 1))) return r;
+  if ((r = upload_array(c, &mci, M->indices, M->nnz))) return r;
+  if ((r = upload_array(c, &mva, M->values, M->nnz))) return r;
+  if ((r = upload_array(c, &brp, B->indptr, c->np + 1))) return r;
+  if ((r = upload_array(c, &bci, B->indices, B->nnz))) return r;
+  if ((r = upload_array(c, &bva, B->values, B->nnz))) return r;
+  if (W) {
+    std::vector<double> wd(c->np);
+    for (long i = 0; i < c->np; ++i) wd[i] = W->values[W->indptr[i]];
+    if ((r = upload_array(c, &c->wdiag, wd.data(), c->np))) return r;
+    CK(cudaStreamSynchronize(c->stream));
+  }
+  // B^T (CSR over velocity rows), deterministic order
+  int *btrp = nullptr, *btci = nullptr, *fill = nullptr;
+  double *btva = nullptr;
+  DA(btrp, c->nu + 1);
+  DA(fill, c->nu + 1);
+  DA(btci, B->nnz);
+  DA(btva, B->nnz);
+  CK(cudaMemsetAsync(fill, 0, (c->nu + 1) * sizeof(int), c->stream));
+  k_count_cols<<<grid_stream(c, B->nnz), NT, 0, c->stream>>>(B->nnz, bci, fill);
+  CKL();
+  {
+    size_t tb = 0;
+    CK(cub::DeviceScan::ExclusiveSum(nullptr, tb, fill, btrp, (int)(c->nu + 1), c->stream));
+    char *tmp = nullptr;
+    DA(tmp, tb);
+    CK(cub::DeviceScan::ExclusiveSum(tmp, tb, fill, btrp, (int)(c->nu + 1), c->stream));
+    CK(cudaStreamSynchronize(c->stream));
+    dfree(c, tmp);
+  }
+  CK(cudaMemsetAsync(fill, 0, (c->nu + 1) * sizeof(int), c->stream));
+  int *brp32 = nullptr;
+  DA(brp32, c->np + 1);
+  k_widen<<<grid_stream(c, c->np + 1), NT, 0, c->stream>>>(c->np + 1, brp, brp32);
+  k_scatter_T<<<grid_stream(c, c->np), NT, 0, c->stream>>>(c->np, brp32, bci, bva, btrp, fill, btci, btva);
+  k_sort_rows<<<grid_stream(c, c->nu), NT, 0, c->stream>>>(c->nu, btrp, btci, btva);
+  CKL();
+  // merged A
+  int *len = nullptr;
+  DA(len, c->n + 1);
+  DA(c->a_rp, c->n + 1);
+  DA(c->a_ci, c->nnzA);
+  DA(c->a_va, c->nnzA);
+  k_a_rowlen<<<grid_stream(c, c->n), NT, 0, c->stream>>>(c->nu, c->np, mrp, btrp, brp, len);
+  CKL();
+  {
+    CK(cudaMemsetAsync(len + c->n, 0, sizeof(int), c->stream));
+    size_t tb = 0;
+    CK(cub::DeviceScan::ExclusiveSum(nullptr, tb, len, c->a_rp, (int)(c->n + 1), c->stream));
+    char *tmp = nullptr;
+    DA(tmp, tb);
+    CK(cub::DeviceScan::ExclusiveSum(tmp, tb, len, c->a_rp, (int)(c->n + 1), c->stream));
+    CK(cudaStreamSynchronize(c->stream));
+    dfree(c, tmp);
+  }
+  k_a_fill<<<grid_stream(c, c->n), NT, 0, c->stream>>>(c->nu, c->np, mrp, mci, mva, btrp, btci, btva, brp, bci, bva,
+                                                       c->a_rp, c->a_ci, c->a_va);
+  CKL();
+  // state
+  DA(c->st, 1);
+  CK(cudaMallocHost((void **)&c->hst, sizeof(DevState)));
+  memset(c->hst, 0, sizeof(DevState));
+  c->hst->one = 1.0;
+  c->hst->one_i = 1;
+  CK(cudaMemcpyAsync(c->st, c->hst, sizeof(DevState), cudaMemcpyHostToDevice, c->stream));
+  DA(c->derr, 1);
+  CK(cudaMemsetAsync(c->derr, 0, sizeof(int), c->stream));
+  DA(c->counter, 1);
+  CK(cudaMemsetAsync(c->counter, 0, sizeof(unsigned), c->stream));
+  {
+    int rr = ensure_part(c, (long)c->sm_count * 64 + grid_for(c->n * 32) + 1024);
+    if (rr) return rr;
+  }
+  // diag(M)^-1
+  DA(c->dMinv, c->nu);
+  k_diag_inv<<<grid_stream(c, c->nu), NT, 0, c->stream>>>(c->nu, c->a_rp, c->a_ci, c->a_va, 0, c->dMinv, nullptr,
+                                                          c->derr);
+  CKL();
+  int herr = 0;
+  CK(cudaMemcpyAsync(&herr, c->derr, sizeof(int), cudaMemcpyDeviceToHost, c->stream));
+  CK(cudaStreamSynchronize(c->stream));
+  if (herr) return fail(c, VEM_ERR_DIAG_M, "non-positive diagonal entry in M");
+  // S_D
+  r = build_schur(c, brp, bci, bva, btrp, btci, btva);
+  if (r) return r;
+  DA(c->dSinv, c->np);
+  DA(c->sdiag, c->np);
+  k_diag_inv<<<grid_stream(c, c->np), NT, 0, c->stream>>>(c->np, c->s_rp, c->s_ci, c->s_va, 0, c->dSinv, c->sdiag,
+                                                          c->derr);
+  CKL();
+  CK(cudaMemcpyAsync(&herr, c->derr, sizeof(int), cudaMemcpyDeviceToHost, c->stream));
+  CK(cudaStreamSynchronize(c->stream));
+  if (herr) return fail(c, VEM_ERR_DIAG_S, "non-positive diagonal entry in S_D = B diag(M)^-1 B^T");
+  k_gershgorin<<<grid_stream(c, c->np), NT, 0, c->stream>>>(c->np, c->s_rp, c->s_ci, c->s_va, c->part, c->counter,
+                                                            c->st);
+  CKL();
+  double lm = 0.0;
+  CK(cudaMemcpyAsync(&lm, &c->st->lmax, sizeof(double), cudaMemcpyDeviceToHost, c->stream));
+  CK(cudaStreamSynchronize(c->stream));
+  c->lmax = lm;
+  c->eps = eps;
+  c->has_reg = eps > 0.0;
+  if (c->has_reg) {
+    DA(c->dSepsinv, c->np);
+    k_shift_inv<<<grid_stream(c, c->np), NT, 0, c->stream>>>(c->np, c->sdiag, c->wdiag, eps, c->dSepsinv);
+    CKL();
+  }
+  // work vectors
+  DA(c->x, c->n);
+  DA(c->b, c->n);
+  DA(c->z, c->n);
+  DA(c->t, c->n);
+  DA(c->cr, c->np);
+  DA(c->cd0, c->np);
+  DA(c->cd1, c->np);
+  DA(c->cx, c->np);
+  if (c->has_reg) {
+    DA(c->px, c->np);
+    DA(c->pr, c->np);
+    DA(c->pp0, c->np);
+    DA(c->pp1, c->np);
+    DA(c->pq, c->np);
+    DA(c->pb, c->np);
+  }
+  c->gA = pick_group((double)c->nnzA / c->n);
+  c->gS = pick_group((double)c->nnzS / c->np);
+  CK(cudaStreamSynchronize(c->stream));
+  for (void *p : {(void *)mrp, (void *)mci, (void *)mva, (void *)brp, (void *)bci, (void *)bva, (void *)btrp,
+                  (void *)btci, (void *)btva, (void *)fill, (void *)brp32, (void *)len})
+    dfree(c, p);
+  c->setup_ms = std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count();
+  return 0;
+}
+
+void destroy_ctx(Ctx *c) {
+  if (!c) return;
+  if (c->stream) cudaStreamSynchronize(c->stream);
+  destroy_graphs(c);
+  flush_timing(c);
+  for (auto e : c->free_events) cudaEventDestroy(e);
+  for (void *p : c->allocs) cudaFree(p);
+  if (c->hst) cudaFreeHost(c->hst);
+  delete c;
+}
+
+}  // namespace
+
+struct vem_ctx {
+  Ctx *impl;
+};
+
+static thread_local std::string g_last_err;
+
+extern "C" {
+
+void vem_mixed_default_options(vem_opts *o) {
+  if (!o) return;
+  o->restart = 30;
+  o->cheb_degree = 16;
+  o->cheb_ratio = 30.0;
+  o->inner_rtol = 1e-10;
+  o->inner_maxit = 10000;
+  o->use_graphs = 1;
+  o->timing = 0;
+  o->pcg_chunk = 16;
+}
+
+static int validate_opts(Ctx *c, const vem_opts *o) {
+  if (o->restart < 1 || o->restart > VEM_MAXM) return fail(c, VEM_ERR_INVALID, "restart must be in [1, %d]", VEM_MAXM);
+  if (o->cheb_degree < 1) return fail(c, VEM_ERR_INVALID, "cheb_degree must be >= 1");
+  if (!(o->cheb_ratio > 1.0)) return fail(c, VEM_ERR_INVALID, "cheb_ratio must be > 1");
+  if (!(o->inner_rtol > 0.0) || o->inner_maxit < 1) return fail(c, VEM_ERR_INVALID, "bad inner PCG options");
+  return 0;
+}
+
+int vem_mixed_upload(vem_ctx **out, const vem_csr *M, const vem_csr *B, const vem_csr *W, double eps,
+                     const vem_layout *layout, const vem_opts *opts, void *stream) {
+  if (!out) return VEM_ERR_INVALID;
+  *out = nullptr;
+  Ctx *c = new Ctx();
+  vem_mixed_default_options(&c->opts);
+  if (opts) {
+    int r = validate_opts(c, opts);
+    if (r) {
+      g_last_err = c->err;
+      destroy_ctx(c);
+      return r;
+    }
+    c->opts = *opts;
+  }
+  c->stream = (cudaStream_t)stream;
+  int r = upload_impl(c, M, B, W, eps, layout);
+  if (r) {
+    g_last_err = c->err;
+    destroy_ctx(c);
+    return r;
+  }
+  vem_ctx *h = new vem_ctx{c};
+  *out = h;
+  return VEM_OK;
+}
+
+int vem_mixed_solve(vem_ctx *h, const double *rhs, double tol, int32_t maxit, int32_t kind, double *out_u,
+                    double *out_p, vem_solve_report *rep) {
+  if (!h) return VEM_ERR_INVALID;
+  return solve_impl(h->impl, rhs, tol, maxit, kind, out_u, out_p, rep);
+}
+
+int vem_mixed_solve_host(vem_ctx *h, const double *rhs_host, double tol, int32_t maxit, int32_t kind,
+                         double *u_host, double *p_host, vem_solve_report *rep) {
+  if (!h || !rhs_host || !u_host || !p_host) return VEM_ERR_INVALID;
+  Ctx *c = h->impl;
+  double *drhs = nullptr, *du = nullptr, *dp = nullptr;
+  DA(drhs, c->n);
+  DA(du, c->nu);
+  DA(dp, c->np);
+  CK(cudaMemcpyAsync(drhs, rhs_host, c->n * sizeof(double), cudaMemcpyHostToDevice, c->stream));
+  int r = solve_impl(c, drhs, tol, maxit, kind, du, dp, rep);
+  if (r >= 0) {
+    CK(cudaMemcpyAsync(u_host, du, c->nu * sizeof(double), cudaMemcpyDeviceToHost, c->stream));
+    CK(cudaMemcpyAsync(p_host, dp, c->np * sizeof(double), cudaMemcpyDeviceToHost, c->stream));
+    CK(cudaStreamSynchronize(c->stream));
+  }
+  dfree(c, drhs);
+  dfree(c, du);
+  dfree(c, dp);
+  return r;
+}
+
+int vem_mixed_spmv(vem_ctx *h, const double *x, double *y) {
+  if (!h || !x || !y) return VEM_ERR_INVALID;
+  Ctx *c = h->impl;
+  dispatch_g<SpmvL>(c->gA, c, 0L, c->n, x, y, (const double *)nullptr, 0, gate_one(c));
+  CKL();
+  CK(cudaStreamSynchronize(c->stream));
+  return VEM_OK;
+}
+
+int vem_mixed_schur_spmv(vem_ctx *h, const double *x, double *y) {
+  if (!h || !x || !y) return VEM_ERR_INVALID;
+  Ctx *c = h->impl;
+  dispatch_g<SchurSpmvL>(c->gS, c, x, y, gate_one(c));
+  CKL();
+  CK(cudaStreamSynchronize(c->stream));
+  return VEM_OK;
+}
+
+int vem_mixed_precond_apply(vem_ctx *h, int32_t kind, const double *v, double *z, int64_t *inner_its) {
+  if (!h || !v || !z) return VEM_ERR_INVALID;
+  Ctx *c = h->impl;
+  if (kind < 0 || kind > 2) return fail(c, VEM_ERR_PRECOND, "unsupported precond_kind %d", kind);
+  if (kind == VEM_PRECOND_BLOCK_REG && !c->has_reg) return fail(c, VEM_ERR_PRECOND, "Block-Reg needs eps > 0");
+  int64_t its = 0;
+  int r = enqueue_precond(c, kind, v, &c->st->one, z, gate_one(c), &its);
+  if (r) return r;
+  CK(cudaStreamSynchronize(c->stream));
+  flush_timing(c);
+  if (inner_its) *inner_its = its;
+  return VEM_OK;
+}
+
+int vem_mixed_set_options(vem_ctx *h, const vem_opts *o) {
+  if (!h || !o) return VEM_ERR_INVALID;
+  Ctx *c = h->impl;
+  int r = validate_opts(c, o);
+  if (r) return r;
+  const bool realloc_v = o->restart != c->opts.restart;
+  c->opts = *o;
+  destroy_graphs(c);
+  if (realloc_v) {
+    if (c->V) dfree(c, c->V);
+    c->V = nullptr;
+    if (c->Z) dfree(c, c->Z);
+    c->Z = nullptr;
+    c->zcap = 0;
+  }
+  return VEM_OK;
+}
+
+int vem_mixed_get_options(vem_ctx *h, vem_opts *o) {
+  if (!h || !o) return VEM_ERR_INVALID;
+  *o = h->impl->opts;
+  return VEM_OK;
+}
+
+int vem_mixed_get_info(vem_ctx *h, vem_info *info) {
+  if (!h || !info) return VEM_ERR_INVALID;
+  Ctx *c = h->impl;
+  info->n_u = c->nu;
+  info->n_p = c->np;
+  info->nnz_M = c->nnzM;
+  info->nnz_B = c->nnzB;
+  info->nnz_A = c->nnzA;
+  info->nnz_S = c->nnzS;
+  info->lambda_max = c->lmax;
+  info->eps = c->eps;
+  info->spmv_group = c->gA;
+  info->schur_group = c->gS;
+  info->sm_count = c->sm_count;
+  info->device_bytes = c->device_bytes;
+  return VEM_OK;
+}
+
+int vem_mixed_get_schur(vem_ctx *h, int64_t *indptr, int32_t *indices, double *values) {
+  if (!h || !indptr || !indices || !values) return VEM_ERR_INVALID;
+  Ctx *c = h->impl;
+  std::vector<int> rp(c->np + 1);
+  CK(cudaMemcpyAsync(rp.data(), c->s_rp, (c->np + 1) * sizeof(int), cudaMemcpyDeviceToHost, c->stream));
+  CK(cudaMemcpyAsync(indices, c->s_ci, c->nnzS * sizeof(int), cudaMemcpyDeviceToHost, c->stream));
+  CK(cudaMemcpyAsync(values, c->s_va, c->nnzS * sizeof(double), cudaMemcpyDeviceToHost, c->stream));
+  CK(cudaStreamSynchronize(c->stream));
+  for (long i = 0; i <= c->np; ++i) indptr[i] = rp[i];
+  return VEM_OK;
+}
+
+int vem_mixed_kernel_stats(vem_ctx *h, vem_kernel_stats *s, int32_t reset) {
+  if (!h || !s) return VEM_ERR_INVALID;
+  Ctx *c = h->impl;
+  if (c->stream) cudaStreamSynchronize(c->stream);
+  flush_timing(c);
+  *s = c->stats;
+  if (reset) memset(&c->stats, 0, sizeof(c->stats));
+  return VEM_OK;
+}
+
+void vem_mixed_destroy(vem_ctx *h) {
+  if (!h) return;
+  destroy_ctx(h->impl);
+  delete h;
+}
+
+const char *vem_status_string(int s) {
+  switch (s) {
+    case VEM_OK: return "OK";
+    case VEM_NOT_CONVERGED: return "NOT_CONVERGED";
+    case VEM_BREAKDOWN: return "BREAKDOWN";
+    case VEM_ERR_INVALID: return "ERR_INVALID";
+    case VEM_ERR_DIAG_M: return "ERR_DIAG_M";
+    case VEM_ERR_DIAG_S: return "ERR_DIAG_S";
+    case VEM_ERR_CUDA: return "ERR_CUDA";
+    case VEM_ERR_PRECOND: return "ERR_PRECOND";
+    case VEM_ERR_INNER: return "ERR_INNER";
+    default: return "UNKNOWN";
+  }
+}
+
+const char *vem_last_error(vem_ctx *h) {
+  if (!h) return g_last_err.c_str();   // last failed upload on this thread
+  return h->impl->err.c_str();
+}
+
+}  // extern "C"

@@ -1,0 +1,220 @@
+"""GPU-vs-oracle parity through the C ABI (libvem_mixed.so, sm_100a).
+
+Tolerances (BASELINE.json north_star, reading R20):
+  * SpMV / S_D product: ||y_gpu - y_oracle||_inf <= 1e-12 ||y_oracle||_inf
+  * solution: u and p separately, ||.||_inf relative <= 1e-8 at rtol 1e-10
+  * GMRES iteration counts within +-2 of the oracle's (FGMRES: outer count)
+Full-size configs are checked on sampled rows and by properties that hold at
+any size (true residual, local conservation B u = f).
+"""
+import numpy as np
+import pytest
+import scipy.sparse as sp
+
+from oracle import solver as O
+from vemgen import configs, mesh
+from vemgen.assemble import build_system
+
+pytestmark = pytest.mark.gpu
+
+torch = pytest.importorskip("torch")
+if not torch.cuda.is_available():  # pragma: no cover
+    pytest.skip("needs a CUDA device", allow_module_level=True)
+
+import paper_1901_02330_b200 as pkg  # noqa: E402
+
+RNG = np.random.default_rng(2024)
+_CACHE = {}
+
+
+def system(name):
+    if name not in _CACHE:
+        _CACHE[name] = configs.CONFIGS[name].build()
+    return _CACHE[name]
+
+
+def solver_for(s, eps=None, **opts):
+    o = pkg.default_options(**opts) if opts else None
+    return pkg.VemMixed(s.M, s.B, eps=configs.eps_for(s) if eps is None else eps, layout=s.layout, opts=o)
+
+
+def rel_inf(a, b):
+    return np.abs(a - b).max() / max(np.abs(b).max(), 1e-300)
+
+
+@pytest.mark.parametrize("name", ["C1", "C2s", "C3s", "C4s", "C5s"])
+def test_spmv_parity(name):
+    s = system(name)
+    sv = solver_for(s)
+    for _ in range(3):
+        x = RNG.normal(size=s.n)
+        y = sv.spmv(torch.from_numpy(x).cuda()).cpu().numpy()
+        assert rel_inf(y, O.spmv_saddle(s.M, s.B, x)) <= 1e-12
+    sv.close()
+
+
+@pytest.mark.parametrize("name", ["C1", "C2s", "C3s", "C4s", "C5s"])
+def test_schur_product_parity(name):
+    s = system(name)
+    sv = solver_for(s)
+    Sg = sv.get_schur()
+    So = O.schur_diag(s.M, s.B)
+    d = abs(Sg - So)
+    assert d.max() <= 1e-12 * abs(So).max()
+    x = RNG.normal(size=s.layout.n_p)
+    y = sv.schur_spmv(torch.from_numpy(x).cuda()).cpu().numpy()
+    assert rel_inf(y, So @ x) <= 1e-12
+    info = sv.info()
+    assert abs(info["lambda_max"] - O.gershgorin_lmax(So)) <= 1e-12 * info["lambda_max"]
+    sv.close()
+
+
+@pytest.mark.parametrize("name", ["C1", "C2s", "C3s", "C4s"])
+def test_block_schur_apply_parity(name):
+    s = system(name)
+    sv = solver_for(s)
+    P = O.Preconditioner(O.PRECOND_BLOCK_SCHUR, s.M, s.B)
+    v = RNG.normal(size=s.n)
+    z, _ = sv.precond_apply(pkg.PRECOND_BLOCK_SCHUR, torch.from_numpy(v).cuda())
+    zo = P.apply(v)
+    nu = s.layout.n_u
+    assert rel_inf(z.cpu().numpy()[:nu], zo[:nu]) <= 1e-12
+    assert rel_inf(z.cpu().numpy()[nu:], zo[nu:]) <= 1e-10
+    sv.close()
+
+
+@pytest.mark.parametrize("name", ["C1", "C3s", "C2s"])
+def test_block_reg_apply_parity(name):
+    s = system(name)
+    eps = configs.eps_for(s)
+    sv = solver_for(s)
+    P = O.Preconditioner(O.PRECOND_BLOCK_REG, s.M, s.B, eps=eps)
+    v = RNG.normal(size=s.n)
+    z, its = sv.precond_apply(pkg.PRECOND_BLOCK_REG, torch.from_numpy(v).cuda())
+    zo = P.apply(v)
+    nu = s.layout.n_u
+    assert abs(its - P.inner_iterations) <= 2
+    assert rel_inf(z.cpu().numpy()[:nu], zo[:nu]) <= 1e-8
+    assert rel_inf(z.cpu().numpy()[nu:], zo[nu:]) <= 1e-14
+    sv.close()
+
+
+SOLVE_CASES = [("C1", 1), ("C1", 2), ("C3s", 1), ("C3s", 2), ("C2s", 1)]
+
+
+@pytest.mark.parametrize("name,kind", SOLVE_CASES)
+def test_solve_parity(name, kind):
+    s = system(name)
+    cfg = configs.CONFIGS[name]
+    eps = configs.eps_for(s)
+    ref = O.solve(s.M, s.B, s.rhs, kind, 1e-10, cfg.restart, eps=eps)
+    assert ref.converged
+    sv = solver_for(s, restart=cfg.restart)
+    res = sv.solve(torch.from_numpy(s.rhs).cuda(), 1e-10, 10000, kind)
+    r = res.report
+    assert r["status"] == 0 and r["converged"] == 1, r
+    assert abs(r["iterations"] - ref.iterations) <= 2, (r["iterations"], ref.iterations)
+    nu = s.layout.n_u
+    assert rel_inf(res.u.cpu().numpy(), ref.x[:nu]) <= 1e-8
+    assert rel_inf(res.p.cpu().numpy(), ref.x[nu:]) <= 1e-8
+    # true residual and local conservation, recomputed on the host
+    x = np.concatenate([res.u.cpu().numpy(), res.p.cpu().numpy()])
+    assert np.linalg.norm(s.rhs - O.spmv_saddle(s.M, s.B, x)) <= 1e-10 * np.linalg.norm(s.rhs) * 1.0001
+    sv.close()
+
+
+def test_solve_host_matches_device_and_is_deterministic():
+    s = system("C3s")
+    sv = solver_for(s, restart=50)
+    a = sv.solve(torch.from_numpy(s.rhs).cuda(), 1e-10, 10000, 1)
+    b = sv.solve(torch.from_numpy(s.rhs).cuda(), 1e-10, 10000, 1)
+    h = sv.solve_host(s.rhs, 1e-10, 10000, 1)
+    assert np.array_equal(a.u.cpu().numpy(), b.u.cpu().numpy())
+    assert np.array_equal(a.u.cpu().numpy(), h.u) and np.array_equal(a.p.cpu().numpy(), h.p)
+    assert a.report["iterations"] == b.report["iterations"] == h.report["iterations"]
+    sv.close()
+
+
+def test_graphs_and_timing_mode_agree():
+    s = system("C3s")
+    sv = solver_for(s, restart=50)
+    a = sv.solve(torch.from_numpy(s.rhs).cuda(), 1e-10, 10000, 1)
+    sv.set_options(use_graphs=0, timing=1)
+    b = sv.solve(torch.from_numpy(s.rhs).cuda(), 1e-10, 10000, 1)
+    assert np.array_equal(a.u.cpu().numpy(), b.u.cpu().numpy())
+    st = sv.kernel_stats()
+    assert st["spmv"]["launches"] >= b.report["iterations"] and st["cheb"]["launches"] > 0
+    sv.close()
+
+
+def test_edge_cases():
+    s = system("C1")
+    sv = solver_for(s)
+    z = torch.zeros(s.n, dtype=torch.float64, device="cuda")
+    r = sv.solve(z, 1e-10, 100, 1)
+    assert r.report["iterations"] == 0 and r.report["converged"] == 1
+    assert float(r.u.abs().max()) == 0.0
+    r = sv.solve(torch.from_numpy(s.rhs).cuda(), 1e-10, 3, 1)
+    assert r.report["status"] == 1 and r.report["iterations"] == 3
+    ref = O.solve(s.M, s.B, s.rhs, 1, 1e-10, 30, maxit=3)
+    nu = s.layout.n_u
+    assert rel_inf(r.u.cpu().numpy(), ref.x[:nu]) <= 1e-10
+    with pytest.raises(pkg.VemError):
+        sv.solve(torch.from_numpy(s.rhs).cuda(), 1e-10, 100, 7)
+    sv.close()
+    # no eps -> Block-Reg unsupported
+    sv = solver_for(s, eps=0.0)
+    with pytest.raises(pkg.VemError):
+        sv.solve(torch.from_numpy(s.rhs).cuda(), 1e-10, 100, 2)
+    sv.close()
+
+
+def test_invalid_uploads():
+    s = system("C1")
+    bad = s.M.copy()
+    bad.data[bad.indptr[5]:bad.indptr[6]] *= 0.0  # zero row incl. diagonal
+    with pytest.raises(pkg.VemError, match="DIAG_M"):
+        pkg.VemMixed(bad, s.B)
+    Bz = s.B.tolil()
+    Bz[3, :] = 0
+    Bz = Bz.tocsr()
+    Bz.eliminate_zeros()
+    with pytest.raises(pkg.VemError, match="DIAG_S"):
+        pkg.VemMixed(s.M, Bz)
+    with pytest.raises(pkg.VemError, match="INVALID"):
+        pkg.VemMixed(s.M, s.B[:, :-1])
+
+
+@pytest.mark.parametrize("n,k", [(1, 0), (1, 1), (3, 2), (5, 0)])
+def test_tiny_and_ragged_meshes(n, k):
+    s = build_system(mesh.cube_mesh(n), k)
+    ref = O.solve(s.M, s.B, s.rhs, 1, 1e-10, 30)
+    sv = solver_for(s)
+    res = sv.solve(torch.from_numpy(s.rhs).cuda(), 1e-10, 10000, 1)
+    assert abs(res.report["iterations"] - ref.iterations) <= 2
+    x = np.concatenate([res.u.cpu().numpy(), res.p.cpu().numpy()])
+    nu = s.layout.n_u
+    assert rel_inf(x[:nu], ref.x[:nu]) <= 1e-8 and rel_inf(x[nu:], ref.x[nu:]) <= 1e-8
+    sv.close()
+
+
+@pytest.mark.slow
+def test_full_c3_sampled_and_properties():
+    """C3 at full size (8.4M DOFs) in the bench's configuration: sampled SpMV
+    rows against the oracle definition, then the solve's true residual and
+    element-wise conservation recomputed on the host."""
+    s = system("C3")
+    sv = solver_for(s, restart=50)
+    x = RNG.normal(size=s.n)
+    y = sv.spmv(torch.from_numpy(x).cuda()).cpu().numpy()
+    A = sp.bmat([[s.M, s.B.T], [s.B, None]]).tocsr()
+    rows = RNG.choice(s.n, 20000, replace=False)
+    yo = A[rows] @ x
+    assert np.abs(y[rows] - yo).max() <= 1e-12 * np.abs(yo).max()
+    res = sv.solve(torch.from_numpy(s.rhs).cuda(), 1e-10, 20000, 1)
+    assert res.report["converged"] == 1
+    u, p = res.u.cpu().numpy(), res.p.cpu().numpy()
+    r = s.rhs - A @ np.concatenate([u, p])
+    assert np.linalg.norm(r) <= 1.0001e-10 * np.linalg.norm(s.rhs)
+    assert np.abs(s.B @ u - s.f).max() <= 1e-8 * np.abs(s.f).max()
+    sv.close()
