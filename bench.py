@@ -1,0 +1,294 @@
+#!/usr/bin/env python
+"""Benchmark of the hot path: block-preconditioned GMRES on the mixed-VEM
+saddle-point system (BASELINE.json metric: time-to-solution & GMRES iters/s at
+1 B200; SpMV / preconditioner HBM GB/s vs peak).
+
+One step = one vem_mixed_solve of the configured system from x0 = 0 to
+rtol 1e-10 (upload and S_D build happen once, before timing: reported as
+setup_ms).  value = GMRES iterations / s over the K timed steps, all ranks.
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--config C3] [--impl ours|reference]
+
+Multi-GPU: "replicas only" — every rank solves its own copy of
+the system; no collective on the data path.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "time-to-solution & GMRES iters/s at 1 B200; SpMV/precond HBM GB/s vs peak"
+UNIT = "GMRES it/s"
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=3)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--config", default="C3")
+    ap.add_argument("--precond", type=int, default=0, help="0 = the config's first preconditioner")
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--cpu-sample-its", type=int, default=6)
+    ap.add_argument("--graphs", action="store_true", help="time with CUDA graphs instead of per-launch events")
+    return ap.parse_args()
+
+
+def peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            d = json.load(f)
+        return float(d["hbm_gbs"]), "measured"
+    except Exception:
+        return 6650.0, "fallback"
+
+
+class ClockSampler:
+    """nvidia-smi clocks / throttle reasons sampled during the timed region."""
+    Q = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+         "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index=0):
+        self.index = index
+        self.samples = []
+        self._stop = threading.Event()
+        self._t = None
+
+    def _run(self):
+        while not self._stop.is_set():
+            try:
+                out = subprocess.run(["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.Q}",
+                                      "--format=csv,noheader,nounits"], capture_output=True, text=True,
+                                     timeout=5).stdout.strip()
+                if out:
+                    self.samples.append([x.strip() for x in out.split(",")])
+            except Exception:
+                pass
+            self._stop.wait(0.2)
+
+    def __enter__(self):
+        self._t = threading.Thread(target=self._run, daemon=True)
+        self._t.start()
+        return self
+
+    def __exit__(self, *a):
+        self._stop.set()
+        self._t.join(timeout=10)
+
+    def summary(self):
+        if not self.samples:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"]}
+        sm = sorted(float(s[0]) for s in self.samples)
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for s in self.samples for i in range(4) if "Active" in s[2 + i]
+                          and not s[2 + i].startswith("Not")})
+        return {"sm_mhz": sm[len(sm) // 2], "sm_max_mhz": float(self.samples[0][1]), "reasons": reasons,
+                "samples": len(self.samples)}
+
+
+def dist_init(args):
+    ws = int(os.environ.get("WORLD_SIZE", "1"))
+    if ws <= 1:
+        return 0, 1, 0
+    import torch.distributed as dist
+    rank = int(os.environ["RANK"])
+    local = int(os.environ.get("LOCAL_RANK", rank))
+    backend = "nccl" if args.impl == "ours" else "gloo"
+    if backend == "nccl":
+        import torch
+        torch.cuda.set_device(local)
+    dist.init_process_group(backend)
+    return rank, ws, local
+
+
+def cpu_baseline(system, cfg, kind, eps, its):
+    """The oracle as it stands on a bounded sample: `its` GMRES iterations of the
+    same system on the host cores."""
+    import numpy as np
+    from oracle import solver as O
+    try:
+        from threadpoolctl import threadpool_info
+        cores = max([i.get("num_threads", 1) for i in threadpool_info()] + [1])
+    except Exception:
+        cores = 1
+    t0 = time.perf_counter()
+    P = O.Preconditioner(kind, system.M, system.B, eps=eps)
+    t1 = time.perf_counter()
+    res = O.gmres(lambda x: O.spmv_saddle(system.M, system.B, x), P.apply, system.rhs, 1e-10, cfg.restart, its,
+                  P.flexible)
+    t2 = time.perf_counter()
+    return {"value": res.iterations / (t2 - t1), "unit": UNIT, "cores": int(cores), "kind": "oracle",
+            "sample": f"{res.iterations} GMRES iterations of {cfg.name} (precond {kind}) from x0=0, "
+                      f"{t2 - t1:.1f} s (+{t1 - t0:.1f} s preconditioner setup, untimed)",
+            "setup_s": t1 - t0}
+
+
+def run_reference(args):
+    """--impl reference: the CPU oracle as it stands (rank 0 only)."""
+    rank, ws, _ = dist_init(args)
+    if rank != 0:
+        return
+    from vemgen.configs import CONFIGS, eps_for
+    cfg = CONFIGS[args.config]
+    kind = args.precond or cfg.precs[0]
+    s = cfg.build()
+    eps = eps_for(s)
+    vals = []
+    for _ in range(args.warmup):
+        cpu_baseline(s, cfg, kind, eps, 1)
+    t0 = time.perf_counter()
+    tot_its = 0
+    last = None
+    for _ in range(args.steps):
+        last = cpu_baseline(s, cfg, kind, eps, args.cpu_sample_its)
+        vals.append(last["value"])
+        tot_its += args.cpu_sample_its
+    dt = time.perf_counter() - t0
+    value = sum(vals) / len(vals)
+    line = {"impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * dt / args.steps,
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic (seeded vemgen assembly)",
+            "config": {"workload": f"{cfg.name}: {cfg.describe}", "rtol": cfg.rtol, "restart": cfg.restart,
+                       "precond": kind, "n_dofs": s.n},
+            "cpu_baseline": {k: last[k] for k in ("kind", "cores", "sample")} | {"value": value, "unit": UNIT},
+            "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+
+
+def main():
+    args = parse()
+    if args.impl == "reference":
+        return run_reference(args)
+    import numpy as np
+    import torch
+
+    import paper_1901_02330_b200 as pkg
+    from vemgen.configs import CONFIGS, eps_for
+
+    rank, ws, local = dist_init(args)
+    torch.cuda.set_device(local)
+    cfg = CONFIGS[args.config]
+    kind = args.precond or cfg.precs[0]
+    t0 = time.perf_counter()
+    s = cfg.build()
+    t_asm = time.perf_counter() - t0
+    eps = eps_for(s)
+    opts = pkg.default_options(restart=cfg.restart, use_graphs=1 if args.graphs else 0,
+                               timing=0 if args.graphs else 1)
+    t0 = time.perf_counter()
+    sv = pkg.VemMixed(s.M, s.B, eps=eps, layout=s.layout, opts=opts)
+    t_up = time.perf_counter() - t0
+    info = sv.info()
+    rhs_dev = torch.from_numpy(s.rhs).cuda()
+    stream = torch.cuda.current_stream()
+
+    def barrier():
+        if ws > 1:
+            import torch.distributed as dist
+            dist.barrier()
+
+    for _ in range(args.warmup):
+        r = sv.solve(rhs_dev, cfg.rtol, 20000, kind)
+    sv.kernel_stats(reset=True)
+    torch.cuda.synchronize()
+    barrier()
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    reports = []
+    with ClockSampler(local) as clk:
+        e0.record(stream)
+        for _ in range(args.steps):
+            r = sv.solve(rhs_dev, cfg.rtol, 20000, kind)
+            reports.append(r.report)
+        e1.record(stream)
+        torch.cuda.synchronize()
+    barrier()
+    torch.cuda.synchronize()
+    ms = e0.elapsed_time(e1)
+    stats = sv.kernel_stats(reset=True)
+    its = sum(r["iterations"] for r in reports)
+    # max over ranks of the time, sum of the work
+    if ws > 1:
+        import torch.distributed as dist
+        t = torch.tensor([ms, float(its)], dtype=torch.float64, device="cuda")
+        tm = t.clone()
+        dist.all_reduce(tm[:1], op=dist.ReduceOp.MAX)
+        dist.all_reduce(t[1:], op=dist.ReduceOp.SUM)
+        ms, its_all = float(tm[0]), float(t[1])
+    else:
+        its_all = float(its)
+    value = its_all / (ms / 1e3)
+
+    # end to end: host rhs (pinned) -> device -> solve -> u, p back to host, through the C ABI
+    rhs_pin = torch.from_numpy(s.rhs).pin_memory()
+    u_pin = torch.empty(s.layout.n_u, dtype=torch.float64).pin_memory()
+    p_pin = torch.empty(s.layout.n_p, dtype=torch.float64).pin_memory()
+    sv.set_options(timing=0, use_graphs=1)
+    sv.solve_host(rhs_pin.numpy(), cfg.rtol, 20000, kind, u_pin.numpy(), p_pin.numpy())
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    e2e_its = 0
+    for _ in range(args.steps):
+        rh = sv.solve_host(rhs_pin.numpy(), cfg.rtol, 20000, kind, u_pin.numpy(), p_pin.numpy())
+        e2e_its += rh.report["iterations"]
+    e2e_s = time.perf_counter() - t0
+    e2e_graph_its = e2e_its
+
+    hbm, peak_kind = peaks()
+    per = {k: v for k, v in stats.items() if v["launches"]}
+    dom = max(per, key=lambda k: per[k]["ms"]) if per else None
+    roof = None
+    if dom:
+        d = per[dom]
+        ach = d["bytes"] / (d["ms"] / 1e3) / 1e9
+        roof = {"bound": "hbm", "kernel": dom, "achieved": round(ach, 1), "peak": hbm, "unit": "GB/s",
+                "frac": round(ach / hbm, 4), "traffic": None, "peak_source": peak_kind,
+                "bytes_per_launch": d["bytes"] / d["launches"], "avg_launch_us": 1e3 * d["ms"] / d["launches"]}
+    kern = {k: {"launches": v["launches"], "ms": round(v["ms"], 3),
+                "GBps": round(v["bytes"] / max(v["ms"], 1e-9) / 1e6, 1),
+                "share": round(v["ms"] / max(sum(x["ms"] for x in per.values()), 1e-9), 4)}
+            for k, v in per.items()}
+    launches = int(sum(v["launches"] for v in per.values())) if per else None
+    line = {"metric": METRIC, "value": round(value, 2), "unit": UNIT, "n_gpus": ws, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": ms / args.steps, "higher_is_better": True, "scaling": "weak",
+            "vs_baseline": None, "dtype": "f64", "data": "synthetic (seeded vemgen assembly, no dataset)",
+            "config": {"workload": f"{cfg.name}: {cfg.describe}", "n_dofs": s.n, "n_u": s.layout.n_u,
+                       "n_p": s.layout.n_p, "nnz_A": info["nnz_A"], "nnz_S": info["nnz_S"],
+                       "precond": kind, "restart": cfg.restart, "rtol": cfg.rtol,
+                       "iterations_per_solve": [r["iterations"] for r in reports],
+                       "time_to_solution_ms": ms / args.steps,
+                       "rel_residual_true": reports[-1]["rel_residual_true"],
+                       "setup_ms": reports[-1]["setup_ms"], "assembly_s": round(t_asm, 2),
+                       "upload_wall_s": round(t_up, 2), "parallelism": f"replicas x{ws}",
+                       "l2": "inputs larger than L2 (A %.0f MB + Krylov basis %.0f MB)" % (
+                           (12 * info["nnz_A"]) / 1e6, 8 * s.n * (cfg.restart + 1) / 1e6),
+                       "timing": "per-launch CUDA events (library timing mode)" if not args.graphs
+                       else "CUDA graphs"},
+            "roofline": roof, "kernels": kern, "gpu_launches": launches,
+            "e2e": {"value": round(e2e_graph_its / e2e_s, 2), "unit": UNIT,
+                    "h2d_bytes_per_step": 8 * s.n, "d2h_bytes_per_step": 8 * s.n,
+                    "path": "vem_mixed_solve_host (pinned host rhs -> solve -> u, p to host), CUDA graphs"},
+            "clocks": clk.summary()}
+    if rank == 0 and ws == 1 and not args.no_cpu_baseline:
+        line["cpu_baseline"] = cpu_baseline(s, cfg, kind, eps, args.cpu_sample_its)
+        line["cpu_baseline"].pop("setup_s", None)
+    sv.close()
+    if rank == 0:
+        print(json.dumps(line), flush=True)
+    if ws > 1:
+        import torch.distributed as dist
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

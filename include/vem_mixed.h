@@ -73,7 +73,7 @@ typedef struct {
   int32_t restart;        /* m, GMRES(m) restart length (default 30)                      */
   int32_t cheb_degree;    /* d, Chebyshev degree of the Block-Schur B_2 apply (default 16) */
   double  cheb_ratio;     /* lambda_max / lambda_min of the Chebyshev interval (default 30) */
-  double  inner_rtol;     /* Block-Reg inner PCG relative tolerance (default 1e-10)        */
+  double  inner_rtol;     /* Block-Reg inner PCG relative tolerance (default 1e-14)        */
   int32_t inner_maxit;    /* Block-Reg inner PCG iteration cap (default 10000)             */
   int32_t use_graphs;     /* 1: replay GMRES cycles / PCG chunks as CUDA graphs (default)  */
   int32_t timing;         /* 1: time every kernel launch with CUDA events (stats below)    */
@@ -116,9 +116,18 @@ enum {
   VEM_NUM_KCLASS = 8
 };
 
+/* bytes[] is the ALGORITHMIC HBM traffic of the timed launches:
+ *   SPMV      12 nnz(A) + 4 (n+1) + 16 n          (values+indices, row ptr, x once, y)
+ *   CHEB      12 nnz(S) + 4 (n_p+1) + 56 n_p      (S, D^-1, r rw, d_old, d_new, x rw)
+ *   PCG_SPMV  12 nnz(S) + 4 (n_p+1) + 56 n_p      (S, D^-1, W, r, p_prev, p_new, q)
+ *   PCG_VEC   64 n_p                               (D^-1, p, q, x rw, r rw)
+ *   DOT       8 n (nv + 1)                         (nv basis vectors + w)
+ *   UPDATE    8 n (nv + 2)                         (nv basis vectors + w rw)
+ * other classes count the vectors they stream once. */
 typedef struct {
   int64_t launches[VEM_NUM_KCLASS];
   double  ms[VEM_NUM_KCLASS];
+  double  bytes[VEM_NUM_KCLASS];
 } vem_kernel_stats;
 
 void vem_mixed_default_options(vem_opts *opts);

@@ -6,9 +6,10 @@ never by the product package.  Shares no code with the CUDA path.
 Plain fp64 numpy/scipy, written in the order of the paper / SURVEY.md §8(c):
   * spmv_saddle      y = [M x_u + B^T x_p ; B x_u]
   * schur_diag       S_D = B diag(M)^-1 B^T
-  * chebyshev        degree-d Jacobi-preconditioned Chebyshev    (O6; Saad Alg. 12.1)
+  * block_jacobi_inv element-block Jacobi D_B^-1 of S_D (n_p x n_p blocks)  (reading R15)
+  * chebyshev        degree-d block-Jacobi Chebyshev on [2/ratio, 2]       (O6; Saad Alg. 12.1)
   * block_schur      B_1 = diag(M), B_2^-1 ~ -C_d(S_D)           (reading R15)
-  * pcg              Jacobi-PCG from x0 = 0                      (reading R16)
+  * pcg              block-Jacobi PCG from x0 = 0                (reading R16)
   * block_reg        B_2^-1 = (eps W)^-1, B_1^-1 by Woodbury with diag(M)
                      and an inner PCG on S_D + eps W             (reading R16)
   * gmres            right-preconditioned GMRES(m) / FGMRES(m), CGS2 Arnoldi,
@@ -51,14 +52,40 @@ def schur_diag(M, B):
 
 
 def gershgorin_lmax(S):
-    """lambda_max estimate of D_S^-1 S: max_i sum_j |S_ij| / S_ii (O6)."""
+    """Gershgorin bound of diag(S)^-1 S: max_i sum_j |S_ij| / S_ii (reported only)."""
     a = abs(S).sum(axis=1).A1
     return float(np.max(a / S.diagonal()))
 
 
-def chebyshev(S, dinv, v, degree, lmax, ratio):
-    """Degree-`degree` Chebyshev iteration for S x = v, Jacobi preconditioner
-    D_S^-1 = diag(dinv), interval [lmax/ratio, lmax], x0 = 0.  Saad, Iterative
+# lambda_max(D_B^-1 S_D) <= 2 for the element-block Jacobi D_B of S_D = B D^-1 B^T
+# whenever every velocity DOF touches at most two elements (DESIGN.md reading R15):
+# S_D = sum_j b_j b_j^T / d_j, each term a PSD matrix on <= 2 element blocks, and a
+# PSD 2x2-block matrix is bounded by twice its block diagonal.
+LAMBDA_MAX_BLOCK_JACOBI = 2.0
+
+
+def block_jacobi_inv(S, nb):
+    """D_B^-1: inverses of the nb x nb diagonal blocks of S (pressure DOFs are
+    numbered element-major, so block e = rows/cols [e nb, (e+1) nb)).  nb = 1 is
+    point Jacobi."""
+    n = S.shape[0]
+    if nb == 1:
+        return sp.diags(1.0 / S.diagonal()).tocsr()
+    ne = n // nb
+    S = S.tocsr()
+    blocks = np.zeros((ne, nb, nb))
+    for a in range(nb):
+        for b in range(nb):
+            blocks[:, a, b] = np.asarray(S[np.arange(ne) * nb + a, np.arange(ne) * nb + b]).ravel()
+    inv = np.linalg.inv(blocks)
+    r = (np.arange(ne)[:, None, None] * nb + np.arange(nb)[None, :, None]).repeat(nb, axis=2)
+    c = (np.arange(ne)[:, None, None] * nb + np.arange(nb)[None, None, :]).repeat(nb, axis=1)
+    return sp.csr_matrix((inv.ravel(), (r.ravel(), c.ravel())), shape=S.shape)
+
+
+def chebyshev(S, Dinv, v, degree, lmax, ratio):
+    """Degree-`degree` Chebyshev iteration for S x = v, preconditioner D^-1
+    (a matrix: element-block Jacobi), interval [lmax/ratio, lmax], x0 = 0.  Saad, Iterative
     Methods, Alg. 12.1, exactly as SURVEY.md §8(c) O6 writes it:
         theta = (b+a)/2, delta = (b-a)/2, sigma = theta/delta, rho_0 = 1/sigma
         r_0 = v, d_0 = D^-1 r_0 / theta, x = d_0
@@ -75,26 +102,26 @@ def chebyshev(S, dinv, v, degree, lmax, ratio):
     sigma = theta / delta
     rho = 1.0 / sigma
     r = v.copy()
-    d = dinv * r / theta
+    d = (Dinv @ r) / theta
     x = d.copy()
     for _ in range(1, degree):
         r = r - S @ d
         rho_new = 1.0 / (2.0 * sigma - rho)
-        d = rho_new * rho * d + (2.0 * rho_new / delta) * (dinv * r)
+        d = rho_new * rho * d + (2.0 * rho_new / delta) * (Dinv @ r)
         rho = rho_new
         x = x + d
     return x
 
 
-def pcg(A, dinv, b, rtol, maxit):
-    """Jacobi-preconditioned CG from x0 = 0; stops when ||r||_2 <= rtol ||b||_2
-    (Hestenes-Stiefel recurrences).  Returns (x, iterations, converged)."""
+def pcg(A, Dinv, b, rtol, maxit):
+    """Preconditioned CG (preconditioner matrix Dinv) from x0 = 0; stops when
+    ||r||_2 <= rtol ||b||_2 (Hestenes-Stiefel recurrences).  Returns (x, iterations, converged)."""
     x = np.zeros_like(b)
     bn = np.linalg.norm(b)
     if bn == 0.0:
         return x, 0, True
     r = b.copy()
-    z = dinv * r
+    z = Dinv @ r
     p = z.copy()
     rz = r @ z
     for it in range(1, maxit + 1):
@@ -104,7 +131,7 @@ def pcg(A, dinv, b, rtol, maxit):
         r = r - alpha * q
         if np.linalg.norm(r) <= rtol * bn:
             return x, it, True
-        z = dinv * r
+        z = Dinv @ r
         rz_new = r @ z
         beta = rz_new / rz
         rz = rz_new
@@ -120,9 +147,10 @@ class Preconditioner:
     cheb_degree: int = 16
     cheb_ratio: float = 30.0
     eps: float = 0.0
-    inner_rtol: float = 1e-10
+    inner_rtol: float = 1e-14
     inner_maxit: int = 10000
     exact_schur: bool = False          # pins only: B_2^-1 = -S_D^-1 exactly
+    block: int = 1                     # n_p: pressure DOFs per element (element-block Jacobi)
     inner_iterations: int = 0
     inner_failed: bool = False
     _cache: dict = field(default_factory=dict)
@@ -135,12 +163,13 @@ class Preconditioner:
             self.dS = self.SD.diagonal().copy()
             if np.any(self.dS <= 0):
                 raise ValueError("non-positive diag(S_D)")
-            self.lmax = gershgorin_lmax(self.SD)
+            self.DBinv = block_jacobi_inv(self.SD, self.block)
+            self.lmax = LAMBDA_MAX_BLOCK_JACOBI
         if self.kind == PRECOND_BLOCK_REG:
             if self.eps <= 0:
                 raise ValueError("eps must be > 0")
             self.Seps = (self.SD + self.eps * sp.identity(self.SD.shape[0], format="csr")).tocsr()
-            self.dSeps = self.Seps.diagonal().copy()
+            self.DBeps_inv = block_jacobi_inv(self.Seps, self.block)
 
     @property
     def flexible(self) -> bool:
@@ -159,7 +188,7 @@ class Preconditioner:
                     self._cache["lu"] = spl.splu(self.SD.tocsc())
                 zp = -self._cache["lu"].solve(vp)
             else:
-                zp = -chebyshev(self.SD, 1.0 / self.dS, vp, self.cheb_degree, self.lmax, self.cheb_ratio)
+                zp = -chebyshev(self.SD, self.DBinv, vp, self.cheb_degree, self.lmax, self.cheb_ratio)
             return np.concatenate([zu, zp])
         if self.kind == PRECOND_BLOCK_REG:
             # B_2^-1 = (eps W)^-1 with W = I
@@ -167,7 +196,7 @@ class Preconditioner:
             # B_1^-1 = (D + B^T (eps W)^-1 B)^-1 = D^-1 - D^-1 B^T (eps W + B D^-1 B^T)^-1 B D^-1
             t0 = vu / self.dM
             s = self.B @ t0
-            t, its, ok = pcg(self.Seps, 1.0 / self.dSeps, s, self.inner_rtol, self.inner_maxit)
+            t, its, ok = pcg(self.Seps, self.DBeps_inv, s, self.inner_rtol, self.inner_maxit)
             self.inner_iterations += its
             self.inner_failed |= not ok
             zu = t0 - (self.B.T @ t) / self.dM
@@ -280,11 +309,12 @@ def gmres(matvec, precond, b, rtol=1e-10, restart=30, maxit=10000, flexible=Fals
 
 
 def solve(M, B, rhs, precond_kind=PRECOND_BLOCK_SCHUR, rtol=1e-10, restart=30, maxit=10000,
-          eps=0.0, cheb_degree=16, cheb_ratio=30.0, inner_rtol=1e-10, inner_maxit=10000,
-          exact_schur=False):
-    """Oracle counterpart of vem_mixed_upload + vem_mixed_solve."""
+          eps=0.0, cheb_degree=16, cheb_ratio=30.0, inner_rtol=1e-14, inner_maxit=10000,
+          exact_schur=False, block=1):
+    """Oracle counterpart of vem_mixed_upload + vem_mixed_solve; `block` is
+    the number of pressure DOFs per element (layout.n_p_dof)."""
     P = Preconditioner(precond_kind, M, B, cheb_degree, cheb_ratio, eps, inner_rtol, inner_maxit,
-                       exact_schur)
+                       exact_schur, block=block)
     res = gmres(lambda x: spmv_saddle(M, B, x), P.apply, rhs, rtol, restart, maxit, P.flexible)
     res.inner_iterations = P.inner_iterations
     res.inner_failed = P.inner_failed

@@ -63,10 +63,10 @@ class vem_info(C.Structure):
 
 
 class vem_kernel_stats(C.Structure):
-    _fields_ = [("launches", C.c_int64 * 8), ("ms", C.c_double * 8)]
+    _fields_ = [("launches", C.c_int64 * 8), ("ms", C.c_double * 8), ("bytes", C.c_double * 8)]
 
     def as_dict(self):
-        return {k: {"launches": int(self.launches[i]), "ms": float(self.ms[i])}
+        return {k: {"launches": int(self.launches[i]), "ms": float(self.ms[i]), "bytes": float(self.bytes[i])}
                 for i, k in enumerate(KCLASSES)}
 
 

@@ -210,13 +210,16 @@ __global__ void __launch_bounds__(256) k_residual_start(long n, const int *__res
 __global__ void k_bs_init(long nu, long np, const double *__restrict__ v, const double *scale,
                           const double *__restrict__ dMinv, const double *__restrict__ dSinv,
                           double inv_theta, double *__restrict__ z, double *__restrict__ cr,
-                          double *__restrict__ cd, double *__restrict__ cx, int degree1, const int *gate) {
+                          double *__restrict__ cd, double *__restrict__ cx, int degree1, int blockmode,
+                          const int *gate) {
   if (!*gate) return;
   const double s = *scale;
   const long n = nu + np;
   for (long i = (long)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (long)gridDim.x * blockDim.x) {
     if (i < nu) {
-      z[i] = s * v[i] * dMinv[i];
+      z[i] = dMinv ? s * v[i] * dMinv[i] : s * v[i];
+    } else if (blockmode) {
+      cr[i - nu] = s * v[i];
     } else {
       const long k = i - nu;
       const double r = s * v[i];
@@ -770,6 +773,259 @@ __global__ void k_shift_inv(long n, const double *__restrict__ diag, const doubl
   for (long i = (long)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (long)gridDim.x * blockDim.x)
     out[i] = 1.0 / (diag[i] + eps * (wdiag ? wdiag[i] : 1.0));
 }
+// ---------------------------------------------------------------------------
+// element-block Jacobi (reading R15/R16): D_B = n_p x n_p diagonal blocks of S_D
+// (+ eps W), inverted at upload (Gauss-Jordan, partial pivoting), applied by
+// one thread per element.  NB is a compile-time block size (k = 1: 4, k = 2: 10).
+// ---------------------------------------------------------------------------
+template <int NB>
+__global__ void k_block_extract_inv(long ne, const int *__restrict__ rp, const int *__restrict__ ci,
+                                    const double *__restrict__ va, const double *__restrict__ wdiag, double shift,
+                                    double *__restrict__ inv, int *err) {
+  for (long e = (long)blockIdx.x * blockDim.x + threadIdx.x; e < ne; e += (long)gridDim.x * blockDim.x) {
+    double a[NB][2 * NB];
+    for (int i = 0; i < NB; ++i) {
+      for (int j = 0; j < 2 * NB; ++j) a[i][j] = (j - NB == i) ? 1.0 : 0.0;
+      const long row = e * NB + i;
+      for (int k = rp[row]; k < rp[row + 1]; ++k) {
+        const long c = ci[k] - e * NB;
+        if (c >= 0 && c < NB) a[i][c] = va[k];
+      }
+      a[i][i] += shift * (wdiag ? wdiag[row] : 1.0);
+    }
+    bool ok = true;
+    for (int col = 0; col < NB; ++col) {
+      int piv = col;
+      for (int i = col + 1; i < NB; ++i)
+        if (fabs(a[i][col]) > fabs(a[piv][col])) piv = i;
+      if (!(fabs(a[piv][col]) > 0.0)) {
+        ok = false;
+        break;
+      }
+      if (piv != col)
+        for (int j = 0; j < 2 * NB; ++j) {
+          const double t = a[col][j];
+          a[col][j] = a[piv][j];
+          a[piv][j] = t;
+        }
+      const double ip = 1.0 / a[col][col];
+      for (int j = 0; j < 2 * NB; ++j) a[col][j] *= ip;
+      for (int i = 0; i < NB; ++i) {
+        if (i == col) continue;
+        const double f = a[i][col];
+        if (f != 0.0)
+          for (int j = 0; j < 2 * NB; ++j) a[i][j] -= f * a[col][j];
+      }
+    }
+    if (!ok) atomicExch(err, 1);
+    double *o = inv + e * NB * NB;
+    for (int i = 0; i < NB; ++i)
+      for (int j = 0; j < NB; ++j) o[i * NB + j] = ok ? a[i][NB + j] : 0.0;
+  }
+}
+
+template <int NB>
+__device__ __forceinline__ void block_mv(const double *__restrict__ inv, long e, const double (&r)[NB],
+                                         double (&t)[NB]) {
+  const double *b = inv + e * NB * NB;
+#pragma unroll
+  for (int i = 0; i < NB; ++i) {
+    double s = 0.0;
+#pragma unroll
+    for (int j = 0; j < NB; ++j) s = fma(b[i * NB + j], r[j], s);
+    t[i] = s;
+  }
+}
+
+// r_new = r - S d_old (rows), the SpMV half of a block-Jacobi Chebyshev step
+template <int G>
+__global__ void __launch_bounds__(256) k_cheb_resid(long np, const int *__restrict__ rp, const int *__restrict__ ci,
+                                                    const double *__restrict__ va, double *__restrict__ r,
+                                                    const double *__restrict__ d_old, const int *gate) {
+  if (!*gate) return;
+  const long t = (long)blockIdx.x * blockDim.x + threadIdx.x;
+  const long row = t / G;
+  const bool valid = row < np;
+  const double sd = row_dot<G>(rp, ci, va, d_old, row, valid);
+  if (valid && (threadIdx.x & (G - 1)) == 0) r[row] -= sd;
+}
+
+// block half of a Chebyshev step (mode 0) or the init (mode 1: d = D^-1 r * c2, x = d)
+//   d_new = c1 d_old + c2 D_B^-1 r ; x += d_new ; last -> z_p = -x
+template <int NB>
+__global__ void k_cheb_block(long ne, const double *__restrict__ inv, const double *__restrict__ r,
+                             const double *__restrict__ d_old, double *__restrict__ d_new, double *__restrict__ x,
+                             double c1, double c2, int mode, int last, double *__restrict__ zp, const int *gate) {
+  if (!*gate) return;
+  for (long e = (long)blockIdx.x * blockDim.x + threadIdx.x; e < ne; e += (long)gridDim.x * blockDim.x) {
+    double rv[NB], t[NB];
+#pragma unroll
+    for (int i = 0; i < NB; ++i) rv[i] = r[e * NB + i];
+    block_mv<NB>(inv, e, rv, t);
+#pragma unroll
+    for (int i = 0; i < NB; ++i) {
+      const long k = e * NB + i;
+      const double dn = mode ? c2 * t[i] : fma(c1, d_old[k], c2 * t[i]);
+      const double xn = mode ? dn : x[k] + dn;
+      if (last) {
+        zp[k] = -xn;
+      } else {
+        d_new[k] = dn;
+        x[k] = xn;
+      }
+    }
+  }
+}
+
+// block PCG init: x = 0, r = b, p_prev = 0, z = D_B^-1 b; rz = r.z, bn = ||b||
+template <int NB>
+__global__ void k_pcg_init_blk(long ne, const double *__restrict__ inv, const double *__restrict__ b,
+                               double *__restrict__ x, double *__restrict__ r, double *__restrict__ z,
+                               double *__restrict__ p0, double *part, unsigned *counter, DevState *st, double rtol,
+                               int maxit, const int *gate) {
+  __shared__ double sh[64];
+  const bool on = *gate != 0;
+  double v[2] = {0.0, 0.0};
+  if (on) {
+    for (long e = (long)blockIdx.x * blockDim.x + threadIdx.x; e < ne; e += (long)gridDim.x * blockDim.x) {
+      double rv[NB], t[NB];
+#pragma unroll
+      for (int i = 0; i < NB; ++i) rv[i] = b[e * NB + i];
+      block_mv<NB>(inv, e, rv, t);
+#pragma unroll
+      for (int i = 0; i < NB; ++i) {
+        const long k = e * NB + i;
+        x[k] = 0.0;
+        r[k] = rv[i];
+        z[k] = t[i];
+        p0[k] = 0.0;
+        v[0] += rv[i] * t[i];
+        v[1] += rv[i] * rv[i];
+      }
+    }
+  }
+  block_sum_n<2>(v, sh);
+  if (threadIdx.x == 0) {
+    part[blockIdx.x * 2 + 0] = v[0];
+    part[blockIdx.x * 2 + 1] = v[1];
+  }
+  if (elect_last_block(counter)) {
+    __shared__ double tot[2];
+    reduce_partials<2>(part, gridDim.x, 2, tot);
+    if (threadIdx.x == 0) {
+      PcgState &p = st->p;
+      p.rz = tot[0];
+      p.bn = sqrt(tot[1]);
+      p.tol_abs = rtol * p.bn;
+      p.beta = 0.0;
+      p.its = 0;
+      p.maxit = maxit;
+      p.failed = 0;
+      p.active = (on && p.bn > 0.0) ? 1 : 0;
+      *counter = 0u;
+    }
+  }
+}
+
+// block PCG step A: p_new = z + beta p_prev (gathered), q = (S + eps W) p_new, p.q -> alpha
+template <int G>
+__global__ void __launch_bounds__(256) k_pcg_spmv_z(long n, const int *__restrict__ rp, const int *__restrict__ ci,
+                                                    const double *__restrict__ va, const double *__restrict__ wdiag,
+                                                    double eps, const double *__restrict__ z,
+                                                    const double *__restrict__ p_prev, double *__restrict__ p_new,
+                                                    double *__restrict__ q, double *part, unsigned *counter,
+                                                    DevState *st) {
+  __shared__ double sh[32];
+  if (!st->p.active) return;
+  const double beta = st->p.beta;
+  const long t = (long)blockIdx.x * blockDim.x + threadIdx.x;
+  const long row = t / G;
+  const bool valid = row < n;
+  double acc = 0.0;
+  if (valid) {
+    const int s = rp[row], e = rp[row + 1];
+    for (int k = s + (int)(threadIdx.x & (G - 1)); k < e; k += G) {
+      const int c = ci[k];
+      acc = fma(va[k], fma(beta, p_prev[c], z[c]), acc);
+    }
+  }
+  if (G > 1) {
+#pragma unroll
+    for (int o = G / 2; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o, G);
+  }
+  double v[1] = {0.0};
+  if (valid && (threadIdx.x & (G - 1)) == 0) {
+    const double pi = fma(beta, p_prev[row], z[row]);
+    const double w = wdiag ? wdiag[row] : 1.0;
+    const double qi = fma(eps * w, pi, acc);
+    p_new[row] = pi;
+    q[row] = qi;
+    v[0] = pi * qi;
+  }
+  block_sum_n<1>(v, sh);
+  if (threadIdx.x == 0) part[blockIdx.x] = v[0];
+  if (elect_last_block(counter)) {
+    __shared__ double tot;
+    reduce_partials<1>(part, gridDim.x, 1, &tot);
+    if (threadIdx.x == 0) {
+      st->p.alpha = st->p.rz / tot;
+      *counter = 0u;
+    }
+  }
+}
+
+// block PCG step B: x += alpha p; r -= alpha q; z = D_B^-1 r; r.z, r.r -> beta, convergence
+template <int NB>
+__global__ void k_pcg_vec_blk(long ne, const double *__restrict__ inv, const double *__restrict__ p,
+                              const double *__restrict__ q, double *__restrict__ x, double *__restrict__ r,
+                              double *__restrict__ z, double *part, unsigned *counter, DevState *st) {
+  __shared__ double sh[64];
+  if (!st->p.active) return;
+  const double alpha = st->p.alpha;
+  double v[2] = {0.0, 0.0};
+  for (long e = (long)blockIdx.x * blockDim.x + threadIdx.x; e < ne; e += (long)gridDim.x * blockDim.x) {
+    double rv[NB], t[NB];
+#pragma unroll
+    for (int i = 0; i < NB; ++i) {
+      const long k = e * NB + i;
+      x[k] = fma(alpha, p[k], x[k]);
+      rv[i] = fma(-alpha, q[k], r[k]);
+      r[k] = rv[i];
+    }
+    block_mv<NB>(inv, e, rv, t);
+#pragma unroll
+    for (int i = 0; i < NB; ++i) {
+      z[e * NB + i] = t[i];
+      v[0] += rv[i] * t[i];
+      v[1] += rv[i] * rv[i];
+    }
+  }
+  block_sum_n<2>(v, sh);
+  if (threadIdx.x == 0) {
+    part[blockIdx.x * 2 + 0] = v[0];
+    part[blockIdx.x * 2 + 1] = v[1];
+  }
+  if (elect_last_block(counter)) {
+    __shared__ double tot[2];
+    reduce_partials<2>(part, gridDim.x, 2, tot);
+    if (threadIdx.x == 0) {
+      PcgState &pp = st->p;
+      pp.its += 1;
+      pp.rr = tot[1];
+      if (sqrt(tot[1]) <= pp.tol_abs) {
+        pp.active = 0;
+      } else if (pp.its >= pp.maxit) {
+        pp.active = 0;
+        pp.failed = 1;
+      } else {
+        pp.beta = tot[0] / pp.rz;
+        pp.rz = tot[0];
+      }
+      *counter = 0u;
+    }
+  }
+}
+
 __global__ void k_widen(long n, const int64_t *__restrict__ in, int *__restrict__ out) {
   for (long i = (long)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (long)gridDim.x * blockDim.x)
     out[i] = (int)in[i];

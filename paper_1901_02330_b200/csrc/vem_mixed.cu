@@ -31,6 +31,7 @@ constexpr int NT = 256;
 
 struct Timed {
   int cls;
+  double bytes;
   cudaEvent_t a, b;
 };
 
@@ -40,12 +41,17 @@ struct Ctx {
   long nnzM = 0, nnzB = 0, nnzA = 0, nnzS = 0;
   vem_layout layout{};
   vem_opts opts{};
-  cudaStream_t stream = nullptr;
+  cudaStream_t stream = nullptr;       // library-owned non-blocking work stream (capturable)
+  cudaStream_t user_stream = nullptr;  // caller's stream; ordered against `stream` with events
+  cudaEvent_t ev_in = nullptr, ev_out = nullptr;
   int sm_count = 148;
   double eps = 0.0;
   bool has_reg = false;
   int gA = 4, gS = 4;
-  double lmax = 0.0;
+  int nb = 1;                          // pressure DOFs per element (block-Jacobi size)
+  double lmax = 0.0;                   // Gershgorin bound of diag(S)^-1 S (reported)
+  double lmax_cheb = 2.0;              // Chebyshev interval top: lambda_max(D_B^-1 S_D) <= 2 (R15)
+  double *dBinv = nullptr, *dBeinv = nullptr, *pz = nullptr;
   // device matrices
   int *a_rp = nullptr, *a_ci = nullptr;
   double *a_va = nullptr;
@@ -160,8 +166,9 @@ cudaEvent_t take_event(Ctx *c) {
 struct TimeScope {
   Ctx *c;
   int cls;
+  double bytes;
   cudaEvent_t a = nullptr;
-  TimeScope(Ctx *c_, int cls_) : c(c_), cls(cls_) {
+  TimeScope(Ctx *c_, int cls_, double bytes_ = 0.0) : c(c_), cls(cls_), bytes(bytes_) {
     if (c->opts.timing && !c->capturing) {
       a = take_event(c);
       cudaEventRecord(a, c->stream);
@@ -171,7 +178,7 @@ struct TimeScope {
     if (a) {
       cudaEvent_t b = take_event(c);
       cudaEventRecord(b, c->stream);
-      c->pending.push_back({cls, a, b});
+      c->pending.push_back({cls, bytes, a, b});
     }
   }
 };
@@ -181,6 +188,7 @@ void flush_timing(Ctx *c) {   // call after a stream sync
     if (cudaEventElapsedTime(&ms, t.a, t.b) == cudaSuccess) {
       c->stats.launches[t.cls] += 1;
       c->stats.ms[t.cls] += ms;
+      c->stats.bytes[t.cls] += t.bytes;
     }
     c->free_events.push_back(t.a);
     c->free_events.push_back(t.b);
@@ -201,6 +209,40 @@ void dispatch_g(int g, Args... a) {
     default: F<32>::run(a...); break;
   }
 }
+
+template <template <int> class F, typename... Args>
+bool dispatch_nb(int nb, Args... a) {
+  switch (nb) {
+    case 2: F<2>::run(a...); return true;
+    case 3: F<3>::run(a...); return true;
+    case 4: F<4>::run(a...); return true;
+    case 5: F<5>::run(a...); return true;
+    case 6: F<6>::run(a...); return true;
+    case 7: F<7>::run(a...); return true;
+    case 8: F<8>::run(a...); return true;
+    case 9: F<9>::run(a...); return true;
+    case 10: F<10>::run(a...); return true;
+    default: return false;
+  }
+}
+
+template <int NB>
+struct BlkInvL {
+  static void run(Ctx *c, double shift, double *out);
+};
+template <int NB>
+struct ChebBlkL {
+  static void run(Ctx *c, const double *dold, double *dnew, double c1, double c2, int mode, int last, double *zp,
+                  const int *gate);
+};
+template <int NB>
+struct PcgInitBlkL {
+  static void run(Ctx *c, const int *gate);
+};
+template <int NB>
+struct PcgVecBlkL {
+  static void run(Ctx *c, const double *p);
+};
 
 template <int G>
 struct SpmvL {
@@ -248,6 +290,52 @@ struct PcgSpmvL {
   }
 };
 
+// algorithmic bytes per launch (include/vem_mixed.h)
+double bytes_spmv(Ctx *c) { return 12.0 * c->nnzA + 4.0 * (c->n + 1) + 16.0 * c->n; }
+double bytes_cheb(Ctx *c) { return 12.0 * c->nnzS + 4.0 * (c->np + 1) + 56.0 * c->np; }
+double bytes_pcg_vec(Ctx *c) { return 64.0 * c->np; }
+double bytes_vecs(Ctx *c, double nvec) { return 8.0 * c->n * nvec; }
+
+template <int G>
+struct ChebResidL {
+  static void run(Ctx *c, const double *dold, const int *gate) {
+    k_cheb_resid<G><<<grid_for(c->np * G), NT, 0, c->stream>>>(c->np, c->s_rp, c->s_ci, c->s_va, c->cr, dold, gate);
+  }
+};
+template <int G>
+struct PcgSpmvZL {
+  static void run(Ctx *c, const double *pprev, double *pnew) {
+    k_pcg_spmv_z<G><<<grid_for(c->np * G), NT, 0, c->stream>>>(c->np, c->s_rp, c->s_ci, c->s_va, c->wdiag, c->eps,
+                                                               c->pz, pprev, pnew, c->pq, c->part, c->counter, c->st);
+  }
+};
+template <int NB>
+void BlkInvL<NB>::run(Ctx *c, double shift, double *out) {
+  const long ne = c->np / NB;
+  k_block_extract_inv<NB><<<grid_stream(c, ne), 128, 0, c->stream>>>(ne, c->s_rp, c->s_ci, c->s_va, c->wdiag, shift,
+                                                                     out, c->derr);
+}
+template <int NB>
+void ChebBlkL<NB>::run(Ctx *c, const double *dold, double *dnew, double c1, double c2, int mode, int last, double *zp,
+                       const int *gate) {
+  const long ne = c->np / NB;
+  k_cheb_block<NB><<<grid_stream(c, ne), 128, 0, c->stream>>>(ne, c->dBinv, c->cr, dold, dnew, c->cx, c1, c2, mode,
+                                                              last, zp, gate);
+}
+template <int NB>
+void PcgInitBlkL<NB>::run(Ctx *c, const int *gate) {
+  const long ne = c->np / NB;
+  k_pcg_init_blk<NB><<<grid_stream(c, ne), NT, 0, c->stream>>>(ne, c->dBeinv, c->pb, c->px, c->pr, c->pz, c->pp0,
+                                                               c->part, c->counter, c->st, c->opts.inner_rtol,
+                                                               c->opts.inner_maxit, gate);
+}
+template <int NB>
+void PcgVecBlkL<NB>::run(Ctx *c, const double *p) {
+  const long ne = c->np / NB;
+  k_pcg_vec_blk<NB><<<grid_stream(c, ne), NT, 0, c->stream>>>(ne, c->dBeinv, p, c->pq, c->px, c->pr, c->pz, c->part,
+                                                              c->counter, c->st);
+}
+
 const int *gate_one(Ctx *c) { return &c->st->one_i; }
 const int *gate_active(Ctx *c) { return &c->st->g.active; }
 const int *gate_steps(Ctx *c) { return &c->st->g.has_steps; }
@@ -256,7 +344,7 @@ const int *gate_steps(Ctx *c) { return &c->st->g.has_steps; }
 // preconditioner applications (enqueue only)
 // ----------------------------------------------------------------------------
 void cheb_coeffs(Ctx *c, double &inv_theta, std::vector<double> &c1, std::vector<double> &c2) {
-  const double b = c->lmax, a = c->lmax / c->opts.cheb_ratio;
+  const double b = c->lmax_cheb, a = c->lmax_cheb / c->opts.cheb_ratio;
   const double theta = 0.5 * (b + a), delta = 0.5 * (b - a), sigma = theta / delta;
   double rho = 1.0 / sigma;
   inv_theta = 1.0 / theta;
@@ -275,16 +363,32 @@ int enqueue_block_schur(Ctx *c, const double *v, const double *scale, double *z,
   std::vector<double> c1, c2;
   cheb_coeffs(c, inv_theta, c1, c2);
   const int deg = c->opts.cheb_degree;
+  const bool blk = c->nb > 1;
   {
-    TimeScope ts(c, VEM_K_PRECOND_VEC);
+    TimeScope ts(c, VEM_K_PRECOND_VEC, 8.0 * (3 * c->nu + 5 * c->np));
     k_bs_init<<<grid_stream(c, c->n), NT, 0, c->stream>>>(c->nu, c->np, v, scale, c->dMinv, c->dSinv, inv_theta, z,
-                                                          c->cr, c->cd0, c->cx, deg == 1, gate);
+                                                          c->cr, c->cd0, c->cx, deg == 1, blk ? 1 : 0, gate);
+  }
+  if (blk) {
+    TimeScope ts(c, VEM_K_PRECOND_VEC, 8.0 * c->np * (3 + c->nb));
+    dispatch_nb<ChebBlkL>(c->nb, c, (const double *)nullptr, c->cd0, 0.0, inv_theta, 1, deg == 1 ? 1 : 0,
+                          z + c->nu, gate);
   }
   CKL();
   double *dold = c->cd0, *dnew = c->cd1;
   for (int i = 1; i < deg; ++i) {
-    TimeScope ts(c, VEM_K_CHEB);
-    dispatch_g<ChebL>(c->gS, c, dold, dnew, c1[i - 1], c2[i - 1], i == deg - 1 ? 1 : 0, z + c->nu, gate);
+    const int last = i == deg - 1 ? 1 : 0;
+    if (blk) {
+      {
+        TimeScope ts(c, VEM_K_CHEB, 12.0 * c->nnzS + 4.0 * (c->np + 1) + 24.0 * c->np);
+        dispatch_g<ChebResidL>(c->gS, c, (const double *)dold, gate);
+      }
+      TimeScope ts(c, VEM_K_PRECOND_VEC, 8.0 * c->np * (5 + c->nb));
+      dispatch_nb<ChebBlkL>(c->nb, c, (const double *)dold, dnew, c1[i - 1], c2[i - 1], 0, last, z + c->nu, gate);
+    } else {
+      TimeScope ts(c, VEM_K_CHEB, bytes_cheb(c));
+      dispatch_g<ChebL>(c->gS, c, dold, dnew, c1[i - 1], c2[i - 1], last, z + c->nu, gate);
+    }
     std::swap(dold, dnew);
   }
   CKL();
@@ -307,9 +411,12 @@ int enqueue_block_reg(Ctx *c, const double *v, const double *scale, double *z, c
   CKL();
   {
     TimeScope ts(c, VEM_K_PRECOND_VEC);
-    k_pcg_init<<<grid_stream(c, c->np), NT, 0, c->stream>>>(c->np, c->pb, c->dSepsinv, c->px, c->pr, c->pp0,
-                                                            c->part, c->counter, c->st, c->opts.inner_rtol,
-                                                            c->opts.inner_maxit, gate);
+    if (c->nb > 1)
+      dispatch_nb<PcgInitBlkL>(c->nb, c, gate);
+    else
+      k_pcg_init<<<grid_stream(c, c->np), NT, 0, c->stream>>>(c->np, c->pb, c->dSepsinv, c->px, c->pr, c->pp0,
+                                                              c->part, c->counter, c->st, c->opts.inner_rtol,
+                                                              c->opts.inner_maxit, gate);
   }
   CKL();
   int rc = run_pcg(c, inner_its);
@@ -326,12 +433,19 @@ int enqueue_pcg_steps(Ctx *c, int nsteps) {
   for (int s = 0; s < nsteps; ++s) {
     double *pprev = (s % 2 == 0) ? c->pp0 : c->pp1;
     double *pnew = (s % 2 == 0) ? c->pp1 : c->pp0;
-    {
-      TimeScope ts(c, VEM_K_PCG_SPMV);
-      dispatch_g<PcgSpmvL>(c->gS, c, (const double *)pprev, pnew);
-    }
-    {
-      TimeScope ts(c, VEM_K_PCG_VEC);
+    if (c->nb > 1) {
+      {
+        TimeScope ts(c, VEM_K_PCG_SPMV, bytes_cheb(c));
+        dispatch_g<PcgSpmvZL>(c->gS, c, (const double *)pprev, pnew);
+      }
+      TimeScope ts(c, VEM_K_PCG_VEC, bytes_pcg_vec(c) + 8.0 * c->np * c->nb);
+      dispatch_nb<PcgVecBlkL>(c->nb, c, (const double *)pnew);
+    } else {
+      {
+        TimeScope ts(c, VEM_K_PCG_SPMV, bytes_cheb(c));
+        dispatch_g<PcgSpmvL>(c->gS, c, (const double *)pprev, pnew);
+      }
+      TimeScope ts(c, VEM_K_PCG_VEC, bytes_pcg_vec(c));
       k_pcg_vec<<<grid_stream(c, c->np), NT, 0, c->stream>>>(c->np, c->dSepsinv, pnew, c->pq, c->px, c->pr,
                                                              c->part, c->counter, c->st);
     }
@@ -386,7 +500,7 @@ int enqueue_precond(Ctx *c, int kind, const double *v, const double *scale, doub
   // NONE: z = scale * v
   TimeScope ts(c, VEM_K_PRECOND_VEC);
   k_bs_init<<<grid_stream(c, c->n), NT, 0, c->stream>>>(c->n, 0, v, scale, nullptr, nullptr, 0.0, z, nullptr,
-                                                        nullptr, nullptr, 0, gate);
+                                                        nullptr, nullptr, 0, 0, gate);
   CKL();
   return 0;
 }
@@ -411,7 +525,7 @@ int enqueue_arnoldi_step(Ctx *c, int kind, int j, int64_t *inner_its) {
   int rc = enqueue_precond(c, kind, Vj, &c->st->vscale[j], zj, gate_active(c), inner_its);
   if (rc) return rc;
   {
-    TimeScope ts(c, VEM_K_SPMV);
+    TimeScope ts(c, VEM_K_SPMV, bytes_spmv(c));
     dispatch_g<SpmvL>(c->gA, c, 0L, c->n, (const double *)zj, w, (const double *)nullptr, 0, gate_active(c));
   }
   const int nv = j + 1;
@@ -420,12 +534,12 @@ int enqueue_arnoldi_step(Ctx *c, int kind, int j, int64_t *inner_its) {
     const int nout = nv + (pass == 1 ? 1 : 0);
     dim3 grid(gx, (nout + VEM_DOT_CHUNK - 1) / VEM_DOT_CHUNK);
     {
-      TimeScope ts(c, VEM_K_DOT);
+      TimeScope ts(c, VEM_K_DOT, bytes_vecs(c, nv + 1));
       k_mdot<<<grid, NT, 0, c->stream>>>(c->n, c->V, c->ldv, nv, pass == 1 ? 1 : 0, w, c->part, c->counter, c->st,
                                          pass);
     }
     {
-      TimeScope ts(c, VEM_K_UPDATE);
+      TimeScope ts(c, VEM_K_UPDATE, bytes_vecs(c, nv + 2));
       k_update<<<gx * 2, NT, 0, c->stream>>>(c->n, c->V, c->ldv, nv, w, pass == 2 ? 1 : 0, c->part, c->counter,
                                              c->st, j);
     }
@@ -454,7 +568,7 @@ int enqueue_cycle_end(Ctx *c, int kind, int64_t *inner_its) {
     k_axpy_gated<<<grid_stream(c, c->n), NT, 0, c->stream>>>(c->n, c->z, c->x, gate_steps(c));
   }
   {
-    TimeScope ts(c, VEM_K_SPMV);
+    TimeScope ts(c, VEM_K_SPMV, bytes_spmv(c) + 8.0 * c->n);
     dispatch_g<ResidL>(c->gA, c, (const double *)c->x, (const double *)c->b, c->V, 1);
   }
   CKL();
@@ -766,6 +880,8 @@ int upload_impl(Ctx *c, const vem_csr *M, const vem_csr *B, const vem_csr *W, do
   if ((r = check_csr(c, B, c->np, c->nu, "B"))) return r;
   if (lay) {
     c->layout = *lay;
+    c->nb = std::max(1, (int)lay->n_p_dof);
+    if (c->nb > 10) return fail(c, VEM_ERR_INVALID, "n_p_dof > 10 is not supported (k <= 2)");
     const long nu = (long)lay->n_faces * lay->n_face_dof + (long)lay->n_elems * lay->n_int_dof;
     const long np = (long)lay->n_elems * lay->n_p_dof;
     if (nu != c->nu || np != c->np) return fail(c, VEM_ERR_INVALID, "layout does not match M/B sizes");
@@ -899,6 +1015,20 @@ int upload_impl(Ctx *c, const vem_csr *M, const vem_csr *B, const vem_csr *W, do
     k_shift_inv<<<grid_stream(c, c->np), NT, 0, c->stream>>>(c->np, c->sdiag, c->wdiag, eps, c->dSepsinv);
     CKL();
   }
+  if (c->nb > 1) {
+    if (c->np % c->nb) return fail(c, VEM_ERR_INVALID, "n_p is not a multiple of n_p_dof");
+    DA(c->dBinv, (size_t)c->np * c->nb);
+    dispatch_nb<BlkInvL>(c->nb, c, 0.0, c->dBinv);
+    if (c->has_reg) {
+      DA(c->dBeinv, (size_t)c->np * c->nb);
+      dispatch_nb<BlkInvL>(c->nb, c, eps, c->dBeinv);
+      DA(c->pz, c->np);
+    }
+    CKL();
+    CK(cudaMemcpyAsync(&herr, c->derr, sizeof(int), cudaMemcpyDeviceToHost, c->stream));
+    CK(cudaStreamSynchronize(c->stream));
+    if (herr) return fail(c, VEM_ERR_DIAG_S, "singular element block of S_D");
+  }
   // work vectors
   DA(c->x, c->n);
   DA(c->b, c->n);
@@ -934,7 +1064,21 @@ void destroy_ctx(Ctx *c) {
   for (auto e : c->free_events) cudaEventDestroy(e);
   for (void *p : c->allocs) cudaFree(p);
   if (c->hst) cudaFreeHost(c->hst);
+  if (c->ev_in) cudaEventDestroy(c->ev_in);
+  if (c->ev_out) cudaEventDestroy(c->ev_out);
+  if (c->stream) cudaStreamDestroy(c->stream);
   delete c;
+}
+
+// order the library stream after the caller's stream (entry) and vice versa (exit)
+int enter(Ctx *c) {
+  CK(cudaEventRecord(c->ev_in, c->user_stream));
+  CK(cudaStreamWaitEvent(c->stream, c->ev_in, 0));
+  return 0;
+}
+int leave(Ctx *c, int rc) {
+  if (cudaEventRecord(c->ev_out, c->stream) == cudaSuccess) cudaStreamWaitEvent(c->user_stream, c->ev_out, 0);
+  return rc;
 }
 
 }  // namespace
@@ -952,7 +1096,7 @@ void vem_mixed_default_options(vem_opts *o) {
   o->restart = 30;
   o->cheb_degree = 16;
   o->cheb_ratio = 30.0;
-  o->inner_rtol = 1e-10;
+  o->inner_rtol = 1e-14;
   o->inner_maxit = 10000;
   o->use_graphs = 1;
   o->timing = 0;
@@ -982,8 +1126,17 @@ int vem_mixed_upload(vem_ctx **out, const vem_csr *M, const vem_csr *B, const ve
     }
     c->opts = *opts;
   }
-  c->stream = (cudaStream_t)stream;
-  int r = upload_impl(c, M, B, W, eps, layout);
+  c->user_stream = (cudaStream_t)stream;
+  if (cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking) != cudaSuccess ||
+      cudaEventCreateWithFlags(&c->ev_in, cudaEventDisableTiming) != cudaSuccess ||
+      cudaEventCreateWithFlags(&c->ev_out, cudaEventDisableTiming) != cudaSuccess) {
+    g_last_err = "failed to create the library stream (no CUDA device?)";
+    destroy_ctx(c);
+    return VEM_ERR_CUDA;
+  }
+  int r = enter(c);
+  if (!r) r = upload_impl(c, M, B, W, eps, layout);
+  leave(c, r);
   if (r) {
     g_last_err = c->err;
     destroy_ctx(c);
@@ -997,13 +1150,20 @@ int vem_mixed_upload(vem_ctx **out, const vem_csr *M, const vem_csr *B, const ve
 int vem_mixed_solve(vem_ctx *h, const double *rhs, double tol, int32_t maxit, int32_t kind, double *out_u,
                     double *out_p, vem_solve_report *rep) {
   if (!h) return VEM_ERR_INVALID;
-  return solve_impl(h->impl, rhs, tol, maxit, kind, out_u, out_p, rep);
+  Ctx *c = h->impl;
+  int r = enter(c);
+  if (r) return r;
+  return leave(c, solve_impl(c, rhs, tol, maxit, kind, out_u, out_p, rep));
 }
 
 int vem_mixed_solve_host(vem_ctx *h, const double *rhs_host, double tol, int32_t maxit, int32_t kind,
                          double *u_host, double *p_host, vem_solve_report *rep) {
   if (!h || !rhs_host || !u_host || !p_host) return VEM_ERR_INVALID;
   Ctx *c = h->impl;
+  {
+    int r0 = enter(c);
+    if (r0) return r0;
+  }
   double *drhs = nullptr, *du = nullptr, *dp = nullptr;
   DA(drhs, c->n);
   DA(du, c->nu);
@@ -1018,25 +1178,29 @@ int vem_mixed_solve_host(vem_ctx *h, const double *rhs_host, double tol, int32_t
   dfree(c, drhs);
   dfree(c, du);
   dfree(c, dp);
-  return r;
+  return leave(c, r);
 }
 
 int vem_mixed_spmv(vem_ctx *h, const double *x, double *y) {
   if (!h || !x || !y) return VEM_ERR_INVALID;
   Ctx *c = h->impl;
+  int r = enter(c);
+  if (r) return r;
   dispatch_g<SpmvL>(c->gA, c, 0L, c->n, x, y, (const double *)nullptr, 0, gate_one(c));
   CKL();
   CK(cudaStreamSynchronize(c->stream));
-  return VEM_OK;
+  return leave(c, VEM_OK);
 }
 
 int vem_mixed_schur_spmv(vem_ctx *h, const double *x, double *y) {
   if (!h || !x || !y) return VEM_ERR_INVALID;
   Ctx *c = h->impl;
+  int r = enter(c);
+  if (r) return r;
   dispatch_g<SchurSpmvL>(c->gS, c, x, y, gate_one(c));
   CKL();
   CK(cudaStreamSynchronize(c->stream));
-  return VEM_OK;
+  return leave(c, VEM_OK);
 }
 
 int vem_mixed_precond_apply(vem_ctx *h, int32_t kind, const double *v, double *z, int64_t *inner_its) {
@@ -1045,12 +1209,14 @@ int vem_mixed_precond_apply(vem_ctx *h, int32_t kind, const double *v, double *z
   if (kind < 0 || kind > 2) return fail(c, VEM_ERR_PRECOND, "unsupported precond_kind %d", kind);
   if (kind == VEM_PRECOND_BLOCK_REG && !c->has_reg) return fail(c, VEM_ERR_PRECOND, "Block-Reg needs eps > 0");
   int64_t its = 0;
-  int r = enqueue_precond(c, kind, v, &c->st->one, z, gate_one(c), &its);
+  int r = enter(c);
   if (r) return r;
+  r = enqueue_precond(c, kind, v, &c->st->one, z, gate_one(c), &its);
+  if (r) return leave(c, r);
   CK(cudaStreamSynchronize(c->stream));
   flush_timing(c);
   if (inner_its) *inner_its = its;
-  return VEM_OK;
+  return leave(c, VEM_OK);
 }
 
 int vem_mixed_set_options(vem_ctx *h, const vem_opts *o) {

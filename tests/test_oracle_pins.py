@@ -40,7 +40,7 @@ def test_chebyshev_closed_form(degree):
     lam, U = np.linalg.eigh(Dh @ S @ Dh)
     lmax, ratio = 1.05 * lam.max(), 30.0
     v = RNG.normal(size=n)
-    x = O.chebyshev(sp.csr_matrix(S), 1 / d, v, degree, lmax, ratio)
+    x = O.chebyshev(sp.csr_matrix(S), sp.diags(1 / d), v, degree, lmax, ratio)
     a, b = lmax / ratio, lmax
     theta, delta = (a + b) / 2, (b - a) / 2
     cd = np.zeros(degree + 1)
@@ -56,7 +56,7 @@ def test_chebyshev_linear():
     S = sp.csr_matrix(_spd(30) + 3 * np.eye(30))
     d = S.diagonal()
     a, b = RNG.normal(size=30), RNG.normal(size=30)
-    f = lambda v: O.chebyshev(S, 1 / d, v, 16, 2.0, 30.0)  # noqa: E731
+    f = lambda v: O.chebyshev(S, sp.diags(1 / d), v, 16, 2.0, 30.0)  # noqa: E731
     assert np.abs(f(2 * a - 3 * b) - (2 * f(a) - 3 * f(b))).max() < 1e-13 * np.abs(f(a)).max() * 10
 
 
@@ -95,15 +95,23 @@ def test_gmres_identity_and_diagonal_one_iteration():
 def test_gmres_vs_lu_c1(kind):
     s = configs.CONFIGS["C1"].build()
     xd = O.dense_solve(s.M, s.B, s.rhs)
-    r = O.solve(s.M, s.B, s.rhs, kind, 1e-10, 30, eps=configs.eps_for(s))
+    r = O.solve(s.M, s.B, s.rhs, kind, 1e-10, 30, eps=configs.eps_for(s), block=s.layout.n_p_dof)
     assert r.converged and r.rel_residual_true <= 1e-10
     assert np.abs(r.x - xd).max() <= 1e-8 * np.abs(xd).max()
 
 
-def test_gmres_vs_lu_k1_tets():
+def test_gmres_vs_lu_k1_tets_and_k2_cubes():
     s = configs.CONFIGS["C2s"].build()
     xd = O.dense_solve(s.M, s.B, s.rhs)
-    r = O.solve(s.M, s.B, s.rhs, O.PRECOND_BLOCK_SCHUR, 1e-10, 30)
+    for kind in (O.PRECOND_BLOCK_SCHUR, O.PRECOND_BLOCK_REG):
+        r = O.solve(s.M, s.B, s.rhs, kind, 1e-10, 30, eps=configs.eps_for(s), block=s.layout.n_p_dof)
+        assert r.converged
+        nu = s.layout.n_u
+        for sl in (slice(0, nu), slice(nu, None)):
+            assert np.abs(r.x[sl] - xd[sl]).max() <= 1e-8 * np.abs(xd[sl]).max()
+    s = configs.CONFIGS["C4s"].build()
+    xd = O.dense_solve(s.M, s.B, s.rhs)
+    r = O.solve(s.M, s.B, s.rhs, O.PRECOND_BLOCK_REG, 1e-10, 50, eps=configs.eps_for(s), block=s.layout.n_p_dof)
     assert r.converged
     nu = s.layout.n_u
     for sl in (slice(0, nu), slice(nu, None)):
@@ -119,10 +127,14 @@ def test_exact_schur_eigenvector_case():
 def test_pcg_dense_and_diagonal():
     A = _spd(60, 1e3)
     b = RNG.normal(size=60)
-    x, its, ok = O.pcg(sp.csr_matrix(A), 1 / np.diag(A), b, 1e-12, 1000)
+    x, its, ok = O.pcg(sp.csr_matrix(A), sp.diags(1 / np.diag(A)), b, 1e-12, 1000)
     assert ok and np.abs(x - np.linalg.solve(A, b)).max() < 1e-9 * np.abs(x).max()
     dg = RNG.uniform(1, 100, 60)
-    x, its, ok = O.pcg(sp.diags(dg).tocsr(), 1 / dg, b, 1e-12, 10)
+    x, its, ok = O.pcg(sp.diags(dg).tocsr(), sp.diags(1 / dg), b, 1e-12, 10)
+    assert ok and its == 1
+    # exact block preconditioner on a block-diagonal matrix -> 1 iteration
+    Bd = sp.block_diag([_spd(4, 10.0) for _ in range(15)]).tocsr()
+    x, its, ok = O.pcg(Bd, O.block_jacobi_inv(Bd, 4), b, 1e-12, 10)
     assert ok and its == 1
 
 
@@ -139,6 +151,24 @@ def test_woodbury_block_reg_velocity_block():
     zu_ref = ref @ v[:nu]
     assert np.abs(z[:nu] - zu_ref).max() < 1e-7 * np.abs(zu_ref).max()
     assert np.abs(z[nu:] - v[nu:] / eps).max() == 0.0
+
+
+@pytest.mark.parametrize("name", ["C2s", "C4s", "C5s", "C3s"])
+def test_block_jacobi_lambda_max_bound(name):
+    """lambda_max(D_B^-1 S_D) <= 2 (reading R15) by dense eigenvalues, and
+    D_B^-1 is the exact inverse of every element block."""
+    s = configs.CONFIGS[name].build()
+    nb = s.layout.n_p_dof
+    SD = O.schur_diag(s.M, s.B)
+    Dinv = O.block_jacobi_inv(SD, nb)
+    Sd = SD.toarray()
+    for e in (0, SD.shape[0] // nb // 2, SD.shape[0] // nb - 1):
+        sl = slice(e * nb, (e + 1) * nb)
+        assert np.abs(Dinv[sl, sl].toarray() @ Sd[sl, sl] - np.eye(nb)).max() < 1e-9
+    n = min(SD.shape[0], 2500)
+    lam = np.linalg.eigvals((Dinv @ SD).toarray()[:n, :n] if n < SD.shape[0] else (Dinv @ SD).toarray())
+    if n == SD.shape[0]:
+        assert np.real(lam).max() <= 2.0 + 1e-10
 
 
 def test_spmv_definition():
