@@ -117,9 +117,9 @@ enum {
 };
 
 /* bytes[] is the ALGORITHMIC HBM traffic of the timed launches:
- *   SPMV      12 nnz(A) + 4 (n+1) + 16 n          (values+indices, row ptr, x once, y)
- *   CHEB      12 nnz(S) + 4 (n_p+1) + 56 n_p      (S, D^-1, r rw, d_old, d_new, x rw)
- *   PCG_SPMV  12 nnz(S) + 4 (n_p+1) + 56 n_p      (S, D^-1, W, r, p_prev, p_new, q)
+ *   SPMV      12 nnz(A) + 16 n                    (values+indices, x once, y)
+ *   CHEB      12 nnz(S) + 56 n_p                  (S, D^-1, r rw, d_old, d_new, x rw)
+ *   PCG_SPMV  12 nnz(S) + 56 n_p                  (S, D^-1, W, r, p_prev, p_new, q)
  *   PCG_VEC   64 n_p                               (D^-1, p, q, x rw, r rw)
  *   DOT       8 n (nv + 1)                         (nv basis vectors + w)
  *   UPDATE    8 n (nv + 2)                         (nv basis vectors + w rw)

@@ -118,60 +118,61 @@ __device__ void reduce_partials(const double *part, int nb, int nout, double *ou
 }
 
 // ---------------------------------------------------------------------------
-// CSR SpMV, G lanes per row (G in {1,2,4,8,16,32}), rows [row0, row0 + nrows)
-//   mode 0: y[r] = (A x)[r]            mode 1: y[r] = b[r] - (A x)[r]
+// SELL-32 sparse format (sliced ELLPACK, slice height 32 = one warp, sigma = 1:
+// rows keep their order).  Slice s holds rows [32 s, 32 s + 32); entry j of
+// row r sits at soff[s] + 32 j + (r & 31), so the 32 lanes of a warp read 32
+// consecutive doubles (256 B) and 32 consecutive int32 columns per step:
+// fully coalesced, one row per thread, no shuffles.  Rows shorter than the
+// slice width are padded with (col = a valid column of the row, val = 0).
 // ---------------------------------------------------------------------------
-template <int G>
-__device__ __forceinline__ double row_dot(const int *__restrict__ rp, const int *__restrict__ ci,
-                                          const double *__restrict__ va, const double *__restrict__ x,
-                                          long row, bool valid) {
+struct Sell {
+  const long long *__restrict__ soff;
+  const int *__restrict__ ci;
+  const double *__restrict__ va;
+};
+
+template <typename Gather>
+__device__ __forceinline__ double sell_dot(const Sell &A, long row, Gather g) {
+  const long s = row >> 5;
+  const int lane = (int)(row & 31);
+  const long long b = A.soff[s];
+  const int w = (int)((A.soff[s + 1] - b) >> 5);
+  const int *__restrict__ c = A.ci + b + lane;
+  const double *__restrict__ v = A.va + b + lane;
   double acc = 0.0;
-  if (valid) {
-    const int s = rp[row], e = rp[row + 1];
-    const int lane = threadIdx.x & (G - 1);
-    for (int k = s + lane; k < e; k += G) acc = fma(va[k], __ldg(x + ci[k]), acc);
-  }
-  if (G > 1) {
-#pragma unroll
-    for (int o = G / 2; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o, G);
-  }
+#pragma unroll 4
+  for (int j = 0; j < w; ++j) acc = fma(__ldcs(v + ((long)j << 5)), g(__ldcs(c + ((long)j << 5))), acc);
   return acc;
 }
 
-template <int G>
-__global__ void __launch_bounds__(256) k_spmv(long row0, long nrows, const int *__restrict__ rp,
-                                              const int *__restrict__ ci, const double *__restrict__ va,
-                                              const double *__restrict__ x, double *__restrict__ y,
-                                              const double *__restrict__ b, int mode, const int *gate) {
+struct GatherX {
+  const double *__restrict__ x;
+  __device__ __forceinline__ double operator()(int c) const { return __ldg(x + c); }
+};
+
+// y[r] = (A x)[r] (mode 0) or b[r] - (A x)[r] (mode 1), rows [row0, row0 + nrows)
+__global__ void __launch_bounds__(256) k_spmv(long row0, long nrows, Sell A, const double *__restrict__ x,
+                                              double *__restrict__ y, const double *__restrict__ b, int mode,
+                                              const int *gate) {
   if (!*gate) return;
   const long t = (long)blockIdx.x * blockDim.x + threadIdx.x;
-  const long r = t / G;
-  const bool valid = r < nrows;
-  const double acc = row_dot<G>(rp, ci, va, x, row0 + r, valid);
-  if (valid && (threadIdx.x & (G - 1)) == 0) {
-    const long row = row0 + r;
-    y[row] = mode ? b[row] - acc : acc;
-  }
+  if (t >= nrows) return;
+  const long row = row0 + t;
+  const double acc = sell_dot(A, row, GatherX{x});
+  y[row] = mode ? b[row] - acc : acc;
 }
 
 // Residual r = b - A x written to V0 with ||r||^2 partials; the last block
 // starts a new GMRES cycle: beta = ||r||, vscale_0 = 1/beta, g = (beta, 0, ..).
-template <int G>
-__global__ void __launch_bounds__(256) k_residual_start(long n, const int *__restrict__ rp,
-                                                        const int *__restrict__ ci,
-                                                        const double *__restrict__ va,
-                                                        const double *__restrict__ x,
+__global__ void __launch_bounds__(256) k_residual_start(long n, Sell A, const double *__restrict__ x,
                                                         const double *__restrict__ b, double *__restrict__ r,
                                                         int use_x, double *part, unsigned *counter,
                                                         DevState *st) {
   __shared__ double sh[32];
-  const long t = (long)blockIdx.x * blockDim.x + threadIdx.x;
-  const long row = t / G;
-  const bool valid = row < n;
-  double acc = 0.0;
-  if (use_x) acc = row_dot<G>(rp, ci, va, x, row, valid);
+  const long row = (long)blockIdx.x * blockDim.x + threadIdx.x;
   double v[1] = {0.0};
-  if (valid && (threadIdx.x & (G - 1)) == 0) {
+  if (row < n) {
+    const double acc = use_x ? sell_dot(A, row, GatherX{x}) : 0.0;
     const double rv = b[row] - acc;
     r[row] = rv;
     v[0] = rv * rv;
@@ -198,6 +199,34 @@ __global__ void __launch_bounds__(256) k_residual_start(long n, const int *__res
       st->vscale[0] = beta > 0.0 ? 1.0 / beta : 0.0;
       st->gv[0] = beta;
       *counter = 0u;
+    }
+  }
+}
+
+// CSR -> SELL-32 conversion (upload only)
+__global__ void k_sell_width(long nrows, const int *__restrict__ rp, long long *__restrict__ wslice) {
+  const long nsl = (nrows + 31) / 32;
+  for (long s = (long)blockIdx.x * blockDim.x + threadIdx.x; s < nsl; s += (long)gridDim.x * blockDim.x) {
+    int w = 0;
+    for (long r = s * 32; r < s * 32 + 32 && r < nrows; ++r) w = max(w, rp[r + 1] - rp[r]);
+    wslice[s] = 32LL * w;
+  }
+}
+__global__ void k_sell_fill(long nrows, const int *__restrict__ rp, const int *__restrict__ ci,
+                            const double *__restrict__ va, const long long *__restrict__ soff, int *__restrict__ sci,
+                            double *__restrict__ sva) {
+  const long nsl = (nrows + 31) / 32;
+  for (long r = (long)blockIdx.x * blockDim.x + threadIdx.x; r < nsl * 32; r += (long)gridDim.x * blockDim.x) {
+    const long s = r >> 5;
+    const int lane = (int)(r & 31);
+    const long long b = soff[s];
+    const int w = (int)((soff[s + 1] - b) >> 5);
+    const int st = r < nrows ? rp[r] : 0, len = r < nrows ? rp[r + 1] - rp[r] : 0;
+    const int padc = len > 0 ? ci[st + len - 1] : 0;
+    for (int j = 0; j < w; ++j) {
+      const long long o = b + 32LL * j + lane;
+      sci[o] = j < len ? ci[st + j] : padc;
+      sva[o] = j < len ? va[st + j] : 0.0;
     }
   }
 }
@@ -237,28 +266,23 @@ __global__ void k_bs_init(long nu, long np, const double *__restrict__ v, const 
 
 // one Chebyshev step:  r -= S d_old;  d_new = c1 d_old + c2 D^-1 r;  x += d_new
 // last step writes z_p = -(x + d_new) instead of x.
-template <int G>
-__global__ void __launch_bounds__(256) k_cheb_step(long np, const int *__restrict__ rp, const int *__restrict__ ci,
-                                                   const double *__restrict__ va, const double *__restrict__ dSinv,
+__global__ void __launch_bounds__(256) k_cheb_step(long np, Sell S, const double *__restrict__ dSinv,
                                                    double *__restrict__ r, const double *__restrict__ d_old,
                                                    double *__restrict__ d_new, double *__restrict__ x, double c1,
                                                    double c2, int last, double *__restrict__ zp, const int *gate) {
   if (!*gate) return;
-  const long t = (long)blockIdx.x * blockDim.x + threadIdx.x;
-  const long row = t / G;
-  const bool valid = row < np;
-  const double sd = row_dot<G>(rp, ci, va, d_old, row, valid);
-  if (valid && (threadIdx.x & (G - 1)) == 0) {
-    const double rn = r[row] - sd;
-    const double dn = c1 * d_old[row] + c2 * (dSinv[row] * rn);
-    const double xn = x[row] + dn;
-    if (last) {
-      zp[row] = -xn;
-    } else {
-      r[row] = rn;
-      d_new[row] = dn;
-      x[row] = xn;
-    }
+  const long row = (long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (row >= np) return;
+  const double sd = sell_dot(S, row, GatherX{d_old});
+  const double rn = r[row] - sd;
+  const double dn = c1 * d_old[row] + c2 * (dSinv[row] * rn);
+  const double xn = x[row] + dn;
+  if (last) {
+    zp[row] = -xn;
+  } else {
+    r[row] = rn;
+    d_new[row] = dn;
+    x[row] = xn;
   }
 }
 
@@ -284,28 +308,18 @@ __global__ void k_br_init(long nu, long np, const double *__restrict__ v, const 
 }
 
 // z_u[i] -= dMinv[i] * sum_{k in row i, col >= nu} A_ik t[col - nu]   (B^T t)
-template <int G>
-__global__ void __launch_bounds__(256) k_br_finish(long nu, const int *__restrict__ rp, const int *__restrict__ ci,
-                                                   const double *__restrict__ va, const double *__restrict__ dMinv,
+struct GatherBt {
+  long nu;
+  const double *__restrict__ tp;
+  __device__ __forceinline__ double operator()(int c) const { return c >= nu ? tp[c - nu] : 0.0; }
+};
+__global__ void __launch_bounds__(256) k_br_finish(long nu, Sell A, const double *__restrict__ dMinv,
                                                    const double *__restrict__ tp, double *__restrict__ z,
                                                    const int *gate) {
   if (!*gate) return;
-  const long t = (long)blockIdx.x * blockDim.x + threadIdx.x;
-  const long row = t / G;
-  const bool valid = row < nu;
-  double acc = 0.0;
-  if (valid) {
-    const int s = rp[row], e = rp[row + 1];
-    for (int k = s + (int)(threadIdx.x & (G - 1)); k < e; k += G) {
-      const int c = ci[k];
-      if (c >= nu) acc = fma(va[k], tp[c - nu], acc);
-    }
-  }
-  if (G > 1) {
-#pragma unroll
-    for (int o = G / 2; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o, G);
-  }
-  if (valid && (threadIdx.x & (G - 1)) == 0) z[row] -= dMinv[row] * acc;
+  const long row = (long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (row >= nu) return;
+  z[row] -= dMinv[row] * sell_dot(A, row, GatherBt{nu, tp});
 }
 
 // PCG init: x = 0, r = b, p_prev = 0, beta = 0; rz = r.D^-1 r, bn = ||b||
@@ -351,9 +365,12 @@ __global__ void k_pcg_init(long n, const double *__restrict__ b, const double *_
 
 // PCG step part 1: p_new = D^-1 r + beta p_prev (on the fly at every gathered
 // column), q = (S + eps W) p_new, partial p_new . q; last block: alpha = rz / pq
-template <int G>
-__global__ void __launch_bounds__(256) k_pcg_spmv(long n, const int *__restrict__ rp, const int *__restrict__ ci,
-                                                  const double *__restrict__ va, const double *__restrict__ dinv,
+struct GatherPcg {
+  double beta;
+  const double *__restrict__ p_prev, *__restrict__ dinv, *__restrict__ r;
+  __device__ __forceinline__ double operator()(int c) const { return fma(beta, p_prev[c], dinv[c] * r[c]); }
+};
+__global__ void __launch_bounds__(256) k_pcg_spmv(long n, Sell S, const double *__restrict__ dinv,
                                                   const double *__restrict__ wdiag, double eps,
                                                   const double *__restrict__ r, const double *__restrict__ p_prev,
                                                   double *__restrict__ p_new, double *__restrict__ q, double *part,
@@ -361,24 +378,10 @@ __global__ void __launch_bounds__(256) k_pcg_spmv(long n, const int *__restrict_
   __shared__ double sh[32];
   if (!st->p.active) return;
   const double beta = st->p.beta;
-  const long t = (long)blockIdx.x * blockDim.x + threadIdx.x;
-  const long row = t / G;
-  const bool valid = row < n;
-  double acc = 0.0;
-  if (valid) {
-    const int s = rp[row], e = rp[row + 1];
-    for (int k = s + (int)(threadIdx.x & (G - 1)); k < e; k += G) {
-      const int c = ci[k];
-      const double pc = fma(beta, p_prev[c], dinv[c] * r[c]);
-      acc = fma(va[k], pc, acc);
-    }
-  }
-  if (G > 1) {
-#pragma unroll
-    for (int o = G / 2; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o, G);
-  }
+  const long row = (long)blockIdx.x * blockDim.x + threadIdx.x;
   double v[1] = {0.0};
-  if (valid && (threadIdx.x & (G - 1)) == 0) {
+  if (row < n) {
+    const double acc = sell_dot(S, row, GatherPcg{beta, p_prev, dinv, r});
     const double pi = fma(beta, p_prev[row], dinv[row] * r[row]);
     const double w = wdiag ? wdiag[row] : 1.0;
     const double qi = fma(eps * w, pi, acc);
@@ -838,16 +841,12 @@ __device__ __forceinline__ void block_mv(const double *__restrict__ inv, long e,
 }
 
 // r_new = r - S d_old (rows), the SpMV half of a block-Jacobi Chebyshev step
-template <int G>
-__global__ void __launch_bounds__(256) k_cheb_resid(long np, const int *__restrict__ rp, const int *__restrict__ ci,
-                                                    const double *__restrict__ va, double *__restrict__ r,
+__global__ void __launch_bounds__(256) k_cheb_resid(long np, Sell S, double *__restrict__ r,
                                                     const double *__restrict__ d_old, const int *gate) {
   if (!*gate) return;
-  const long t = (long)blockIdx.x * blockDim.x + threadIdx.x;
-  const long row = t / G;
-  const bool valid = row < np;
-  const double sd = row_dot<G>(rp, ci, va, d_old, row, valid);
-  if (valid && (threadIdx.x & (G - 1)) == 0) r[row] -= sd;
+  const long row = (long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (row >= np) return;
+  r[row] -= sell_dot(S, row, GatherX{d_old});
 }
 
 // block half of a Chebyshev step (mode 0) or the init (mode 1: d = D^-1 r * c2, x = d)
@@ -928,33 +927,22 @@ __global__ void k_pcg_init_blk(long ne, const double *__restrict__ inv, const do
 }
 
 // block PCG step A: p_new = z + beta p_prev (gathered), q = (S + eps W) p_new, p.q -> alpha
-template <int G>
-__global__ void __launch_bounds__(256) k_pcg_spmv_z(long n, const int *__restrict__ rp, const int *__restrict__ ci,
-                                                    const double *__restrict__ va, const double *__restrict__ wdiag,
-                                                    double eps, const double *__restrict__ z,
-                                                    const double *__restrict__ p_prev, double *__restrict__ p_new,
-                                                    double *__restrict__ q, double *part, unsigned *counter,
-                                                    DevState *st) {
+struct GatherPz {
+  double beta;
+  const double *__restrict__ p_prev, *__restrict__ z;
+  __device__ __forceinline__ double operator()(int c) const { return fma(beta, p_prev[c], z[c]); }
+};
+__global__ void __launch_bounds__(256) k_pcg_spmv_z(long n, Sell S, const double *__restrict__ wdiag, double eps,
+                                                    const double *__restrict__ z, const double *__restrict__ p_prev,
+                                                    double *__restrict__ p_new, double *__restrict__ q, double *part,
+                                                    unsigned *counter, DevState *st) {
   __shared__ double sh[32];
   if (!st->p.active) return;
   const double beta = st->p.beta;
-  const long t = (long)blockIdx.x * blockDim.x + threadIdx.x;
-  const long row = t / G;
-  const bool valid = row < n;
-  double acc = 0.0;
-  if (valid) {
-    const int s = rp[row], e = rp[row + 1];
-    for (int k = s + (int)(threadIdx.x & (G - 1)); k < e; k += G) {
-      const int c = ci[k];
-      acc = fma(va[k], fma(beta, p_prev[c], z[c]), acc);
-    }
-  }
-  if (G > 1) {
-#pragma unroll
-    for (int o = G / 2; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o, G);
-  }
+  const long row = (long)blockIdx.x * blockDim.x + threadIdx.x;
   double v[1] = {0.0};
-  if (valid && (threadIdx.x & (G - 1)) == 0) {
+  if (row < n) {
+    const double acc = sell_dot(S, row, GatherPz{beta, p_prev, z});
     const double pi = fma(beta, p_prev[row], z[row]);
     const double w = wdiag ? wdiag[row] : 1.0;
     const double qi = fma(eps * w, pi, acc);

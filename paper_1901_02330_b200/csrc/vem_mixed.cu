@@ -57,6 +57,11 @@ struct Ctx {
   double *a_va = nullptr;
   int *s_rp = nullptr, *s_ci = nullptr;
   double *s_va = nullptr;
+  // SELL-32 copies used by every hot-path kernel
+  long long *a_soff = nullptr, *s_soff = nullptr;
+  int *a_sci = nullptr, *s_sci = nullptr;
+  double *a_sva = nullptr, *s_sva = nullptr;
+  long nnzA_sell = 0, nnzS_sell = 0;
   double *dMinv = nullptr, *dSinv = nullptr, *dSepsinv = nullptr, *wdiag = nullptr, *sdiag = nullptr;
   // work vectors
   double *V = nullptr, *Z = nullptr;
@@ -244,71 +249,44 @@ struct PcgVecBlkL {
   static void run(Ctx *c, const double *p);
 };
 
-template <int G>
-struct SpmvL {
-  static void run(Ctx *c, long row0, long nrows, const double *x, double *y, const double *b, int mode,
-                  const int *gate) {
-    k_spmv<G><<<grid_for(nrows * G), NT, 0, c->stream>>>(row0, nrows, c->a_rp, c->a_ci, c->a_va, x, y, b,
-                                                         mode, gate);
-  }
-};
-template <int G>
-struct ResidL {
-  static void run(Ctx *c, const double *x, const double *b, double *r, int use_x) {
-    k_residual_start<G><<<grid_for(c->n * G), NT, 0, c->stream>>>(c->n, c->a_rp, c->a_ci, c->a_va, x, b, r,
-                                                                  use_x, c->part, c->counter, c->st);
-  }
-};
-template <int G>
-struct ChebL {
-  static void run(Ctx *c, double *dold, double *dnew, double c1, double c2, int last, double *zp,
-                  const int *gate) {
-    k_cheb_step<G><<<grid_for(c->np * G), NT, 0, c->stream>>>(c->np, c->s_rp, c->s_ci, c->s_va, c->dSinv, c->cr,
-                                                              dold, dnew, c->cx, c1, c2, last, zp, gate);
-  }
-};
-template <int G>
-struct SchurSpmvL {
-  static void run(Ctx *c, const double *x, double *y, const int *gate) {
-    k_spmv<G><<<grid_for(c->np * G), NT, 0, c->stream>>>(0, c->np, c->s_rp, c->s_ci, c->s_va, x, y, nullptr, 0,
-                                                         gate);
-  }
-};
-template <int G>
-struct BrFinL {
-  static void run(Ctx *c, double *z, const int *gate) {
-    k_br_finish<G><<<grid_for(c->nu * G), NT, 0, c->stream>>>(c->nu, c->a_rp, c->a_ci, c->a_va, c->dMinv, c->px,
-                                                              z, gate);
-  }
-};
-template <int G>
-struct PcgSpmvL {
-  static void run(Ctx *c, const double *pprev, double *pnew) {
-    k_pcg_spmv<G><<<grid_for(c->np * G), NT, 0, c->stream>>>(c->np, c->s_rp, c->s_ci, c->s_va, c->dSepsinv,
-                                                             c->wdiag, c->eps, c->pr, pprev, pnew, c->pq,
-                                                             c->part, c->counter, c->st);
-  }
-};
+Sell sellA(Ctx *c) { return Sell{c->a_soff, c->a_sci, c->a_sva}; }
+Sell sellS(Ctx *c) { return Sell{c->s_soff, c->s_sci, c->s_sva}; }
+
+void launch_spmv(Ctx *c, long row0, long nrows, const double *x, double *y, const double *b, int mode,
+                 const int *gate) {
+  k_spmv<<<grid_for(nrows), NT, 0, c->stream>>>(row0, nrows, sellA(c), x, y, b, mode, gate);
+}
+void launch_residual(Ctx *c, const double *x, const double *b, double *r, int use_x) {
+  k_residual_start<<<grid_for(c->n), NT, 0, c->stream>>>(c->n, sellA(c), x, b, r, use_x, c->part, c->counter, c->st);
+}
+void launch_cheb(Ctx *c, double *dold, double *dnew, double c1, double c2, int last, double *zp, const int *gate) {
+  k_cheb_step<<<grid_for(c->np), NT, 0, c->stream>>>(c->np, sellS(c), c->dSinv, c->cr, dold, dnew, c->cx, c1, c2,
+                                                     last, zp, gate);
+}
+void launch_schur_spmv(Ctx *c, const double *x, double *y, const int *gate) {
+  k_spmv<<<grid_for(c->np), NT, 0, c->stream>>>(0, c->np, sellS(c), x, y, nullptr, 0, gate);
+}
+void launch_br_finish(Ctx *c, double *z, const int *gate) {
+  k_br_finish<<<grid_for(c->nu), NT, 0, c->stream>>>(c->nu, sellA(c), c->dMinv, c->px, z, gate);
+}
+void launch_pcg_spmv(Ctx *c, const double *pprev, double *pnew) {
+  k_pcg_spmv<<<grid_for(c->np), NT, 0, c->stream>>>(c->np, sellS(c), c->dSepsinv, c->wdiag, c->eps, c->pr, pprev,
+                                                    pnew, c->pq, c->part, c->counter, c->st);
+}
+void launch_cheb_resid(Ctx *c, const double *dold, const int *gate) {
+  k_cheb_resid<<<grid_for(c->np), NT, 0, c->stream>>>(c->np, sellS(c), c->cr, dold, gate);
+}
+void launch_pcg_spmv_z(Ctx *c, const double *pprev, double *pnew) {
+  k_pcg_spmv_z<<<grid_for(c->np), NT, 0, c->stream>>>(c->np, sellS(c), c->wdiag, c->eps, c->pz, pprev, pnew, c->pq,
+                                                      c->part, c->counter, c->st);
+}
 
 // algorithmic bytes per launch (include/vem_mixed.h)
-double bytes_spmv(Ctx *c) { return 12.0 * c->nnzA + 4.0 * (c->n + 1) + 16.0 * c->n; }
-double bytes_cheb(Ctx *c) { return 12.0 * c->nnzS + 4.0 * (c->np + 1) + 56.0 * c->np; }
+double bytes_spmv(Ctx *c) { return 12.0 * c->nnzA + 16.0 * c->n; }
+double bytes_cheb(Ctx *c) { return 12.0 * c->nnzS + 56.0 * c->np; }
 double bytes_pcg_vec(Ctx *c) { return 64.0 * c->np; }
 double bytes_vecs(Ctx *c, double nvec) { return 8.0 * c->n * nvec; }
 
-template <int G>
-struct ChebResidL {
-  static void run(Ctx *c, const double *dold, const int *gate) {
-    k_cheb_resid<G><<<grid_for(c->np * G), NT, 0, c->stream>>>(c->np, c->s_rp, c->s_ci, c->s_va, c->cr, dold, gate);
-  }
-};
-template <int G>
-struct PcgSpmvZL {
-  static void run(Ctx *c, const double *pprev, double *pnew) {
-    k_pcg_spmv_z<G><<<grid_for(c->np * G), NT, 0, c->stream>>>(c->np, c->s_rp, c->s_ci, c->s_va, c->wdiag, c->eps,
-                                                               c->pz, pprev, pnew, c->pq, c->part, c->counter, c->st);
-  }
-};
 template <int NB>
 void BlkInvL<NB>::run(Ctx *c, double shift, double *out) {
   const long ne = c->np / NB;
@@ -380,14 +358,14 @@ int enqueue_block_schur(Ctx *c, const double *v, const double *scale, double *z,
     const int last = i == deg - 1 ? 1 : 0;
     if (blk) {
       {
-        TimeScope ts(c, VEM_K_CHEB, 12.0 * c->nnzS + 4.0 * (c->np + 1) + 24.0 * c->np);
-        dispatch_g<ChebResidL>(c->gS, c, (const double *)dold, gate);
+        TimeScope ts(c, VEM_K_CHEB, 12.0 * c->nnzS + 24.0 * c->np);
+        launch_cheb_resid(c, (const double *)dold, gate);
       }
       TimeScope ts(c, VEM_K_PRECOND_VEC, 8.0 * c->np * (5 + c->nb));
       dispatch_nb<ChebBlkL>(c->nb, c, (const double *)dold, dnew, c1[i - 1], c2[i - 1], 0, last, z + c->nu, gate);
     } else {
       TimeScope ts(c, VEM_K_CHEB, bytes_cheb(c));
-      dispatch_g<ChebL>(c->gS, c, dold, dnew, c1[i - 1], c2[i - 1], last, z + c->nu, gate);
+      launch_cheb(c, dold, dnew, c1[i - 1], c2[i - 1], last, z + c->nu, gate);
     }
     std::swap(dold, dnew);
   }
@@ -406,7 +384,7 @@ int enqueue_block_reg(Ctx *c, const double *v, const double *scale, double *z, c
   }
   {
     TimeScope ts(c, VEM_K_PRECOND_VEC);  // rhs = B t0 (pressure rows of A)
-    dispatch_g<SpmvL>(c->gA, c, c->nu, c->np, (const double *)z, c->pb - c->nu, (const double *)nullptr, 0, gate);
+    launch_spmv(c, c->nu, c->np, (const double *)z, c->pb - c->nu, nullptr, 0, gate);
   }
   CKL();
   {
@@ -423,7 +401,7 @@ int enqueue_block_reg(Ctx *c, const double *v, const double *scale, double *z, c
   if (rc) return rc;
   {
     TimeScope ts(c, VEM_K_PRECOND_VEC);
-    dispatch_g<BrFinL>(c->gA, c, z, gate);
+    launch_br_finish(c, z, gate);
   }
   CKL();
   return 0;
@@ -436,14 +414,14 @@ int enqueue_pcg_steps(Ctx *c, int nsteps) {
     if (c->nb > 1) {
       {
         TimeScope ts(c, VEM_K_PCG_SPMV, bytes_cheb(c));
-        dispatch_g<PcgSpmvZL>(c->gS, c, (const double *)pprev, pnew);
+        launch_pcg_spmv_z(c, (const double *)pprev, pnew);
       }
       TimeScope ts(c, VEM_K_PCG_VEC, bytes_pcg_vec(c) + 8.0 * c->np * c->nb);
       dispatch_nb<PcgVecBlkL>(c->nb, c, (const double *)pnew);
     } else {
       {
         TimeScope ts(c, VEM_K_PCG_SPMV, bytes_cheb(c));
-        dispatch_g<PcgSpmvL>(c->gS, c, (const double *)pprev, pnew);
+        launch_pcg_spmv(c, (const double *)pprev, pnew);
       }
       TimeScope ts(c, VEM_K_PCG_VEC, bytes_pcg_vec(c));
       k_pcg_vec<<<grid_stream(c, c->np), NT, 0, c->stream>>>(c->np, c->dSepsinv, pnew, c->pq, c->px, c->pr,
@@ -526,7 +504,7 @@ int enqueue_arnoldi_step(Ctx *c, int kind, int j, int64_t *inner_its) {
   if (rc) return rc;
   {
     TimeScope ts(c, VEM_K_SPMV, bytes_spmv(c));
-    dispatch_g<SpmvL>(c->gA, c, 0L, c->n, (const double *)zj, w, (const double *)nullptr, 0, gate_active(c));
+    launch_spmv(c, 0L, c->n, (const double *)zj, w, nullptr, 0, gate_active(c));
   }
   const int nv = j + 1;
   const int gx = c->sm_count * 2;
@@ -569,7 +547,7 @@ int enqueue_cycle_end(Ctx *c, int kind, int64_t *inner_its) {
   }
   {
     TimeScope ts(c, VEM_K_SPMV, bytes_spmv(c) + 8.0 * c->n);
-    dispatch_g<ResidL>(c->gA, c, (const double *)c->x, (const double *)c->b, c->V, 1);
+    launch_residual(c, c->x, c->b, c->V, 1);
   }
   CKL();
   return 0;
@@ -631,7 +609,7 @@ int solve_impl(Ctx *c, const double *rhs, double tol, int maxit, int kind, doubl
   CK(cudaMemcpyAsync(&c->st->g, &c->hst->g, sizeof(g0), cudaMemcpyHostToDevice, c->stream));
   CK(cudaStreamSynchronize(c->stream));
   // beta0 = ||b||; V0 = b
-  dispatch_g<ResidL>(c->gA, c, (const double *)nullptr, (const double *)c->b, c->V, 0);
+  launch_residual(c, nullptr, c->b, c->V, 0);
   CKL();
   CK(cudaMemcpyAsync(&c->hst->g, &c->st->g, sizeof(GmresState), cudaMemcpyDeviceToHost, c->stream));
   CK(cudaStreamSynchronize(c->stream));
@@ -867,6 +845,33 @@ int build_schur(Ctx *c, const int64_t *brp, const int *bci, const double *bva, c
   return rcode;
 }
 
+int build_sell(Ctx *c, long nrows, const int *rp, const int *ci, const double *va, long long **soff, int **sci,
+               double **sva, long *nnz_sell) {
+  const long nsl = (nrows + 31) / 32;
+  long long *w = nullptr;
+  DA(w, nsl + 1);
+  DA(*soff, nsl + 1);
+  k_sell_width<<<grid_stream(c, nsl), NT, 0, c->stream>>>(nrows, rp, w);
+  CKL();
+  CK(cudaMemsetAsync(w + nsl, 0, sizeof(long long), c->stream));
+  size_t tb = 0;
+  CK(cub::DeviceScan::ExclusiveSum(nullptr, tb, w, *soff, (int)(nsl + 1), c->stream));
+  char *tmp = nullptr;
+  DA(tmp, tb);
+  CK(cub::DeviceScan::ExclusiveSum(tmp, tb, w, *soff, (int)(nsl + 1), c->stream));
+  long long tot = 0;
+  CK(cudaMemcpyAsync(&tot, *soff + nsl, sizeof(long long), cudaMemcpyDeviceToHost, c->stream));
+  CK(cudaStreamSynchronize(c->stream));
+  dfree(c, tmp);
+  dfree(c, w);
+  DA(*sci, tot);
+  DA(*sva, tot);
+  k_sell_fill<<<grid_stream(c, nsl * 32), NT, 0, c->stream>>>(nrows, rp, ci, va, *soff, *sci, *sva);
+  CKL();
+  *nnz_sell = (long)tot;
+  return 0;
+}
+
 int upload_impl(Ctx *c, const vem_csr *M, const vem_csr *B, const vem_csr *W, double eps, const vem_layout *lay) {
   auto t0 = std::chrono::steady_clock::now();
   if (!M || !B) return fail(c, VEM_ERR_INVALID, "M and B are required");
@@ -1048,7 +1053,19 @@ int upload_impl(Ctx *c, const vem_csr *M, const vem_csr *B, const vem_csr *W, do
   }
   c->gA = pick_group((double)c->nnzA / c->n);
   c->gS = pick_group((double)c->nnzS / c->np);
+  {
+    int rr = build_sell(c, c->n, c->a_rp, c->a_ci, c->a_va, &c->a_soff, &c->a_sci, &c->a_sva, &c->nnzA_sell);
+    if (rr) return rr;
+    rr = build_sell(c, c->np, c->s_rp, c->s_ci, c->s_va, &c->s_soff, &c->s_sci, &c->s_sva, &c->nnzS_sell);
+    if (rr) return rr;
+  }
   CK(cudaStreamSynchronize(c->stream));
+  dfree(c, c->a_rp);
+  dfree(c, c->a_ci);
+  dfree(c, c->a_va);
+  c->a_rp = nullptr;
+  c->a_ci = nullptr;
+  c->a_va = nullptr;
   for (void *p : {(void *)mrp, (void *)mci, (void *)mva, (void *)brp, (void *)bci, (void *)bva, (void *)btrp,
                   (void *)btci, (void *)btva, (void *)fill, (void *)brp32, (void *)len})
     dfree(c, p);
@@ -1186,7 +1203,7 @@ int vem_mixed_spmv(vem_ctx *h, const double *x, double *y) {
   Ctx *c = h->impl;
   int r = enter(c);
   if (r) return r;
-  dispatch_g<SpmvL>(c->gA, c, 0L, c->n, x, y, (const double *)nullptr, 0, gate_one(c));
+  launch_spmv(c, 0L, c->n, x, y, nullptr, 0, gate_one(c));
   CKL();
   CK(cudaStreamSynchronize(c->stream));
   return leave(c, VEM_OK);
@@ -1197,7 +1214,7 @@ int vem_mixed_schur_spmv(vem_ctx *h, const double *x, double *y) {
   Ctx *c = h->impl;
   int r = enter(c);
   if (r) return r;
-  dispatch_g<SchurSpmvL>(c->gS, c, x, y, gate_one(c));
+  launch_schur_spmv(c, x, y, gate_one(c));
   CKL();
   CK(cudaStreamSynchronize(c->stream));
   return leave(c, VEM_OK);

@@ -101,11 +101,24 @@ def test_block_reg_apply_parity(name):
 
 # (config, preconditioner) pairs of BASELINE.json at reduced size, plus C1/C3s Block-Reg.
 SOLVE_CASES = [("C1", 1), ("C1", 2), ("C3s", 1), ("C3s", 2), ("C2s", 1), ("C2s", 2), ("C4s", 1), ("C4s", 2)]
-# C1 + Block-Reg is not a BASELINE pair: with K = I and the sin source the RHS is
-# (nearly) an eigenvector, GMRES stalls on the 1/eps-scaled pressure block after
-# 3-4 steps and the restart pattern is decided by rounding; its
-# iteration count is reported, not asserted.
-ITER_EXEMPT = {("C1", 2)}
+
+
+def oracle_iteration_band(s, kind, restart, eps, trials=3):
+    """DESIGN.md reading R20: restarted GMRES iteration counts can be
+    ill-conditioned (a cycle that ends with the estimate just above rtol
+    restarts; just below, it stops).  The oracle's own count is therefore taken
+    as the set of counts over the unperturbed RHS and `trials` RHS perturbed by
+    1e-15 relative (a few ulps); the GPU must land within +-2 of that band."""
+    rng = np.random.default_rng(99)
+    its = []
+    ref = None
+    for t in range(trials + 1):
+        rhs = s.rhs if t == 0 else s.rhs * (1 + 1e-15 * rng.normal(size=s.rhs.size))
+        r = O.solve(s.M, s.B, rhs, kind, 1e-10, restart, eps=eps, block=s.layout.n_p_dof)
+        assert r.converged
+        its.append(r.iterations)
+        ref = ref or r
+    return ref, min(its), max(its)
 
 
 @pytest.mark.parametrize("name,kind", SOLVE_CASES)
@@ -113,15 +126,13 @@ def test_solve_parity(name, kind):
     s = system(name)
     cfg = configs.CONFIGS[name]
     eps = configs.eps_for(s)
-    ref = O.solve(s.M, s.B, s.rhs, kind, 1e-10, cfg.restart, eps=eps, block=s.layout.n_p_dof)
-    assert ref.converged
+    ref, lo, hi = oracle_iteration_band(s, kind, cfg.restart, eps)
     sv = solver_for(s, restart=cfg.restart)
     res = sv.solve(torch.from_numpy(s.rhs).cuda(), 1e-10, 10000, kind)
     r = res.report
     assert r["status"] == 0 and r["converged"] == 1, r
-    print(f"{name} precond={kind}: gpu {r['iterations']} oracle {ref.iterations} its")
-    if (name, kind) not in ITER_EXEMPT:
-        assert abs(r["iterations"] - ref.iterations) <= 2, (r["iterations"], ref.iterations)
+    print(f"{name} precond={kind}: gpu {r['iterations']} oracle {ref.iterations} band [{lo}, {hi}] its")
+    assert lo - 2 <= r["iterations"] <= hi + 2, (r["iterations"], lo, hi)
     nu = s.layout.n_u
     assert rel_inf(res.u.cpu().numpy(), ref.x[:nu]) <= 1e-8
     assert rel_inf(res.p.cpu().numpy(), ref.x[nu:]) <= 1e-8
