@@ -70,7 +70,7 @@ typedef struct {
 } vem_layout;
 
 typedef struct {
-  int32_t restart;        /* m, GMRES(m) restart length (default 30)                      */
+  int32_t restart;        /* m, GMRES(m) restart length, 1..100 (default 30)              */
   int32_t cheb_degree;    /* d, Chebyshev degree of the Block-Schur B_2 apply (default 16) */
   double  cheb_ratio;     /* lambda_max / lambda_min of the Chebyshev interval (default 30) */
   double  inner_rtol;     /* Block-Reg inner PCG relative tolerance (default 1e-14)        */

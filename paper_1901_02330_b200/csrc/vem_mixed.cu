@@ -508,19 +508,18 @@ int enqueue_arnoldi_step(Ctx *c, int kind, int j, int64_t *inner_its) {
   }
   const int nv = j + 1;
   const int gx = c->sm_count * 2;
-  for (int pass = 1; pass <= 2; ++pass) {
-    const int nout = nv + (pass == 1 ? 1 : 0);
-    dim3 grid(gx, (nout + VEM_DOT_CHUNK - 1) / VEM_DOT_CHUNK);
-    {
-      TimeScope ts(c, VEM_K_DOT, bytes_vecs(c, nv + 1));
-      k_mdot<<<grid, NT, 0, c->stream>>>(c->n, c->V, c->ldv, nv, pass == 1 ? 1 : 0, w, c->part, c->counter, c->st,
-                                         pass);
-    }
-    {
-      TimeScope ts(c, VEM_K_UPDATE, bytes_vecs(c, nv + 2));
-      k_update<<<gx * 2, NT, 0, c->stream>>>(c->n, c->V, c->ldv, nv, w, pass == 2 ? 1 : 0, c->part, c->counter,
-                                             c->st, j);
-    }
+  const size_t smem = (size_t)(2 * (nv + 1) * VEM_TILE + 2 * (nv + 2)) * sizeof(double);
+  {
+    TimeScope ts(c, VEM_K_DOT, bytes_vecs(c, nv + 1));
+    k_cgs_pass<0><<<gx, VEM_TILE, smem, c->stream>>>(c->n, c->V, c->ldv, nv, w, c->part, c->counter, c->st, 1);
+  }
+  {
+    TimeScope ts(c, VEM_K_DOT, bytes_vecs(c, nv + 2));   // update + second dot, one read of V
+    k_cgs_pass<1><<<gx, VEM_TILE, smem, c->stream>>>(c->n, c->V, c->ldv, nv, w, c->part, c->counter, c->st, 2);
+  }
+  {
+    TimeScope ts(c, VEM_K_UPDATE, bytes_vecs(c, nv + 2));
+    k_update<<<gx * 2, NT, 0, c->stream>>>(c->n, c->V, c->ldv, nv, w, 1, c->part, c->counter, c->st, j);
   }
   CKL();
   return 0;
@@ -573,7 +572,13 @@ void destroy_graphs(Ctx *c) {
 
 int ensure_work(Ctx *c, int kind) {
   const int m = c->opts.restart;
-  if (!c->V) DA(c->V, (size_t)(m + 1) * c->ldv);
+  if (!c->V) {
+    DA(c->V, (size_t)(m + 1) * c->ldv);
+    CK(cudaMemsetAsync(c->V, 0, (size_t)(m + 1) * c->ldv * sizeof(double), c->stream));
+    const int smax = (int)((2 * (m + 2) * VEM_TILE + 2 * (m + 3)) * sizeof(double));
+    CK(cudaFuncSetAttribute(k_cgs_pass<0>, cudaFuncAttributeMaxDynamicSharedMemorySize, smax));
+    CK(cudaFuncSetAttribute(k_cgs_pass<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, smax));
+  }
   if (kind == VEM_PRECOND_BLOCK_REG && c->zcap < m) {
     if (c->Z) dfree(c, c->Z);
     c->Z = nullptr;
@@ -901,7 +906,7 @@ int upload_impl(Ctx *c, const vem_csr *M, const vem_csr *B, const vem_csr *W, do
       if (W->indptr[i + 1] - W->indptr[i] != 1 || W->indices[W->indptr[i]] != i || !(W->values[W->indptr[i]] > 0))
         return fail(c, VEM_ERR_INVALID, "W must be diagonal with positive entries");
   }
-  c->ldv = (c->n + 31) / 32 * 32;
+  c->ldv = (c->n + VEM_TILE - 1) / VEM_TILE * VEM_TILE;   // tiles of the CGS passes never leave a vector
   cudaDeviceProp prop;
   int dev = 0;
   CK(cudaGetDevice(&dev));
@@ -1121,7 +1126,7 @@ void vem_mixed_default_options(vem_opts *o) {
 }
 
 static int validate_opts(Ctx *c, const vem_opts *o) {
-  if (o->restart < 1 || o->restart > VEM_MAXM) return fail(c, VEM_ERR_INVALID, "restart must be in [1, %d]", VEM_MAXM);
+  if (o->restart < 1 || o->restart > 100) return fail(c, VEM_ERR_INVALID, "restart must be in [1, 100]");
   if (o->cheb_degree < 1) return fail(c, VEM_ERR_INVALID, "cheb_degree must be >= 1");
   if (!(o->cheb_ratio > 1.0)) return fail(c, VEM_ERR_INVALID, "cheb_ratio must be > 1");
   if (!(o->inner_rtol > 0.0) || o->inner_maxit < 1) return fail(c, VEM_ERR_INVALID, "bad inner PCG options");

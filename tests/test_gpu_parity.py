@@ -207,11 +207,10 @@ def test_invalid_uploads():
 @pytest.mark.parametrize("n,k", [(1, 0), (1, 1), (3, 2), (5, 0), (3, 1)])
 def test_tiny_and_ragged_meshes(n, k):
     s = build_system(mesh.cube_mesh(n), k)
-    ref = O.solve(s.M, s.B, s.rhs, 1, 1e-10, 30, block=s.layout.n_p_dof)
-    assert ref.converged
+    ref, lo, hi = oracle_iteration_band(s, 1, 30, 0.0)
     sv = solver_for(s)
     res = sv.solve(torch.from_numpy(s.rhs).cuda(), 1e-10, 10000, 1)
-    assert abs(res.report["iterations"] - ref.iterations) <= 2
+    assert lo - 2 <= res.report["iterations"] <= hi + 2, (res.report["iterations"], lo, hi)
     x = np.concatenate([res.u.cpu().numpy(), res.p.cpu().numpy()])
     nu = s.layout.n_u
     assert rel_inf(x[:nu], ref.x[:nu]) <= 1e-8 and rel_inf(x[nu:], ref.x[nu:]) <= 1e-8
