@@ -491,106 +491,7 @@ __global__ void __launch_bounds__(256) k_mdot(long n, const double *__restrict__
   }
 }
 
-// ---------------------------------------------------------------------------
-// Tiled CGS pass (one read of the basis per pass).  A persistent block walks
-// 128-element tiles; for each tile the nv basis rows are staged into shared
-// memory with cp.async (16-byte LDGSTS, double-buffered so tile t+1 streams in
-// while tile t is consumed) together with w.
-//   UPDATE = 0:  partial dots V_o . w (o < nv) and w . w            (pass 1)
-//   UPDATE = 1:  w -= sum_o coef_o V_o (written back), then partial
-//                dots V_o . w_new                                     (pass 2 fused)
-// Each warp owns the vectors o = warp, warp + 4, ... and accumulates its tile
-// sums in shared memory in a fixed order (deterministic); the per-block
-// results go to part[o * gridDim.x + block] and the last block reduces them.
-// ---------------------------------------------------------------------------
 #define VEM_TILE 128
-__device__ __forceinline__ void cp_async16(void *smem, const void *gmem) {
-  const unsigned sa = (unsigned)__cvta_generic_to_shared(smem);
-  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(sa), "l"(gmem));
-}
-__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::); }
-template <int N>
-__device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;\n" ::"n"(N)); }
-
-__device__ __forceinline__ void stage_tile(double *buf, const double *__restrict__ V, long ldv, int nv,
-                                           const double *__restrict__ w, long t) {
-  // rows 0..nv-1: basis vectors; row nv: w.  16-byte chunks: 64 per 128-double row.
-  const int chunks = (nv + 1) * (VEM_TILE / 2);
-  for (int q = threadIdx.x; q < chunks; q += blockDim.x) {
-    const int o = q / (VEM_TILE / 2), c = q % (VEM_TILE / 2);
-    const double *src = (o < nv ? V + (size_t)o * ldv : w) + t * VEM_TILE + 2 * c;
-    cp_async16(buf + (size_t)o * VEM_TILE + 2 * c, src);
-  }
-}
-
-template <int UPDATE>
-__global__ void __launch_bounds__(VEM_TILE) k_cgs_pass(long n, const double *__restrict__ V, long ldv, int nv,
-                                                       double *__restrict__ w, double *part, unsigned *counter,
-                                                       DevState *st, int pass) {
-  extern __shared__ double smem[];
-  if (!st->g.active) return;
-  const int nrow = nv + 1;
-  double *buf0 = smem, *buf1 = smem + (size_t)nrow * VEM_TILE;
-  double *acc = buf1 + (size_t)nrow * VEM_TILE;      // nv + 1 accumulators
-  double *cf = acc + nrow;                            // nv coefficients
-  for (int o = threadIdx.x; o < nrow; o += blockDim.x) acc[o] = 0.0;
-  if (UPDATE)
-    for (int o = threadIdx.x; o < nv; o += blockDim.x) cf[o] = st->coef[o];
-  const long ntiles = (n + VEM_TILE - 1) / VEM_TILE;
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
-  long t = blockIdx.x;
-  if (t < ntiles) stage_tile(buf0, V, ldv, nv, w, t);
-  cp_async_commit();
-  int cur = 0;
-  for (; t < ntiles; t += gridDim.x) {
-    const long tn = t + gridDim.x;
-    double *bc = cur ? buf1 : buf0, *bn = cur ? buf0 : buf1;
-    if (tn < ntiles) stage_tile(bn, V, ldv, nv, w, tn);
-    cp_async_commit();
-    cp_async_wait<1>();
-    __syncthreads();
-    double *wt = bc + (size_t)nv * VEM_TILE;
-    const long i = t * VEM_TILE + threadIdx.x;
-    if (UPDATE) {
-      double wi = wt[threadIdx.x];
-      for (int o = 0; o < nv; ++o) wi = fma(-cf[o], bc[(size_t)o * VEM_TILE + threadIdx.x], wi);
-      if (i < n) w[i] = wi;
-      wt[threadIdx.x] = i < n ? wi : 0.0;
-      __syncthreads();
-    } else if (i >= n) {
-      wt[threadIdx.x] = 0.0;
-      __syncthreads();
-    }
-    const int nout = UPDATE ? nv : nrow;   // pass 1 also returns w . w
-    for (int o = warp; o < nout; o += nw) {
-      const double *vr = bc + (size_t)o * VEM_TILE;
-      double sdot = 0.0;
-#pragma unroll
-      for (int l = lane; l < VEM_TILE; l += 32) sdot = fma(vr[l], wt[l], sdot);
-      sdot = warp_sum(sdot);
-      if (lane == 0) acc[o] += sdot;
-    }
-    __syncthreads();
-    cur ^= 1;
-  }
-  cp_async_wait<0>();
-  __syncthreads();
-  const int nout = UPDATE ? nv : nrow;
-  for (int o = threadIdx.x; o < nout; o += blockDim.x) part[(size_t)o * gridDim.x + blockIdx.x] = acc[o];
-  if (elect_last_block(counter)) {
-    __shared__ double tot[VEM_MAXM + 2];
-    reduce_partials<1>(part, gridDim.x, nout, tot);
-    if (threadIdx.x == 0) {
-      for (int o = 0; o < nv; ++o) {
-        const double h = st->vscale[o] * tot[o];
-        st->coef[o] = h * st->vscale[o];
-        st->h1[o] = (pass == 1) ? h : st->h1[o] + h;
-      }
-      if (!UPDATE) st->g.wnorm0 = sqrt(tot[nv]);
-      *counter = 0u;
-    }
-  }
-}
 
 // Givens step for column j, executed by one thread.
 __device__ void givens_column(DevState *st, int j, double hn) {

@@ -508,18 +508,19 @@ int enqueue_arnoldi_step(Ctx *c, int kind, int j, int64_t *inner_its) {
   }
   const int nv = j + 1;
   const int gx = c->sm_count * 2;
-  const size_t smem = (size_t)(2 * (nv + 1) * VEM_TILE + 2 * (nv + 2)) * sizeof(double);
-  {
-    TimeScope ts(c, VEM_K_DOT, bytes_vecs(c, nv + 1));
-    k_cgs_pass<0><<<gx, VEM_TILE, smem, c->stream>>>(c->n, c->V, c->ldv, nv, w, c->part, c->counter, c->st, 1);
-  }
-  {
-    TimeScope ts(c, VEM_K_DOT, bytes_vecs(c, nv + 2));   // update + second dot, one read of V
-    k_cgs_pass<1><<<gx, VEM_TILE, smem, c->stream>>>(c->n, c->V, c->ldv, nv, w, c->part, c->counter, c->st, 2);
-  }
-  {
-    TimeScope ts(c, VEM_K_UPDATE, bytes_vecs(c, nv + 2));
-    k_update<<<gx * 2, NT, 0, c->stream>>>(c->n, c->V, c->ldv, nv, w, 1, c->part, c->counter, c->st, j);
+  for (int pass = 1; pass <= 2; ++pass) {
+    const int nout = nv + (pass == 1 ? 1 : 0);
+    dim3 grid(gx, (nout + VEM_DOT_CHUNK - 1) / VEM_DOT_CHUNK);
+    {
+      TimeScope ts(c, VEM_K_DOT, bytes_vecs(c, nv + 1));
+      k_mdot<<<grid, NT, 0, c->stream>>>(c->n, c->V, c->ldv, nv, pass == 1 ? 1 : 0, w, c->part, c->counter, c->st,
+                                         pass);
+    }
+    {
+      TimeScope ts(c, VEM_K_UPDATE, bytes_vecs(c, nv + 2));
+      k_update<<<gx * 2, NT, 0, c->stream>>>(c->n, c->V, c->ldv, nv, w, pass == 2 ? 1 : 0, c->part, c->counter,
+                                             c->st, j);
+    }
   }
   CKL();
   return 0;
@@ -575,9 +576,6 @@ int ensure_work(Ctx *c, int kind) {
   if (!c->V) {
     DA(c->V, (size_t)(m + 1) * c->ldv);
     CK(cudaMemsetAsync(c->V, 0, (size_t)(m + 1) * c->ldv * sizeof(double), c->stream));
-    const int smax = (int)((2 * (m + 2) * VEM_TILE + 2 * (m + 3)) * sizeof(double));
-    CK(cudaFuncSetAttribute(k_cgs_pass<0>, cudaFuncAttributeMaxDynamicSharedMemorySize, smax));
-    CK(cudaFuncSetAttribute(k_cgs_pass<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, smax));
   }
   if (kind == VEM_PRECOND_BLOCK_REG && c->zcap < m) {
     if (c->Z) dfree(c, c->Z);
