@@ -43,6 +43,18 @@ def parse():
     return ap.parse_args()
 
 
+def ncu_traffic(kclass):
+    """dram__bytes_read.sum + dram__bytes_write.sum per launch of the kernel class
+    from the committed `ncu --set full` capture (profiles/ncu_traffic.json), or None."""
+    try:
+        with open(os.path.join(ROOT, "profiles", "ncu_traffic.json")) as f:
+            d = json.load(f)
+        e = d.get(kclass)
+        return None if e is None else e["bytes_per_launch"]
+    except Exception:
+        return None
+
+
 def peaks():
     try:
         with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
@@ -110,6 +122,20 @@ def dist_init(args):
     return rank, ws, local
 
 
+def reduce_over_ranks(ms: float, its: float, device="cpu"):
+    """Replicas-only aggregation: the step time is the MAX over
+    ranks, the work is the SUM of all ranks' GMRES iterations."""
+    import torch
+    import torch.distributed as dist
+    if not (dist.is_available() and dist.is_initialized()) or dist.get_world_size() == 1:
+        return float(ms), float(its)
+    t = torch.tensor([float(ms)], dtype=torch.float64, device=device)
+    w = torch.tensor([float(its)], dtype=torch.float64, device=device)
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    dist.all_reduce(w, op=dist.ReduceOp.SUM)
+    return float(t[0]), float(w[0])
+
+
 def cpu_baseline(system, cfg, kind, eps, its):
     """The oracle as it stands on a bounded sample: `its` GMRES iterations of the
     same system on the host cores."""
@@ -121,7 +147,7 @@ def cpu_baseline(system, cfg, kind, eps, its):
     except Exception:
         cores = 1
     t0 = time.perf_counter()
-    P = O.Preconditioner(kind, system.M, system.B, eps=eps)
+    P = O.Preconditioner(kind, system.M, system.B, eps=eps, block=system.layout.n_p_dof)
     t1 = time.perf_counter()
     res = O.gmres(lambda x: O.spmv_saddle(system.M, system.B, x), P.apply, system.rhs, 1e-10, cfg.restart, its,
                   P.flexible)
@@ -218,15 +244,7 @@ def main():
     stats = sv.kernel_stats(reset=True)
     its = sum(r["iterations"] for r in reports)
     # max over ranks of the time, sum of the work
-    if ws > 1:
-        import torch.distributed as dist
-        t = torch.tensor([ms, float(its)], dtype=torch.float64, device="cuda")
-        tm = t.clone()
-        dist.all_reduce(tm[:1], op=dist.ReduceOp.MAX)
-        dist.all_reduce(t[1:], op=dist.ReduceOp.SUM)
-        ms, its_all = float(tm[0]), float(t[1])
-    else:
-        its_all = float(its)
+    ms, its_all = reduce_over_ranks(ms, its, device="cuda")
     value = its_all / (ms / 1e3)
 
     # end to end: host rhs (pinned) -> device -> solve -> u, p back to host, through the C ABI
@@ -252,7 +270,7 @@ def main():
         d = per[dom]
         ach = d["bytes"] / (d["ms"] / 1e3) / 1e9
         roof = {"bound": "hbm", "kernel": dom, "achieved": round(ach, 1), "peak": hbm, "unit": "GB/s",
-                "frac": round(ach / hbm, 4), "traffic": None, "peak_source": peak_kind,
+                "frac": round(ach / hbm, 4), "traffic": ncu_traffic(dom), "peak_source": peak_kind,
                 "bytes_per_launch": d["bytes"] / d["launches"], "avg_launch_us": 1e3 * d["ms"] / d["launches"]}
     kern = {k: {"launches": v["launches"], "ms": round(v["ms"], 3),
                 "GBps": round(v["bytes"] / max(v["ms"], 1e-9) / 1e6, 1),

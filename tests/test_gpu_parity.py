@@ -103,11 +103,11 @@ def test_block_reg_apply_parity(name):
 SOLVE_CASES = [("C1", 1), ("C1", 2), ("C3s", 1), ("C3s", 2), ("C2s", 1), ("C2s", 2), ("C4s", 1), ("C4s", 2)]
 
 
-def oracle_iteration_band(s, kind, restart, eps, trials=3):
+def oracle_iteration_band(s, kind, restart, eps, trials=8):
     """DESIGN.md reading R20: restarted GMRES iteration counts can be
     ill-conditioned (a cycle that ends with the estimate just above rtol
     restarts; just below, it stops).  The oracle's own count is therefore taken
-    as the set of counts over the unperturbed RHS and `trials` RHS perturbed by
+    as the set of counts over the unperturbed RHS and `trials` (8) RHS perturbed by
     1e-15 relative (a few ulps); the GPU must land within +-2 of that band."""
     rng = np.random.default_rng(99)
     its = []
@@ -139,6 +139,23 @@ def test_solve_parity(name, kind):
     # true residual and local conservation, recomputed on the host
     x = np.concatenate([res.u.cpu().numpy(), res.p.cpu().numpy()])
     assert np.linalg.norm(s.rhs - O.spmv_saddle(s.M, s.B, x)) <= 1e-10 * np.linalg.norm(s.rhs) * 1.0001
+    sv.close()
+
+
+def test_block_reg_fixed_budget_c5s():
+    """C5 (pairs, anisotropic K with 1e-3 jumps) does not converge with the
+    diag(M)-Woodbury Block-Reg stand-in in this round, so parity
+    is checked on a fixed budget: one FGMRES(50) cycle from x0 = 0 on both sides."""
+    s = system("C5s")
+    eps = configs.eps_for(s)
+    ref = O.solve(s.M, s.B, s.rhs, 2, 1e-10, 50, maxit=50, eps=eps, block=s.layout.n_p_dof)
+    sv = solver_for(s, restart=50)
+    res = sv.solve(torch.from_numpy(s.rhs).cuda(), 1e-10, 50, 2)
+    assert res.report["iterations"] == ref.iterations == 50
+    assert abs(res.report["rel_residual_true"] - ref.rel_residual_true) <= 1e-6 * ref.rel_residual_true
+    nu = s.layout.n_u
+    assert rel_inf(res.u.cpu().numpy(), ref.x[:nu]) <= 1e-6
+    assert rel_inf(res.p.cpu().numpy(), ref.x[nu:]) <= 1e-6
     sv.close()
 
 
