@@ -558,62 +558,6 @@ __global__ void __launch_bounds__(256) k_update(long n, const double *__restrict
   }
 }
 
-// CGS2 pass 2 fused: w -= sum_{o<nv} coef_o V_o (first projection), then the
-// reorthogonalisation dots V_o . w_new, with ONE read of the basis from HBM: each
-// thread re-reads its own V_o[i] right after the update, while the line is still
-// in L1 (one 256-thread block per SM keeps the working set 256 * nv * 8 B in
-// L1).  Per-warp partial sums go through shuffles into per-warp shared
-// accumulators (fixed order), then a fixed-order block sum; the last block
-// finishes the coefficients exactly as k_mdot pass 2 does.
-__global__ void __launch_bounds__(256, 1) k_update_dot(long n, const double *__restrict__ V, long ldv, int nv,
-                                                       double *__restrict__ w, double *part, unsigned *counter,
-                                                       DevState *st) {
-  __shared__ double cf[VEM_MAXM + 1];
-  __shared__ double wacc[8][VEM_MAXM + 1];
-  if (!st->g.active) return;
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  for (int o = threadIdx.x; o < nv; o += blockDim.x) cf[o] = st->coef[o];
-  for (int o = lane; o < nv; o += 32) wacc[warp][o] = 0.0;
-  __syncthreads();
-  const long stride = (long)gridDim.x * blockDim.x;
-  const long nit = (n + stride - 1) / stride;
-  for (long it = 0; it < nit; ++it) {
-    const long i = it * stride + (long)blockIdx.x * blockDim.x + threadIdx.x;
-    const bool ok = i < n;
-    double wi = 0.0;
-    if (ok) {
-      wi = w[i];
-#pragma unroll 8
-      for (int o = 0; o < nv; ++o) wi = fma(-cf[o], __ldg(V + (size_t)o * ldv + i), wi);
-      w[i] = wi;
-    }
-#pragma unroll 4
-    for (int o = 0; o < nv; ++o) {
-      double pr = ok ? __ldg(V + (size_t)o * ldv + i) * wi : 0.0;
-      pr = warp_sum(pr);
-      if (lane == 0) wacc[warp][o] += pr;
-    }
-  }
-  __syncthreads();
-  for (int o = threadIdx.x; o < nv; o += blockDim.x) {
-    double t = 0.0;
-    for (int q = 0; q < (int)(blockDim.x >> 5); ++q) t += wacc[q][o];
-    part[(size_t)o * gridDim.x + blockIdx.x] = t;
-  }
-  if (elect_last_block(counter)) {
-    __shared__ double tot[VEM_MAXM + 2];
-    reduce_partials<1>(part, gridDim.x, nv, tot);
-    if (threadIdx.x == 0) {
-      for (int o = 0; o < nv; ++o) {
-        const double h = st->vscale[o] * tot[o];
-        st->coef[o] = h * st->vscale[o];
-        st->h1[o] += h;
-      }
-      *counter = 0u;
-    }
-  }
-}
-
 // y = R^-1 g (back substitution on the rotated Hessenberg), coef_i = y_i * scale_i
 __global__ void k_backsolve(DevState *st, int use_vscale) {
   if (threadIdx.x != 0 || blockIdx.x != 0) return;

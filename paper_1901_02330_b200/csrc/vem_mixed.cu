@@ -508,18 +508,19 @@ int enqueue_arnoldi_step(Ctx *c, int kind, int j, int64_t *inner_its) {
   }
   const int nv = j + 1;
   const int gx = c->sm_count * 2;
-  {  // pass 1: h1 = V^T w and ||w|| (for the breakdown test)
-    dim3 grid(gx, (nv + 1 + VEM_DOT_CHUNK - 1) / VEM_DOT_CHUNK);
-    TimeScope ts(c, VEM_K_DOT, bytes_vecs(c, nv + 1));
-    k_mdot<<<grid, NT, 0, c->stream>>>(c->n, c->V, c->ldv, nv, 1, w, c->part, c->counter, c->st, 1);
-  }
-  {  // w -= V h1 fused with h2 = V^T w (one HBM read of V)
-    TimeScope ts(c, VEM_K_DOT, bytes_vecs(c, nv + 2));
-    k_update_dot<<<c->sm_count, NT, 0, c->stream>>>(c->n, c->V, c->ldv, nv, w, c->part, c->counter, c->st);
-  }
-  {  // w -= V h2, ||w||, Givens
-    TimeScope ts(c, VEM_K_UPDATE, bytes_vecs(c, nv + 2));
-    k_update<<<gx * 2, NT, 0, c->stream>>>(c->n, c->V, c->ldv, nv, w, 1, c->part, c->counter, c->st, j);
+  for (int pass = 1; pass <= 2; ++pass) {
+    const int nout = nv + (pass == 1 ? 1 : 0);
+    dim3 grid(gx, (nout + VEM_DOT_CHUNK - 1) / VEM_DOT_CHUNK);
+    {
+      TimeScope ts(c, VEM_K_DOT, bytes_vecs(c, nv + 1));
+      k_mdot<<<grid, NT, 0, c->stream>>>(c->n, c->V, c->ldv, nv, pass == 1 ? 1 : 0, w, c->part, c->counter, c->st,
+                                         pass);
+    }
+    {
+      TimeScope ts(c, VEM_K_UPDATE, bytes_vecs(c, nv + 2));
+      k_update<<<gx * 2, NT, 0, c->stream>>>(c->n, c->V, c->ldv, nv, w, pass == 2 ? 1 : 0, c->part, c->counter,
+                                             c->st, j);
+    }
   }
   CKL();
   return 0;
