@@ -40,6 +40,7 @@ def parse():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-sample-its", type=int, default=6)
     ap.add_argument("--graphs", action="store_true", help="time with CUDA graphs instead of per-launch events")
+    ap.add_argument("--reorth", type=int, default=1, help="1: CGS2 (default), 0: CGS1")
     return ap.parse_args()
 
 
@@ -210,7 +211,7 @@ def main():
     t_asm = time.perf_counter() - t0
     eps = eps_for(s)
     opts = pkg.default_options(restart=cfg.restart, use_graphs=1 if args.graphs else 0,
-                               timing=0 if args.graphs else 1)
+                               timing=0 if args.graphs else 1, reorth=args.reorth)
     t0 = time.perf_counter()
     sv = pkg.VemMixed(s.M, s.B, eps=eps, layout=s.layout, opts=opts)
     t_up = time.perf_counter() - t0
@@ -283,6 +284,7 @@ def main():
             "config": {"workload": f"{cfg.name}: {cfg.describe}", "n_dofs": s.n, "n_u": s.layout.n_u,
                        "n_p": s.layout.n_p, "nnz_A": info["nnz_A"], "nnz_S": info["nnz_S"],
                        "precond": kind, "restart": cfg.restart, "rtol": cfg.rtol,
+                       "orthogonalisation": "CGS2" if args.reorth else "CGS1",
                        "iterations_per_solve": [r["iterations"] for r in reports],
                        "time_to_solution_ms": ms / args.steps,
                        "rel_residual_true": reports[-1]["rel_residual_true"],

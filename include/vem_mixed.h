@@ -78,6 +78,7 @@ typedef struct {
   int32_t use_graphs;     /* 1: replay GMRES cycles / PCG chunks as CUDA graphs (default)  */
   int32_t timing;         /* 1: time every kernel launch with CUDA events (stats below)    */
   int32_t pcg_chunk;      /* PCG steps per host convergence poll (default 16)              */
+  int32_t reorth;         /* 1: CGS2 (default), 0: CGS1 (one projection pass)              */
 } vem_opts;
 
 typedef struct {

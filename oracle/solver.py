@@ -216,10 +216,10 @@ class GmresResult:
     history: list
 
 
-def gmres(matvec, precond, b, rtol=1e-10, restart=30, maxit=10000, flexible=False):
+def gmres(matvec, precond, b, rtol=1e-10, restart=30, maxit=10000, flexible=False, reorth=1):
     """Right-preconditioned restarted GMRES(m) (flexible=True: FGMRES(m), which
     stores Z_j = P^-1 v_j), x0 = 0, classical Gram-Schmidt applied twice
-    (CGS2), Givens rotations.  Follows SURVEY.md §8(c) O8:
+    (CGS2; reorth=0: once, CGS1), Givens rotations.  Follows SURVEY.md §8(c) O8:
       beta = ||b||; converged when |g_{j+1}| <= rtol * beta; happy breakdown when
       h_{j+1,j} <= 1e-14 ||A z_j||; at cycle end x += P^-1 (V y) (or Z y), the
       true residual r = b - A x is recomputed and the solve stops only if
@@ -258,9 +258,12 @@ def gmres(matvec, precond, b, rtol=1e-10, restart=30, maxit=10000, flexible=Fals
             wnorm0 = np.linalg.norm(w)
             h1 = V[:j + 1] @ w
             w = w - V[:j + 1].T @ h1
-            h2 = V[:j + 1] @ w
-            w = w - V[:j + 1].T @ h2
-            H[:j + 1, j] = h1 + h2
+            if reorth:
+                h2 = V[:j + 1] @ w
+                w = w - V[:j + 1].T @ h2
+                H[:j + 1, j] = h1 + h2
+            else:
+                H[:j + 1, j] = h1
             hn = np.linalg.norm(w)
             H[j + 1, j] = hn
             for i in range(j):
@@ -310,12 +313,12 @@ def gmres(matvec, precond, b, rtol=1e-10, restart=30, maxit=10000, flexible=Fals
 
 def solve(M, B, rhs, precond_kind=PRECOND_BLOCK_SCHUR, rtol=1e-10, restart=30, maxit=10000,
           eps=0.0, cheb_degree=16, cheb_ratio=30.0, inner_rtol=1e-14, inner_maxit=10000,
-          exact_schur=False, block=1):
+          exact_schur=False, block=1, reorth=1):
     """Oracle counterpart of vem_mixed_upload + vem_mixed_solve; `block` is
     the number of pressure DOFs per element (layout.n_p_dof)."""
     P = Preconditioner(precond_kind, M, B, cheb_degree, cheb_ratio, eps, inner_rtol, inner_maxit,
                        exact_schur, block=block)
-    res = gmres(lambda x: spmv_saddle(M, B, x), P.apply, rhs, rtol, restart, maxit, P.flexible)
+    res = gmres(lambda x: spmv_saddle(M, B, x), P.apply, rhs, rtol, restart, maxit, P.flexible, reorth)
     res.inner_iterations = P.inner_iterations
     res.inner_failed = P.inner_failed
     return res

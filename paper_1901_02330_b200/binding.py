@@ -39,7 +39,7 @@ class vem_layout(C.Structure):
 class vem_opts(C.Structure):
     _fields_ = [("restart", C.c_int32), ("cheb_degree", C.c_int32), ("cheb_ratio", C.c_double),
                 ("inner_rtol", C.c_double), ("inner_maxit", C.c_int32), ("use_graphs", C.c_int32),
-                ("timing", C.c_int32), ("pcg_chunk", C.c_int32)]
+                ("timing", C.c_int32), ("pcg_chunk", C.c_int32), ("reorth", C.c_int32)]
 
 
 class vem_solve_report(C.Structure):

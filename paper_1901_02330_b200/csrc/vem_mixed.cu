@@ -508,7 +508,8 @@ int enqueue_arnoldi_step(Ctx *c, int kind, int j, int64_t *inner_its) {
   }
   const int nv = j + 1;
   const int gx = c->sm_count * 2;
-  for (int pass = 1; pass <= 2; ++pass) {
+  const int npass = c->opts.reorth ? 2 : 1;   // CGS2 (default) or CGS1
+  for (int pass = 1; pass <= npass; ++pass) {
     const int nout = nv + (pass == 1 ? 1 : 0);
     dim3 grid(gx, (nout + VEM_DOT_CHUNK - 1) / VEM_DOT_CHUNK);
     {
@@ -518,8 +519,8 @@ int enqueue_arnoldi_step(Ctx *c, int kind, int j, int64_t *inner_its) {
     }
     {
       TimeScope ts(c, VEM_K_UPDATE, bytes_vecs(c, nv + 2));
-      k_update<<<gx * 2, NT, 0, c->stream>>>(c->n, c->V, c->ldv, nv, w, pass == 2 ? 1 : 0, c->part, c->counter,
-                                             c->st, j);
+      k_update<<<gx * 2, NT, 0, c->stream>>>(c->n, c->V, c->ldv, nv, w, pass == npass ? 1 : 0, c->part,
+                                             c->counter, c->st, j);
     }
   }
   CKL();
@@ -1121,6 +1122,7 @@ void vem_mixed_default_options(vem_opts *o) {
   o->use_graphs = 1;
   o->timing = 0;
   o->pcg_chunk = 16;
+  o->reorth = 1;
 }
 
 static int validate_opts(Ctx *c, const vem_opts *o) {
@@ -1128,6 +1130,7 @@ static int validate_opts(Ctx *c, const vem_opts *o) {
   if (o->cheb_degree < 1) return fail(c, VEM_ERR_INVALID, "cheb_degree must be >= 1");
   if (!(o->cheb_ratio > 1.0)) return fail(c, VEM_ERR_INVALID, "cheb_ratio must be > 1");
   if (!(o->inner_rtol > 0.0) || o->inner_maxit < 1) return fail(c, VEM_ERR_INVALID, "bad inner PCG options");
+  if (o->reorth != 0 && o->reorth != 1) return fail(c, VEM_ERR_INVALID, "reorth must be 0 or 1");
   return 0;
 }
 

@@ -159,6 +159,20 @@ def test_block_reg_fixed_budget_c5s():
     sv.close()
 
 
+@pytest.mark.parametrize("name", ["C1", "C3s", "C2s"])
+def test_cgs1_option_parity(name):
+    """opts.reorth = 0 (one classical Gram-Schmidt pass) against the oracle's CGS1."""
+    s = system(name)
+    cfg = configs.CONFIGS[name]
+    ref = O.solve(s.M, s.B, s.rhs, 1, 1e-10, cfg.restart, block=s.layout.n_p_dof, reorth=0)
+    sv = solver_for(s, restart=cfg.restart, reorth=0)
+    res = sv.solve(torch.from_numpy(s.rhs).cuda(), 1e-10, 10000, 1)
+    assert res.report["converged"] == 1 and abs(res.report["iterations"] - ref.iterations) <= 2
+    nu = s.layout.n_u
+    assert rel_inf(res.u.cpu().numpy(), ref.x[:nu]) <= 1e-8 and rel_inf(res.p.cpu().numpy(), ref.x[nu:]) <= 1e-8
+    sv.close()
+
+
 def test_solve_host_matches_device_and_is_deterministic():
     s = system("C3s")
     sv = solver_for(s, restart=50)
