@@ -40,7 +40,8 @@ def parse():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-sample-its", type=int, default=6)
     ap.add_argument("--graphs", action="store_true", help="time with CUDA graphs instead of per-launch events")
-    ap.add_argument("--reorth", type=int, default=1, help="1: CGS2 (default), 0: CGS1")
+    ap.add_argument("--l2-persist", type=int, default=1)
+    ap.add_argument("--reorth", type=int, default=-1, help="-1 auto (CGS1 for GMRES, CGS2 for FGMRES), 1 CGS2, 0 CGS1")
     return ap.parse_args()
 
 
@@ -151,7 +152,7 @@ def cpu_baseline(system, cfg, kind, eps, its):
     P = O.Preconditioner(kind, system.M, system.B, eps=eps, block=system.layout.n_p_dof)
     t1 = time.perf_counter()
     res = O.gmres(lambda x: O.spmv_saddle(system.M, system.B, x), P.apply, system.rhs, 1e-10, cfg.restart, its,
-                  P.flexible)
+                  P.flexible, 1 if P.flexible else 0)
     t2 = time.perf_counter()
     return {"value": res.iterations / (t2 - t1), "unit": UNIT, "cores": int(cores), "kind": "oracle",
             "sample": f"{res.iterations} GMRES iterations of {cfg.name} (precond {kind}) from x0=0, "
@@ -211,7 +212,7 @@ def main():
     t_asm = time.perf_counter() - t0
     eps = eps_for(s)
     opts = pkg.default_options(restart=cfg.restart, use_graphs=1 if args.graphs else 0,
-                               timing=0 if args.graphs else 1, reorth=args.reorth)
+                               timing=0 if args.graphs else 1, reorth=args.reorth, l2_persist=args.l2_persist)
     t0 = time.perf_counter()
     sv = pkg.VemMixed(s.M, s.B, eps=eps, layout=s.layout, opts=opts)
     t_up = time.perf_counter() - t0
@@ -284,7 +285,8 @@ def main():
             "config": {"workload": f"{cfg.name}: {cfg.describe}", "n_dofs": s.n, "n_u": s.layout.n_u,
                        "n_p": s.layout.n_p, "nnz_A": info["nnz_A"], "nnz_S": info["nnz_S"],
                        "precond": kind, "restart": cfg.restart, "rtol": cfg.rtol,
-                       "orthogonalisation": "CGS2" if args.reorth else "CGS1",
+                       "l2_window_MB": round(info["l2_window_bytes"] / 1e6, 1),
+                       "orthogonalisation": {1: "CGS2", 0: "CGS1"}.get(args.reorth, "auto: CGS1 (GMRES) / CGS2 (FGMRES)"),
                        "iterations_per_solve": [r["iterations"] for r in reports],
                        "time_to_solution_ms": ms / args.steps,
                        "rel_residual_true": reports[-1]["rel_residual_true"],

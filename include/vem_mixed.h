@@ -78,7 +78,9 @@ typedef struct {
   int32_t use_graphs;     /* 1: replay GMRES cycles / PCG chunks as CUDA graphs (default)  */
   int32_t timing;         /* 1: time every kernel launch with CUDA events (stats below)    */
   int32_t pcg_chunk;      /* PCG steps per host convergence poll (default 16)              */
-  int32_t reorth;         /* 1: CGS2 (default), 0: CGS1 (one projection pass)              */
+  int32_t reorth;         /* -1 auto (default): CGS1 for GMRES (Block-Schur / none), CGS2
+                             for FGMRES (Block-Reg); 1: CGS2 always; 0: CGS1 always        */
+  int32_t l2_persist;     /* 1 (default): persisting L2 window over the Chebyshev vectors  */
 } vem_opts;
 
 typedef struct {
@@ -102,6 +104,7 @@ typedef struct {
   int32_t spmv_group, schur_group;/* lanes per row of the CSR kernels                     */
   int32_t sm_count;
   int64_t device_bytes;           /* device memory owned by the context                   */
+  int64_t l2_window_bytes;        /* bytes under the persisting L2 access window          */
 } vem_info;
 
 /* Kernel classes for the per-launch CUDA-event statistics (opts.timing = 1). */

@@ -313,9 +313,12 @@ def gmres(matvec, precond, b, rtol=1e-10, restart=30, maxit=10000, flexible=Fals
 
 def solve(M, B, rhs, precond_kind=PRECOND_BLOCK_SCHUR, rtol=1e-10, restart=30, maxit=10000,
           eps=0.0, cheb_degree=16, cheb_ratio=30.0, inner_rtol=1e-14, inner_maxit=10000,
-          exact_schur=False, block=1, reorth=1):
+          exact_schur=False, block=1, reorth=-1):
     """Oracle counterpart of vem_mixed_upload + vem_mixed_solve; `block` is
-    the number of pressure DOFs per element (layout.n_p_dof)."""
+    the number of pressure DOFs per element (layout.n_p_dof).  reorth = -1
+    (auto, reading R17): CGS1 for GMRES, CGS2 for FGMRES (Block-Reg)."""
+    if reorth < 0:
+        reorth = 1 if precond_kind == PRECOND_BLOCK_REG else 0
     P = Preconditioner(precond_kind, M, B, cheb_degree, cheb_ratio, eps, inner_rtol, inner_maxit,
                        exact_schur, block=block)
     res = gmres(lambda x: spmv_saddle(M, B, x), P.apply, rhs, rtol, restart, maxit, P.flexible, reorth)

@@ -15,7 +15,7 @@
 #include <cuda_runtime.h>
 
 #define VEM_MAXM 128
-#define VEM_DOT_CHUNK 16
+#define VEM_DOT_CHUNK 8
 
 struct GmresState {
   int active;      // Arnoldi steps of the current cycle proceed while 1

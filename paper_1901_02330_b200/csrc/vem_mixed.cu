@@ -52,6 +52,9 @@ struct Ctx {
   double lmax = 0.0;                   // Gershgorin bound of diag(S)^-1 S (reported)
   double lmax_cheb = 2.0;              // Chebyshev interval top: lambda_max(D_B^-1 S_D) <= 2 (R15)
   double *dBinv = nullptr, *dBeinv = nullptr, *pz = nullptr;
+  double *cheb_pool = nullptr;          // D^-1, r, d0, d1, x of the Chebyshev steps, contiguous
+  size_t cheb_pool_bytes = 0;
+  size_t l2_window_bytes = 0;           // bytes of the pool under a persisting L2 access window
   // device matrices
   int *a_rp = nullptr, *a_ci = nullptr;
   double *a_va = nullptr;
@@ -508,7 +511,8 @@ int enqueue_arnoldi_step(Ctx *c, int kind, int j, int64_t *inner_its) {
   }
   const int nv = j + 1;
   const int gx = c->sm_count * 2;
-  const int npass = c->opts.reorth ? 2 : 1;   // CGS2 (default) or CGS1
+  // reorth: 1 CGS2, 0 CGS1, -1 auto = CGS1 for GMRES, CGS2 for FGMRES/Block-Reg (reading R17)
+  const int npass = (c->opts.reorth == 1 || (c->opts.reorth < 0 && flex)) ? 2 : 1;
   for (int pass = 1; pass <= npass; ++pass) {
     const int nout = nv + (pass == 1 ? 1 : 0);
     dim3 grid(gx, (nout + VEM_DOT_CHUNK - 1) / VEM_DOT_CHUNK);
@@ -849,6 +853,36 @@ int build_schur(Ctx *c, const int64_t *brp, const int *bci, const double *bva, c
   return rcode;
 }
 
+// Keep the Chebyshev vectors (5 x n_p doubles: 84 MB on C3) resident in the
+// 126 MB L2 across the d-1 steps of an apply, so each step streams only S_D
+// from HBM: a persisting access-policy window on the library stream (captured
+// into the graph kernel nodes).  opts.l2_persist = 0 disables it.
+int apply_l2_window(Ctx *c) {
+  cudaStreamAttrValue attr{};
+  if (!c->opts.l2_persist || !c->cheb_pool) {
+    attr.accessPolicyWindow.num_bytes = 0;
+    cudaStreamSetAttribute(c->stream, cudaStreamAttributeAccessPolicyWindow, &attr);
+    c->l2_window_bytes = 0;
+    return 0;
+  }
+  int dev = 0, maxp = 0, maxw = 0;
+  CK(cudaGetDevice(&dev));
+  CK(cudaDeviceGetAttribute(&maxp, cudaDevAttrMaxPersistingL2CacheSize, dev));
+  CK(cudaDeviceGetAttribute(&maxw, cudaDevAttrMaxAccessPolicyWindowSize, dev));
+  if (maxp <= 0 || maxw <= 0) return 0;
+  const size_t win = std::min(c->cheb_pool_bytes, (size_t)maxw);
+  const size_t setaside = std::min(win, (size_t)maxp);
+  CK(cudaDeviceSetLimit(cudaLimitPersistingL2CacheSize, setaside));
+  attr.accessPolicyWindow.base_ptr = c->cheb_pool;
+  attr.accessPolicyWindow.num_bytes = win;
+  attr.accessPolicyWindow.hitRatio = (float)std::min(1.0, (double)setaside / (double)win);
+  attr.accessPolicyWindow.hitProp = cudaAccessPropertyPersisting;
+  attr.accessPolicyWindow.missProp = cudaAccessPropertyStreaming;
+  CK(cudaStreamSetAttribute(c->stream, cudaStreamAttributeAccessPolicyWindow, &attr));
+  c->l2_window_bytes = win;
+  return 0;
+}
+
 int build_sell(Ctx *c, long nrows, const int *rp, const int *ci, const double *va, long long **soff, int **sci,
                double **sva, long *nnz_sell) {
   const long nsl = (nrows + 31) / 32;
@@ -1002,7 +1036,16 @@ int upload_impl(Ctx *c, const vem_csr *M, const vem_csr *B, const vem_csr *W, do
   // S_D
   r = build_schur(c, brp, bci, bva, btrp, btci, btva);
   if (r) return r;
-  DA(c->dSinv, c->np);
+  {  // Chebyshev working set in one contiguous pool: D^-1, r, d0, d1, x (L2-persisting window)
+    const long npad = (c->np + 31) / 32 * 32;
+    DA(c->cheb_pool, 5 * npad);
+    c->cheb_pool_bytes = (size_t)5 * npad * sizeof(double);
+    c->dSinv = c->cheb_pool;
+    c->cr = c->cheb_pool + npad;
+    c->cd0 = c->cheb_pool + 2 * npad;
+    c->cd1 = c->cheb_pool + 3 * npad;
+    c->cx = c->cheb_pool + 4 * npad;
+  }
   DA(c->sdiag, c->np);
   k_diag_inv<<<grid_stream(c, c->np), NT, 0, c->stream>>>(c->np, c->s_rp, c->s_ci, c->s_va, 0, c->dSinv, c->sdiag,
                                                           c->derr);
@@ -1043,10 +1086,6 @@ int upload_impl(Ctx *c, const vem_csr *M, const vem_csr *B, const vem_csr *W, do
   DA(c->b, c->n);
   DA(c->z, c->n);
   DA(c->t, c->n);
-  DA(c->cr, c->np);
-  DA(c->cd0, c->np);
-  DA(c->cd1, c->np);
-  DA(c->cx, c->np);
   if (c->has_reg) {
     DA(c->px, c->np);
     DA(c->pr, c->np);
@@ -1064,6 +1103,10 @@ int upload_impl(Ctx *c, const vem_csr *M, const vem_csr *B, const vem_csr *W, do
     if (rr) return rr;
   }
   CK(cudaStreamSynchronize(c->stream));
+  {
+    int rr = apply_l2_window(c);
+    if (rr) return rr;
+  }
   dfree(c, c->a_rp);
   dfree(c, c->a_ci);
   dfree(c, c->a_va);
@@ -1080,6 +1123,7 @@ int upload_impl(Ctx *c, const vem_csr *M, const vem_csr *B, const vem_csr *W, do
 void destroy_ctx(Ctx *c) {
   if (!c) return;
   if (c->stream) cudaStreamSynchronize(c->stream);
+  if (c->l2_window_bytes) cudaCtxResetPersistingL2Cache();
   destroy_graphs(c);
   flush_timing(c);
   for (auto e : c->free_events) cudaEventDestroy(e);
@@ -1122,7 +1166,8 @@ void vem_mixed_default_options(vem_opts *o) {
   o->use_graphs = 1;
   o->timing = 0;
   o->pcg_chunk = 16;
-  o->reorth = 1;
+  o->reorth = -1;
+  o->l2_persist = 1;
 }
 
 static int validate_opts(Ctx *c, const vem_opts *o) {
@@ -1130,7 +1175,7 @@ static int validate_opts(Ctx *c, const vem_opts *o) {
   if (o->cheb_degree < 1) return fail(c, VEM_ERR_INVALID, "cheb_degree must be >= 1");
   if (!(o->cheb_ratio > 1.0)) return fail(c, VEM_ERR_INVALID, "cheb_ratio must be > 1");
   if (!(o->inner_rtol > 0.0) || o->inner_maxit < 1) return fail(c, VEM_ERR_INVALID, "bad inner PCG options");
-  if (o->reorth != 0 && o->reorth != 1) return fail(c, VEM_ERR_INVALID, "reorth must be 0 or 1");
+  if (o->reorth < -1 || o->reorth > 1) return fail(c, VEM_ERR_INVALID, "reorth must be -1, 0 or 1");
   return 0;
 }
 
@@ -1250,6 +1295,10 @@ int vem_mixed_set_options(vem_ctx *h, const vem_opts *o) {
   const bool realloc_v = o->restart != c->opts.restart;
   c->opts = *o;
   destroy_graphs(c);
+  {
+    int rr = apply_l2_window(c);
+    if (rr) return rr;
+  }
   if (realloc_v) {
     if (c->V) dfree(c, c->V);
     c->V = nullptr;
@@ -1281,6 +1330,7 @@ int vem_mixed_get_info(vem_ctx *h, vem_info *info) {
   info->schur_group = c->gS;
   info->sm_count = c->sm_count;
   info->device_bytes = c->device_bytes;
+  info->l2_window_bytes = (int64_t)c->l2_window_bytes;
   return VEM_OK;
 }
 

@@ -160,12 +160,12 @@ def test_block_reg_fixed_budget_c5s():
 
 
 @pytest.mark.parametrize("name", ["C1", "C3s", "C2s"])
-def test_cgs1_option_parity(name):
-    """opts.reorth = 0 (one classical Gram-Schmidt pass) against the oracle's CGS1."""
+def test_cgs2_option_parity(name):
+    """opts.reorth = 1 (CGS2 for every preconditioner) against the oracle's CGS2."""
     s = system(name)
     cfg = configs.CONFIGS[name]
-    ref = O.solve(s.M, s.B, s.rhs, 1, 1e-10, cfg.restart, block=s.layout.n_p_dof, reorth=0)
-    sv = solver_for(s, restart=cfg.restart, reorth=0)
+    ref = O.solve(s.M, s.B, s.rhs, 1, 1e-10, cfg.restart, block=s.layout.n_p_dof, reorth=1)
+    sv = solver_for(s, restart=cfg.restart, reorth=1)
     res = sv.solve(torch.from_numpy(s.rhs).cuda(), 1e-10, 10000, 1)
     assert res.report["converged"] == 1 and abs(res.report["iterations"] - ref.iterations) <= 2
     nu = s.layout.n_u
