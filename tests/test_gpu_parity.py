@@ -249,6 +249,37 @@ def test_tiny_and_ragged_meshes(n, k):
 
 
 @pytest.mark.slow
+@pytest.mark.parametrize("name", ["C2", "C4"])
+def test_full_size_k1_k2_sampled_and_properties(name):
+    """C2 (k=1 tets) and C4 (k=2 cubes) at full size: sampled SpMV rows and S_D
+    rows against the oracle definitions; both preconditioners converge to the
+    true residual with element-wise conservation."""
+    s = system(name)
+    cfg = configs.CONFIGS[name]
+    sv = solver_for(s, restart=cfg.restart)
+    x = RNG.normal(size=s.n)
+    y = sv.spmv(torch.from_numpy(x).cuda()).cpu().numpy()
+    A = sp.bmat([[s.M, s.B.T], [s.B, None]]).tocsr()
+    rows = RNG.choice(s.n, 20000, replace=False)
+    yo = A[rows] @ x
+    assert np.abs(y[rows] - yo).max() <= 1e-12 * np.abs(yo).max()
+    xp = RNG.normal(size=s.layout.n_p)
+    ys = sv.schur_spmv(torch.from_numpy(xp).cuda()).cpu().numpy()
+    prow = RNG.choice(s.layout.n_p, 5000, replace=False)
+    So = (s.B[prow] @ sp.diags(1 / s.M.diagonal()) @ s.B.T).tocsr()
+    yso = So @ xp
+    assert np.abs(ys[prow] - yso).max() <= 1e-12 * np.abs(yso).max()
+    for kind in cfg.precs:
+        res = sv.solve(torch.from_numpy(s.rhs).cuda(), 1e-10, 20000, kind)
+        assert res.report["converged"] == 1, res.report
+        u, p = res.u.cpu().numpy(), res.p.cpu().numpy()
+        r = s.rhs - A @ np.concatenate([u, p])
+        assert np.linalg.norm(r) <= 1.0001e-10 * np.linalg.norm(s.rhs)
+        assert np.abs(s.B @ u - s.f).max() <= 1e-7 * np.abs(s.f).max()
+    sv.close()
+
+
+@pytest.mark.slow
 def test_full_c3_sampled_and_properties():
     """C3 at full size (8.4M DOFs) in the bench's configuration: sampled SpMV
     rows against the oracle definition, then the solve's true residual and
