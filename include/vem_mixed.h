@@ -76,7 +76,9 @@ typedef struct {
   double  inner_rtol;     /* Block-Reg inner PCG relative tolerance (default 1e-14)        */
   int32_t inner_maxit;    /* Block-Reg inner PCG iteration cap (default 10000)             */
   int32_t use_graphs;     /* 1: replay GMRES cycles / PCG chunks as CUDA graphs (default)  */
-  int32_t timing;         /* 1: time every kernel launch with CUDA events (stats below)    */
+  int32_t timing;         /* 1: time every launch with CUDA events (no graphs);
+                             2: sampled, graph-compatible: the middle Chebyshev step of
+                                every Arnoldi step is bracketed by events (k = 0 path)    */
   int32_t pcg_chunk;      /* PCG steps per host convergence poll (default 16)              */
   int32_t reorth;         /* -1 auto (default): CGS1 for GMRES (Block-Schur / none), CGS2
                              for FGMRES (Block-Reg); 1: CGS2 always; 0: CGS1 always        */

@@ -87,6 +87,11 @@ struct Ctx {
   std::vector<cudaEvent_t> free_events;
   vem_kernel_stats stats{};
   bool capturing = false;
+  // timing = 2 (sampled, graph-compatible): one Chebyshev step per Arnoldi step
+  // is bracketed by its own event pair (captured as event-record graph nodes);
+  // the host reads the pairs of the executed steps after every cycle.
+  int sample_slot = -1;
+  std::vector<cudaEvent_t> samp_a, samp_b;
   // misc
   std::string err;
   double setup_ms = 0.0;
@@ -177,7 +182,7 @@ struct TimeScope {
   double bytes;
   cudaEvent_t a = nullptr;
   TimeScope(Ctx *c_, int cls_, double bytes_ = 0.0) : c(c_), cls(cls_), bytes(bytes_) {
-    if (c->opts.timing && !c->capturing) {
+    if (c->opts.timing == 1 && !c->capturing) {
       a = take_event(c);
       cudaEventRecord(a, c->stream);
     }
@@ -190,6 +195,30 @@ struct TimeScope {
     }
   }
 };
+int ensure_samples(Ctx *c) {
+  const int m = c->opts.restart;
+  while ((int)c->samp_a.size() < m) {
+    cudaEvent_t a, b;
+    CK(cudaEventCreate(&a));
+    CK(cudaEventCreate(&b));
+    c->samp_a.push_back(a);
+    c->samp_b.push_back(b);
+  }
+  return 0;
+}
+// after a cycle that executed `steps` Arnoldi steps (stream synchronised)
+void collect_samples(Ctx *c, int steps, double bytes) {
+  if (c->opts.timing != 2) return;
+  for (int j = 0; j < steps && j < (int)c->samp_a.size(); ++j) {
+    float ms = 0.f;
+    if (cudaEventElapsedTime(&ms, c->samp_a[j], c->samp_b[j]) == cudaSuccess) {
+      c->stats.launches[VEM_K_CHEB] += 1;
+      c->stats.ms[VEM_K_CHEB] += ms;
+      c->stats.bytes[VEM_K_CHEB] += bytes;
+    }
+  }
+}
+
 void flush_timing(Ctx *c) {   // call after a stream sync
   for (auto &t : c->pending) {
     float ms = 0.f;
@@ -367,8 +396,13 @@ int enqueue_block_schur(Ctx *c, const double *v, const double *scale, double *z,
       TimeScope ts(c, VEM_K_PRECOND_VEC, 8.0 * c->np * (5 + c->nb));
       dispatch_nb<ChebBlkL>(c->nb, c, (const double *)dold, dnew, c1[i - 1], c2[i - 1], 0, last, z + c->nu, gate);
     } else {
-      TimeScope ts(c, VEM_K_CHEB, bytes_cheb(c));
-      launch_cheb(c, dold, dnew, c1[i - 1], c2[i - 1], last, z + c->nu, gate);
+      const bool sample = c->opts.timing == 2 && c->sample_slot >= 0 && i == deg / 2;
+      if (sample) cudaEventRecord(c->samp_a[c->sample_slot], c->stream);
+      {
+        TimeScope ts(c, VEM_K_CHEB, bytes_cheb(c));
+        launch_cheb(c, dold, dnew, c1[i - 1], c2[i - 1], last, z + c->nu, gate);
+      }
+      if (sample) cudaEventRecord(c->samp_b[c->sample_slot], c->stream);
     }
     std::swap(dold, dnew);
   }
@@ -440,7 +474,7 @@ int enqueue_pcg_steps(Ctx *c, int nsteps) {
 int run_pcg(Ctx *c, int64_t *inner_its) {
   int chunk = std::max(2, c->opts.pcg_chunk);
   if (chunk % 2) ++chunk;
-  const bool graphs = c->opts.use_graphs && !c->opts.timing;
+  const bool graphs = c->opts.use_graphs && c->opts.timing != 1;
   if (graphs && (!c->pcg_exec || c->pcg_exec_chunk != chunk)) {
     if (c->pcg_exec) cudaGraphExecDestroy(c->pcg_exec);
     c->pcg_exec = nullptr;
@@ -503,7 +537,9 @@ int enqueue_arnoldi_step(Ctx *c, int kind, int j, int64_t *inner_its) {
   double *Vj = c->V + (size_t)j * c->ldv;
   double *w = c->V + (size_t)(j + 1) * c->ldv;
   double *zj = flex ? c->Z + (size_t)j * c->ldv : c->z;
+  c->sample_slot = j;
   int rc = enqueue_precond(c, kind, Vj, &c->st->vscale[j], zj, gate_active(c), inner_its);
+  c->sample_slot = -1;
   if (rc) return rc;
   {
     TimeScope ts(c, VEM_K_SPMV, bytes_spmv(c));
@@ -631,7 +667,11 @@ int solve_impl(Ctx *c, const double *rhs, double tol, int maxit, int kind, doubl
     gs.active = (gs.its >= gs.maxit) ? 0 : 1;
     gs.conv_true = 0;
     CK(cudaMemcpyAsync(&c->st->g, &gs, sizeof(gs), cudaMemcpyHostToDevice, c->stream));
-    const bool graphs = c->opts.use_graphs && !c->opts.timing && kind != VEM_PRECOND_BLOCK_REG;
+    const bool graphs = c->opts.use_graphs && c->opts.timing != 1 && kind != VEM_PRECOND_BLOCK_REG;
+    if (c->opts.timing == 2) {
+      int rs = ensure_samples(c);
+      if (rs) return rs;
+    }
     int restarts = 0, cycles = 0;
     while (c->hst->g.its < maxit || cycles == 0) {
       if (maxit == 0) break;
@@ -660,6 +700,7 @@ int solve_impl(Ctx *c, const double *rhs, double tol, int maxit, int kind, doubl
       CK(cudaMemcpyAsync(&c->hst->g, &c->st->g, sizeof(GmresState), cudaMemcpyDeviceToHost, c->stream));
       CK(cudaStreamSynchronize(c->stream));
       flush_timing(c);
+      collect_samples(c, c->hst->g.j, bytes_cheb(c));
       const GmresState &h = c->hst->g;
       if (h.conv_true) break;
       if (h.its >= maxit) {
@@ -1127,6 +1168,8 @@ void destroy_ctx(Ctx *c) {
   destroy_graphs(c);
   flush_timing(c);
   for (auto e : c->free_events) cudaEventDestroy(e);
+  for (auto e : c->samp_a) cudaEventDestroy(e);
+  for (auto e : c->samp_b) cudaEventDestroy(e);
   for (void *p : c->allocs) cudaFree(p);
   if (c->hst) cudaFreeHost(c->hst);
   if (c->ev_in) cudaEventDestroy(c->ev_in);

@@ -192,8 +192,13 @@ def test_graphs_and_timing_mode_agree():
     sv.set_options(use_graphs=0, timing=1)
     b = sv.solve(torch.from_numpy(s.rhs).cuda(), 1e-10, 10000, 1)
     assert np.array_equal(a.u.cpu().numpy(), b.u.cpu().numpy())
-    st = sv.kernel_stats()
+    st = sv.kernel_stats(reset=True)
     assert st["spmv"]["launches"] >= b.report["iterations"] and st["cheb"]["launches"] > 0
+    sv.set_options(use_graphs=1, timing=2)      # sampled events inside the cycle graphs
+    c = sv.solve(torch.from_numpy(s.rhs).cuda(), 1e-10, 10000, 1)
+    assert np.array_equal(a.u.cpu().numpy(), c.u.cpu().numpy())
+    st = sv.kernel_stats(reset=True)
+    assert st["cheb"]["launches"] == c.report["iterations"] and st["cheb"]["ms"] > 0
     sv.close()
 
 
