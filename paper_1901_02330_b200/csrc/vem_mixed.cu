@@ -397,12 +397,13 @@ int enqueue_block_schur(Ctx *c, const double *v, const double *scale, double *z,
       dispatch_nb<ChebBlkL>(c->nb, c, (const double *)dold, dnew, c1[i - 1], c2[i - 1], 0, last, z + c->nu, gate);
     } else {
       const bool sample = c->opts.timing == 2 && c->sample_slot >= 0 && i == deg / 2;
-      if (sample) cudaEventRecord(c->samp_a[c->sample_slot], c->stream);
+      // cudaEventRecordExternal: inside a capture this becomes a real event-record node
+      if (sample) cudaEventRecordWithFlags(c->samp_a[c->sample_slot], c->stream, cudaEventRecordExternal);
       {
         TimeScope ts(c, VEM_K_CHEB, bytes_cheb(c));
         launch_cheb(c, dold, dnew, c1[i - 1], c2[i - 1], last, z + c->nu, gate);
       }
-      if (sample) cudaEventRecord(c->samp_b[c->sample_slot], c->stream);
+      if (sample) cudaEventRecordWithFlags(c->samp_b[c->sample_slot], c->stream, cudaEventRecordExternal);
     }
     std::swap(dold, dnew);
   }
