@@ -53,6 +53,7 @@ struct Ctx {
   double lmax_cheb = 2.0;              // Chebyshev interval top: lambda_max(D_B^-1 S_D) <= 2 (R15)
   double *dBinv = nullptr, *dBeinv = nullptr, *pz = nullptr;
   double *cheb_pool = nullptr;          // D^-1, r, d0, d1, x of the Chebyshev steps, contiguous
+  double *h_rhs = nullptr, *h_u = nullptr, *h_p = nullptr;   // vem_mixed_solve_host staging
   size_t cheb_pool_bytes = 0;
   size_t l2_window_bytes = 0;           // bytes of the pool under a persisting L2 access window
   // device matrices
@@ -674,6 +675,7 @@ int solve_impl(Ctx *c, const double *rhs, double tol, int maxit, int kind, doubl
       if (rs) return rs;
     }
     int restarts = 0, cycles = 0;
+    int its_before = c->hst->g.its;
     while (c->hst->g.its < maxit || cycles == 0) {
       if (maxit == 0) break;
       if (graphs) {
@@ -701,7 +703,8 @@ int solve_impl(Ctx *c, const double *rhs, double tol, int maxit, int kind, doubl
       CK(cudaMemcpyAsync(&c->hst->g, &c->st->g, sizeof(GmresState), cudaMemcpyDeviceToHost, c->stream));
       CK(cudaStreamSynchronize(c->stream));
       flush_timing(c);
-      collect_samples(c, c->hst->g.j, bytes_cheb(c));
+      collect_samples(c, c->hst->g.its - its_before, bytes_cheb(c));   // g.j was reset by the restart
+      its_before = c->hst->g.its;
       const GmresState &h = c->hst->g;
       if (h.conv_true) break;
       if (h.its >= maxit) {
@@ -1276,20 +1279,19 @@ int vem_mixed_solve_host(vem_ctx *h, const double *rhs_host, double tol, int32_t
     int r0 = enter(c);
     if (r0) return r0;
   }
-  double *drhs = nullptr, *du = nullptr, *dp = nullptr;
-  DA(drhs, c->n);
-  DA(du, c->nu);
-  DA(dp, c->np);
-  CK(cudaMemcpyAsync(drhs, rhs_host, c->n * sizeof(double), cudaMemcpyHostToDevice, c->stream));
-  int r = solve_impl(c, drhs, tol, maxit, kind, du, dp, rep);
+  // device staging buffers for host solves, allocated once per context
+  if (!c->h_rhs) {
+    DA(c->h_rhs, c->n);
+    DA(c->h_u, c->nu);
+    DA(c->h_p, c->np);
+  }
+  CK(cudaMemcpyAsync(c->h_rhs, rhs_host, c->n * sizeof(double), cudaMemcpyHostToDevice, c->stream));
+  int r = solve_impl(c, c->h_rhs, tol, maxit, kind, c->h_u, c->h_p, rep);
   if (r >= 0) {
-    CK(cudaMemcpyAsync(u_host, du, c->nu * sizeof(double), cudaMemcpyDeviceToHost, c->stream));
-    CK(cudaMemcpyAsync(p_host, dp, c->np * sizeof(double), cudaMemcpyDeviceToHost, c->stream));
+    CK(cudaMemcpyAsync(u_host, c->h_u, c->nu * sizeof(double), cudaMemcpyDeviceToHost, c->stream));
+    CK(cudaMemcpyAsync(p_host, c->h_p, c->np * sizeof(double), cudaMemcpyDeviceToHost, c->stream));
     CK(cudaStreamSynchronize(c->stream));
   }
-  dfree(c, drhs);
-  dfree(c, du);
-  dfree(c, dp);
   return leave(c, r);
 }
 
