@@ -264,6 +264,47 @@ __global__ void k_bs_init(long nu, long np, const double *__restrict__ v, const 
   }
 }
 
+// Block-Schur apply, first Chebyshev step fused with the init (k = 0 path):
+// rows < nu:  z_u = s v_u ./ diag(M);  rows >= nu (pressure row k):
+//   d0 = D^-1 (s v_p) / theta (recomputed at every gathered column),
+//   r1 = s v_p - S d0;  d1 = c1 d0 + c2 D^-1 r1;  x = d0 + d1   (last: z_p = -x)
+struct GatherD0 {
+  const double *__restrict__ vp, *__restrict__ dinv;
+  double f;  // s / theta
+  __device__ __forceinline__ double operator()(int c) const { return dinv[c] * vp[c] * f; }
+};
+__global__ void __launch_bounds__(256) k_cheb_first(long nu, long np, Sell S, const double *__restrict__ v,
+                                                    const double *scale, const double *__restrict__ dMinv,
+                                                    const double *__restrict__ dSinv, double inv_theta, double c1,
+                                                    double c2, double *__restrict__ r, double *__restrict__ d_new,
+                                                    double *__restrict__ x, double *__restrict__ z, int last,
+                                                    const int *gate) {
+  if (!*gate) return;
+  const double s = *scale;
+  const long i = (long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < nu) {
+    z[i] = s * v[i] * dMinv[i];
+    return;
+  }
+  const long row = i - nu;
+  if (row >= np) return;
+  const double *vp = v + nu;
+  const double f = s * inv_theta;
+  const double sd = sell_dot(S, row, GatherD0{vp, dSinv, f});
+  const double r0 = s * vp[row];
+  const double d0 = dSinv[row] * r0 * inv_theta;
+  const double rn = r0 - sd;
+  const double dn = c1 * d0 + c2 * (dSinv[row] * rn);
+  const double xn = d0 + dn;
+  if (last) {
+    z[nu + row] = -xn;
+  } else {
+    r[row] = rn;
+    d_new[row] = dn;
+    x[row] = xn;
+  }
+}
+
 // one Chebyshev step:  r -= S d_old;  d_new = c1 d_old + c2 D^-1 r;  x += d_new
 // last step writes z_p = -(x + d_new) instead of x.
 __global__ void __launch_bounds__(256) k_cheb_step(long np, Sell S, const double *__restrict__ dSinv,
@@ -448,13 +489,17 @@ __global__ void k_pcg_vec(long n, const double *__restrict__ dinv, const double 
 // ---------------------------------------------------------------------------
 // partial dots: out index o < nv: V_o . w ; o == nv (if with_norm): w . w.
 // grid (gx, ceil(nout / 8)); part layout [chunk][block][8]
+// grid (nchunks, nblk): the chunk index is the FASTEST block index, so the
+// blocks that read the same slice of w for different 8-vector chunks run at
+// the same time and w is fetched from HBM once (later chunks hit L2).
 __global__ void __launch_bounds__(256) k_mdot(long n, const double *__restrict__ V, long ldv, int nv,
                                               int with_norm, const double *__restrict__ w, double *part,
                                               unsigned *counter, DevState *st, int pass) {
   __shared__ double sh[32 * VEM_DOT_CHUNK];
   if (!st->g.active) return;
   const int nout = nv + (with_norm ? 1 : 0);
-  const int c0 = blockIdx.y * VEM_DOT_CHUNK;
+  const int c0 = blockIdx.x * VEM_DOT_CHUNK;
+  const int nb = gridDim.y, b = blockIdx.y;
   double acc[VEM_DOT_CHUNK];
 #pragma unroll
   for (int c = 0; c < VEM_DOT_CHUNK; ++c) acc[c] = 0.0;
@@ -464,21 +509,21 @@ __global__ void __launch_bounds__(256) k_mdot(long n, const double *__restrict__
     const int o = c0 + c;
     vp[c] = (o < nv) ? V + (size_t)o * ldv : w;
   }
-  for (long i = (long)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (long)gridDim.x * blockDim.x) {
+  for (long i = (long)b * blockDim.x + threadIdx.x; i < n; i += (long)nb * blockDim.x) {
     const double wi = w[i];
 #pragma unroll
     for (int c = 0; c < VEM_DOT_CHUNK; ++c)
-      if (c0 + c < nout) acc[c] = fma(vp[c][i], wi, acc[c]);
+      if (c0 + c < nout) acc[c] = fma(__ldcs(vp[c] + i), wi, acc[c]);
   }
   block_sum_n<VEM_DOT_CHUNK>(acc, sh);
   if (threadIdx.x == 0) {
-    double *dst = part + ((size_t)blockIdx.y * gridDim.x + blockIdx.x) * VEM_DOT_CHUNK;
+    double *dst = part + ((size_t)blockIdx.x * nb + b) * VEM_DOT_CHUNK;
 #pragma unroll
     for (int c = 0; c < VEM_DOT_CHUNK; ++c) dst[c] = acc[c];
   }
   if (elect_last_block(counter)) {
     __shared__ double tot[VEM_MAXM + 2];
-    reduce_partials<VEM_DOT_CHUNK>(part, gridDim.x, nout, tot);
+    reduce_partials<VEM_DOT_CHUNK>(part, nb, nout, tot);
     if (threadIdx.x == 0) {
       for (int o = 0; o < nv; ++o) {
         const double h = st->vscale[o] * tot[o];

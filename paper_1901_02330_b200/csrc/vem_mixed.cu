@@ -375,6 +375,34 @@ int enqueue_block_schur(Ctx *c, const double *v, const double *scale, double *z,
   cheb_coeffs(c, inv_theta, c1, c2);
   const int deg = c->opts.cheb_degree;
   const bool blk = c->nb > 1;
+  if (!blk && deg > 1) {
+    // k = 0: init fused into the first Chebyshev step (one launch over all n rows)
+    const bool sample = c->opts.timing == 2 && c->sample_slot >= 0 && deg / 2 == 1;
+    if (sample) cudaEventRecordWithFlags(c->samp_a[c->sample_slot], c->stream, cudaEventRecordExternal);
+    {
+      TimeScope ts(c, VEM_K_CHEB, bytes_cheb(c) - 16.0 * c->np + 24.0 * c->nu);
+      k_cheb_first<<<grid_for(c->n), NT, 0, c->stream>>>(c->nu, c->np, sellS(c), v, scale, c->dMinv, c->dSinv,
+                                                         inv_theta, c1[0], c2[0], c->cr, c->cd1, c->cx, z,
+                                                         deg == 2 ? 1 : 0, gate);
+    }
+    if (sample) cudaEventRecordWithFlags(c->samp_b[c->sample_slot], c->stream, cudaEventRecordExternal);
+    CKL();
+    double *dold = c->cd1, *dnew = c->cd0;
+    for (int i = 2; i < deg; ++i) {
+      const int last = i == deg - 1 ? 1 : 0;
+      const bool smp = c->opts.timing == 2 && c->sample_slot >= 0 && i == deg / 2;
+      if (smp) cudaEventRecordWithFlags(c->samp_a[c->sample_slot], c->stream, cudaEventRecordExternal);
+      {
+        TimeScope ts(c, VEM_K_CHEB, bytes_cheb(c));
+        launch_cheb(c, dold, dnew, c1[i - 1], c2[i - 1], last, z + c->nu, gate);
+      }
+      if (smp) cudaEventRecordWithFlags(c->samp_b[c->sample_slot], c->stream, cudaEventRecordExternal);
+      std::swap(dold, dnew);
+    }
+    CKL();
+    return 0;
+  }
+  // k >= 1 (element-block Jacobi) or degree 1: separate init
   {
     TimeScope ts(c, VEM_K_PRECOND_VEC, 8.0 * (3 * c->nu + 5 * c->np));
     k_bs_init<<<grid_stream(c, c->n), NT, 0, c->stream>>>(c->nu, c->np, v, scale, c->dMinv, c->dSinv, inv_theta, z,
@@ -553,7 +581,7 @@ int enqueue_arnoldi_step(Ctx *c, int kind, int j, int64_t *inner_its) {
   const int npass = (c->opts.reorth == 1 || (c->opts.reorth < 0 && flex)) ? 2 : 1;
   for (int pass = 1; pass <= npass; ++pass) {
     const int nout = nv + (pass == 1 ? 1 : 0);
-    dim3 grid(gx, (nout + VEM_DOT_CHUNK - 1) / VEM_DOT_CHUNK);
+    dim3 grid((nout + VEM_DOT_CHUNK - 1) / VEM_DOT_CHUNK, gx);
     {
       TimeScope ts(c, VEM_K_DOT, bytes_vecs(c, nv + 1));
       k_mdot<<<grid, NT, 0, c->stream>>>(c->n, c->V, c->ldv, nv, pass == 1 ? 1 : 0, w, c->part, c->counter, c->st,
