@@ -489,17 +489,16 @@ __global__ void k_pcg_vec(long n, const double *__restrict__ dinv, const double 
 // ---------------------------------------------------------------------------
 // partial dots: out index o < nv: V_o . w ; o == nv (if with_norm): w . w.
 // grid (gx, ceil(nout / 8)); part layout [chunk][block][8]
-// grid (nchunks, nblk): the chunk index is the FASTEST block index, so the
-// blocks that read the same slice of w for different 8-vector chunks run at
-// the same time and w is fetched from HBM once (later chunks hit L2).
+// grid (nblk, nchunks): block b of chunk y dots basis vectors 8y..8y+7 with w
+// over a grid-stride slice of the rows.
 __global__ void __launch_bounds__(256) k_mdot(long n, const double *__restrict__ V, long ldv, int nv,
                                               int with_norm, const double *__restrict__ w, double *part,
                                               unsigned *counter, DevState *st, int pass) {
   __shared__ double sh[32 * VEM_DOT_CHUNK];
   if (!st->g.active) return;
   const int nout = nv + (with_norm ? 1 : 0);
-  const int c0 = blockIdx.x * VEM_DOT_CHUNK;
-  const int nb = gridDim.y, b = blockIdx.y;
+  const int c0 = blockIdx.y * VEM_DOT_CHUNK;
+  const int nb = gridDim.x, b = blockIdx.x;
   double acc[VEM_DOT_CHUNK];
 #pragma unroll
   for (int c = 0; c < VEM_DOT_CHUNK; ++c) acc[c] = 0.0;
@@ -513,11 +512,11 @@ __global__ void __launch_bounds__(256) k_mdot(long n, const double *__restrict__
     const double wi = w[i];
 #pragma unroll
     for (int c = 0; c < VEM_DOT_CHUNK; ++c)
-      if (c0 + c < nout) acc[c] = fma(__ldcs(vp[c] + i), wi, acc[c]);
+      if (c0 + c < nout) acc[c] = fma(vp[c][i], wi, acc[c]);
   }
   block_sum_n<VEM_DOT_CHUNK>(acc, sh);
   if (threadIdx.x == 0) {
-    double *dst = part + ((size_t)blockIdx.x * nb + b) * VEM_DOT_CHUNK;
+    double *dst = part + ((size_t)blockIdx.y * nb + b) * VEM_DOT_CHUNK;
 #pragma unroll
     for (int c = 0; c < VEM_DOT_CHUNK; ++c) dst[c] = acc[c];
   }

@@ -581,7 +581,7 @@ int enqueue_arnoldi_step(Ctx *c, int kind, int j, int64_t *inner_its) {
   const int npass = (c->opts.reorth == 1 || (c->opts.reorth < 0 && flex)) ? 2 : 1;
   for (int pass = 1; pass <= npass; ++pass) {
     const int nout = nv + (pass == 1 ? 1 : 0);
-    dim3 grid((nout + VEM_DOT_CHUNK - 1) / VEM_DOT_CHUNK, gx);
+    dim3 grid(gx, (nout + VEM_DOT_CHUNK - 1) / VEM_DOT_CHUNK);
     {
       TimeScope ts(c, VEM_K_DOT, bytes_vecs(c, nv + 1));
       k_mdot<<<grid, NT, 0, c->stream>>>(c->n, c->V, c->ldv, nv, pass == 1 ? 1 : 0, w, c->part, c->counter, c->st,
