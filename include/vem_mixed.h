@@ -48,7 +48,10 @@ enum {
   VEM_ERR_INNER = -6       /* Block-Reg inner PCG did not reach inner_rtol in inner_maxit        */
 };
 
-enum { VEM_PRECOND_NONE = 0, VEM_PRECOND_BLOCK_SCHUR = 1, VEM_PRECOND_BLOCK_REG = 2 };
+/* 3: Block-Schur with one aggregation V-cycle on S_D in place of the Chebyshev
+ * iteration (the GPU-native stand-in for the exact MUMPS solve of S, P:978;
+ * DESIGN.md reading R22; n_p_dof = 1 only in this version). */
+enum { VEM_PRECOND_NONE = 0, VEM_PRECOND_BLOCK_SCHUR = 1, VEM_PRECOND_BLOCK_REG = 2, VEM_PRECOND_BLOCK_SCHUR_AMG = 3 };
 
 typedef struct vem_ctx vem_ctx;    /* opaque; owns every device buffer it allocates */
 
@@ -107,6 +110,8 @@ typedef struct {
   int32_t sm_count;
   int64_t device_bytes;           /* device memory owned by the context                   */
   int64_t l2_window_bytes;        /* bytes under the persisting L2 access window          */
+  int32_t amg_levels;             /* levels of the S_D hierarchy (0: kind 3 unavailable)   */
+  int64_t amg_coarsest;           /* rows of its coarsest level                            */
 } vem_info;
 
 /* Kernel classes for the per-launch CUDA-event statistics (opts.timing = 1). */
@@ -184,6 +189,10 @@ int vem_mixed_get_schur(vem_ctx *ctx, int64_t *indptr, int32_t *indices, double 
 /* Per-kernel-class launch counts and CUDA-event milliseconds accumulated while
  * opts.timing = 1; reset != 0 clears them after copying. */
 int vem_mixed_kernel_stats(vem_ctx *ctx, vem_kernel_stats *stats, int32_t reset);
+
+/* Size of level `level` of the S_D aggregation hierarchy (kind 3): rows and
+ * nonzeros; VEM_ERR_INVALID if the level does not exist. */
+int vem_mixed_amg_level(vem_ctx *ctx, int32_t level, int64_t *n, int64_t *nnz);
 
 void vem_mixed_destroy(vem_ctx *ctx);
 const char *vem_status_string(int status);

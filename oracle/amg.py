@@ -1,0 +1,175 @@
+"""Oracle of the aggregation-multigrid inner solve for S_D.
+TEST INFRASTRUCTURE ONLY (see oracle/__init__.py).
+
+The paper applies B_2^-1 with an exact MUMPS solve of the approximate Schur
+complement S = -B diag(A)^-1 B^T.  Precond kind 3
+(Block-Schur-AMG) replaces that exact solve by one symmetric aggregation V-cycle
+on S_D (reading R22), a fixed linear operator, so plain GMRES applies.
+
+Definition (the GPU follows it step by step):
+  * strength: off-diagonal (i, j) is strong iff |A_ij| >= theta sqrt(A_ii A_jj), theta = 0.08
+  * keys: key(i) = ((splitmix64(i) >> 33) << 30) | i  (distinct, index recoverable)
+  * MIS-2 (Luby, deterministic): repeat { k1 = max key over N[i], k2 = max k1 over
+    N[i] (N = strong neighbours incl. i; roots count as +inf, excluded as -1);
+    an undecided i with k2 == key(i) becomes a root, one with k2 == +inf is
+    excluded } until no node is undecided
+  * aggregates: roots numbered in index order; pass 1: a non-root joins the
+    root of largest key among its strong neighbours; pass 2: a still free node
+    joins the aggregate of its largest-key assigned strong neighbour; pass 3:
+    the rest become singletons in index order
+  * P piecewise constant, A_c = P^T A P; stop when n <= COARSE_SIZE, at
+    MAX_LEVELS, or when a level coarsens by less than 1/0.75
+  * coarsest level: dense inverse (n <= COARSE_SIZE) applied as a matvec, else
+    (stagnated coarsening) a degree-COARSE_DEGREE Chebyshev smoother
+  * smoother C_l(b): degree-DEGREE point-Jacobi Chebyshev from x0 = 0 (Saad
+    Alg. 12.1, exactly oracle.solver.chebyshev) on [lmax/RATIO, lmax] with the
+    Gershgorin bound lmax = max_i sum_j |A_ij| / A_ii
+  * V(b) at level l: x = C(b); r = b - A x; x += P V(P^T r); x += C(b - A x)
+Parity unpinned by the paper (iteration counts).  Pinned in
+tests/test_oracle_pins.py: MIS-2 property, aggregate validity, Galerkin identity,
+a one-level hierarchy is an exact solve, symmetry of the V-cycle operator.
+"""
+from __future__ import annotations
+
+from dataclasses import dataclass
+
+import numpy as np
+import scipy.sparse as sp
+
+from .solver import chebyshev
+
+THETA = 0.08
+COARSE_SIZE = 512
+MAX_LEVELS = 12
+DEGREE = 3
+RATIO = 30.0
+COARSE_DEGREE = 8
+STAGNATION = 0.75
+KEY_INDEX_BITS = 30
+ROOT_KEY = np.int64(np.iinfo(np.int64).max)
+
+
+def keys(n: int) -> np.ndarray:
+    """key(i) = ((splitmix64(i) >> 33) << 30) | i, i < 2^30."""
+    assert n < (1 << KEY_INDEX_BITS)
+    i = np.arange(n, dtype=np.uint64)
+    with np.errstate(over="ignore"):
+        z = i + np.uint64(0x9E3779B97F4A7C15)
+        z = (z ^ (z >> np.uint64(30))) * np.uint64(0xBF58476D1CE4E5B9)
+        z = (z ^ (z >> np.uint64(27))) * np.uint64(0x94D049BB133111EB)
+    z = z ^ (z >> np.uint64(31))
+    return (((z >> np.uint64(33)) << np.uint64(KEY_INDEX_BITS)) | i).astype(np.int64)
+
+
+def strong_graph(A, theta=THETA):
+    """CSR pattern of the strong connections plus the diagonal."""
+    C = A.tocoo()
+    d = A.diagonal()
+    keep = (C.row == C.col) | (np.abs(C.data) >= theta * np.sqrt(np.abs(d[C.row] * d[C.col])))
+    G = sp.csr_matrix((np.ones(int(keep.sum()), dtype=np.int8), (C.row[keep], C.col[keep])), shape=A.shape)
+    G.sort_indices()
+    return G
+
+
+def nbr_max(G, val):
+    """out[i] = max_{j in N[i]} val[j]."""
+    out = np.full(G.shape[0], np.iinfo(np.int64).min, dtype=np.int64)
+    rows = np.repeat(np.arange(G.shape[0]), np.diff(G.indptr))
+    np.maximum.at(out, rows, val[G.indices])
+    return out
+
+
+def aggregate(A, theta=THETA):
+    """Returns (agg (n,), nc, roots mask)."""
+    n = A.shape[0]
+    G = strong_graph(A, theta)
+    key = keys(n)
+    U, R, X = 0, 1, 2
+    state = np.zeros(n, dtype=np.int8)
+    while np.any(state == U):
+        k = np.where(state == U, key, np.where(state == R, ROOT_KEY, np.int64(-1)))
+        k2 = nbr_max(G, nbr_max(G, k))
+        und = state == U
+        new_root = und & (k2 == key)
+        excl = und & ~new_root & (k2 == ROOT_KEY)
+        state[new_root] = R
+        state[excl] = X
+    mask = (1 << KEY_INDEX_BITS) - 1
+    is_root = state == R
+    agg = np.full(n, -1, dtype=np.int64)
+    agg[is_root] = np.arange(int(is_root.sum()))
+    # pass 1
+    best = nbr_max(G, np.where(is_root, key, np.int64(-1)))
+    m1 = (agg < 0) & (best >= 0)
+    agg1 = agg.copy()
+    agg1[m1] = agg[best[m1] & mask]
+    # pass 2
+    best2 = nbr_max(G, np.where(agg1 >= 0, key, np.int64(-1)))
+    m2 = (agg1 < 0) & (best2 >= 0)
+    agg2 = agg1.copy()
+    agg2[m2] = agg1[best2[m2] & mask]
+    # pass 3
+    left = np.nonzero(agg2 < 0)[0]
+    nroot = int(is_root.sum())
+    agg2[left] = nroot + np.arange(left.size)
+    return agg2, nroot + left.size, is_root
+
+
+def galerkin(A, agg, nc):
+    n = A.shape[0]
+    P = sp.csr_matrix((np.ones(n), (np.arange(n), agg)), shape=(n, nc))
+    Ac = (P.T @ A.tocsr() @ P).tocsr()
+    Ac.sum_duplicates()
+    Ac.sort_indices()
+    return Ac
+
+
+def gershgorin(A):
+    a = abs(A).sum(axis=1).A1
+    return float(np.max(a / A.diagonal()))
+
+
+@dataclass
+class Level:
+    A: sp.csr_matrix
+    Dinv: sp.dia_matrix
+    lmax: float
+    agg: np.ndarray | None = None
+    nc: int = 0
+
+
+class AMG:
+    """Aggregation V-cycle hierarchy for an SPD matrix (point Jacobi smoothing)."""
+
+    def __init__(self, A, theta=THETA, coarse_size=COARSE_SIZE, max_levels=MAX_LEVELS):
+        self.levels = []
+        A = A.tocsr()
+        while True:
+            lev = Level(A, sp.diags(1.0 / A.diagonal()), gershgorin(A))
+            self.levels.append(lev)
+            if A.shape[0] <= coarse_size or len(self.levels) >= max_levels:
+                break
+            agg, nc, _ = aggregate(A, theta)
+            if nc > STAGNATION * A.shape[0]:
+                break
+            lev.agg, lev.nc = agg, nc
+            A = galerkin(A, agg, nc)
+        last = self.levels[-1]
+        self.coarse_inv = np.linalg.inv(last.A.toarray()) if last.A.shape[0] <= coarse_size else None
+
+    def smooth(self, lev, b, degree=DEGREE):
+        return chebyshev(lev.A, lev.Dinv, b, degree, lev.lmax, RATIO)
+
+    def vcycle(self, b, level=0):
+        lev = self.levels[level]
+        if level == len(self.levels) - 1:
+            if self.coarse_inv is not None:
+                return self.coarse_inv @ b
+            return self.smooth(lev, b, COARSE_DEGREE)
+        x = self.smooth(lev, b)
+        r = b - lev.A @ x
+        bc = np.bincount(lev.agg, weights=r, minlength=lev.nc)
+        xc = self.vcycle(bc, level + 1)
+        x = x + xc[lev.agg]
+        x = x + self.smooth(lev, b - lev.A @ x)
+        return x

@@ -33,6 +33,7 @@ import scipy.sparse as sp
 PRECOND_NONE = 0
 PRECOND_BLOCK_SCHUR = 1
 PRECOND_BLOCK_REG = 2
+PRECOND_BLOCK_SCHUR_AMG = 3     # Block-Schur with one aggregation V-cycle on S_D (oracle/amg.py, R22)
 
 
 def spmv_saddle(M, B, x):
@@ -158,13 +159,18 @@ class Preconditioner:
     def __post_init__(self):
         self.nu = self.M.shape[0]
         self.dM = self.M.diagonal().copy()
-        if self.kind in (PRECOND_BLOCK_SCHUR, PRECOND_BLOCK_REG):
+        if self.kind in (PRECOND_BLOCK_SCHUR, PRECOND_BLOCK_REG, PRECOND_BLOCK_SCHUR_AMG):
             self.SD = schur_diag(self.M, self.B)
             self.dS = self.SD.diagonal().copy()
             if np.any(self.dS <= 0):
                 raise ValueError("non-positive diag(S_D)")
             self.DBinv = block_jacobi_inv(self.SD, self.block)
             self.lmax = LAMBDA_MAX_BLOCK_JACOBI
+        if self.kind == PRECOND_BLOCK_SCHUR_AMG:
+            if self.block != 1:
+                raise NotImplementedError("Block-Schur-AMG is defined for n_p = 1 (k = 0) in this round")
+            from .amg import AMG
+            self.amg = AMG(self.SD)
         if self.kind == PRECOND_BLOCK_REG:
             if self.eps <= 0:
                 raise ValueError("eps must be > 0")
@@ -190,6 +196,8 @@ class Preconditioner:
             else:
                 zp = -chebyshev(self.SD, self.DBinv, vp, self.cheb_degree, self.lmax, self.cheb_ratio)
             return np.concatenate([zu, zp])
+        if self.kind == PRECOND_BLOCK_SCHUR_AMG:
+            return np.concatenate([vu / self.dM, -self.amg.vcycle(vp)])
         if self.kind == PRECOND_BLOCK_REG:
             # B_2^-1 = (eps W)^-1 with W = I
             zp = vp / self.eps

@@ -18,6 +18,7 @@ LIB_PATH = os.path.join(HERE, "libvem_mixed.so")
 PRECOND_NONE = 0
 PRECOND_BLOCK_SCHUR = 1
 PRECOND_BLOCK_REG = 2
+PRECOND_BLOCK_SCHUR_AMG = 3
 
 STATUS = {0: "OK", 1: "NOT_CONVERGED", 2: "BREAKDOWN", -1: "ERR_INVALID", -2: "ERR_DIAG_M",
           -3: "ERR_DIAG_S", -4: "ERR_CUDA", -5: "ERR_PRECOND", -6: "ERR_INNER"}
@@ -57,7 +58,8 @@ class vem_info(C.Structure):
     _fields_ = [("n_u", C.c_int64), ("n_p", C.c_int64), ("nnz_M", C.c_int64), ("nnz_B", C.c_int64),
                 ("nnz_A", C.c_int64), ("nnz_S", C.c_int64), ("lambda_max", C.c_double),
                 ("eps", C.c_double), ("spmv_group", C.c_int32), ("schur_group", C.c_int32),
-                ("sm_count", C.c_int32), ("device_bytes", C.c_int64), ("l2_window_bytes", C.c_int64)]
+                ("sm_count", C.c_int32), ("device_bytes", C.c_int64), ("l2_window_bytes", C.c_int64),
+                ("amg_levels", C.c_int32), ("amg_coarsest", C.c_int64)]
 
     def as_dict(self):
         return {f: getattr(self, f) for f, _ in self._fields_}
@@ -74,7 +76,7 @@ class vem_kernel_stats(C.Structure):
 EXPORTS = ["vem_mixed_default_options", "vem_mixed_upload", "vem_mixed_solve", "vem_mixed_solve_host",
            "vem_mixed_spmv", "vem_mixed_schur_spmv", "vem_mixed_precond_apply", "vem_mixed_set_options",
            "vem_mixed_get_options", "vem_mixed_get_info", "vem_mixed_get_schur", "vem_mixed_kernel_stats",
-           "vem_mixed_destroy", "vem_status_string", "vem_last_error"]
+           "vem_mixed_amg_level", "vem_mixed_destroy", "vem_status_string", "vem_last_error"]
 
 _lib = None
 
@@ -104,6 +106,7 @@ def load_library(path: str = LIB_PATH):
     lib.vem_mixed_get_info.argtypes = [P, C.POINTER(vem_info)]
     lib.vem_mixed_get_schur.argtypes = [P, C.POINTER(C.c_int64), C.POINTER(C.c_int32), D]
     lib.vem_mixed_kernel_stats.argtypes = [P, C.POINTER(vem_kernel_stats), C.c_int32]
+    lib.vem_mixed_amg_level.argtypes = [P, C.c_int32, C.POINTER(C.c_int64), C.POINTER(C.c_int64)]
     lib.vem_mixed_destroy.argtypes = [P]
     lib.vem_mixed_destroy.restype = None
     lib.vem_status_string.argtypes = [C.c_int]
@@ -286,6 +289,15 @@ class VemMixed:
             self._h, indptr.ctypes.data_as(C.POINTER(C.c_int64)), indices.ctypes.data_as(C.POINTER(C.c_int32)),
             values.ctypes.data_as(C.POINTER(C.c_double))), "get_schur")
         return sp.csr_matrix((values, indices, indptr), shape=(i["n_p"], i["n_p"]))
+
+    def amg_levels(self):
+        """[(rows, nnz)] of the S_D aggregation hierarchy (precond kind 3)."""
+        out = []
+        n, z = C.c_int64(), C.c_int64()
+        for lev in range(self.info()["amg_levels"]):
+            self._check(self._lib.vem_mixed_amg_level(self._h, lev, C.byref(n), C.byref(z)), "amg_level")
+            out.append((n.value, z.value))
+        return out
 
     def kernel_stats(self, reset=False) -> dict:
         s = vem_kernel_stats()

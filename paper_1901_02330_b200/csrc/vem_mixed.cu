@@ -24,6 +24,7 @@
 
 #include "../../include/vem_mixed.h"
 #include "kernels.cuh"
+#include "amg.cuh"
 
 namespace {
 
@@ -33,6 +34,23 @@ struct Timed {
   int cls;
   double bytes;
   cudaEvent_t a, b;
+};
+
+// one level of the S_D aggregation hierarchy (precond kind 3)
+struct AmgLevel {
+  long n = 0, nnz = 0;
+  int *rp = nullptr, *ci = nullptr;            // CSR (setup)
+  double *va = nullptr;
+  long long *soff = nullptr;                   // SELL-32 (apply)
+  int *sci = nullptr;
+  double *sva = nullptr;
+  long nnz_sell = 0;
+  double *dinv = nullptr;
+  double lmax = 0.0;
+  int *agg = nullptr, *moff = nullptr, *mem = nullptr;  // restriction to the next level
+  long nc = 0;
+  double *b = nullptr, *x = nullptr, *t = nullptr, *y = nullptr, *sr = nullptr, *sd0 = nullptr, *sd1 = nullptr;
+  bool owns_matrix = true;
 };
 
 struct Ctx {
@@ -54,6 +72,9 @@ struct Ctx {
   double *dBinv = nullptr, *dBeinv = nullptr, *pz = nullptr;
   double *cheb_pool = nullptr;          // D^-1, r, d0, d1, x of the Chebyshev steps, contiguous
   double *h_rhs = nullptr, *h_u = nullptr, *h_p = nullptr;   // vem_mixed_solve_host staging
+  std::vector<AmgLevel> amg;                     // S_D hierarchy (kind 3); empty when n_p_dof > 1
+  double *amg_cinv = nullptr;                    // dense inverse of the coarsest level
+  bool amg_dense = false;
   size_t cheb_pool_bytes = 0;
   size_t l2_window_bytes = 0;           // bytes of the pool under a persisting L2 access window
   // device matrices
@@ -80,7 +101,7 @@ struct Ctx {
   int *derr = nullptr;
   long part_cap = 0;
   // graphs
-  cudaGraphExec_t cycle_exec[3] = {nullptr, nullptr, nullptr};
+  cudaGraphExec_t cycle_exec[4] = {nullptr, nullptr, nullptr, nullptr};
   cudaGraphExec_t pcg_exec = nullptr;
   int pcg_exec_chunk = 0;
   // timing
@@ -538,8 +559,101 @@ int run_pcg(Ctx *c, int64_t *inner_its) {
   return 0;
 }
 
+// ----------------------------------------------------------------------------
+// Block-Schur-AMG apply (kind 3): z_u = s v_u ./ diag(M), z_p = -V(s v_p)
+// (oracle/amg.py AMG.vcycle, reading R22)
+// ----------------------------------------------------------------------------
+constexpr double AMG_THETA = 0.08, AMG_RATIO = 30.0, AMG_STAGNATION = 0.75;
+constexpr int AMG_COARSE_SIZE = 512, AMG_MAX_LEVELS = 12, AMG_DEGREE = 3, AMG_COARSE_DEGREE = 8;
+
+void amg_cheb_coeffs(double lmax, int degree, double &inv_theta, std::vector<double> &c1, std::vector<double> &c2) {
+  const double b = lmax, a = lmax / AMG_RATIO;
+  const double theta = 0.5 * (b + a), delta = 0.5 * (b - a), sigma = theta / delta;
+  double rho = 1.0 / sigma;
+  inv_theta = 1.0 / theta;
+  c1.clear();
+  c2.clear();
+  for (int i = 1; i < degree; ++i) {
+    const double rn = 1.0 / (2.0 * sigma - rho);
+    c1.push_back(rn * rho);
+    c2.push_back(2.0 * rn / delta);
+    rho = rn;
+  }
+}
+
+// out = C_degree(b) on level L (x0 = 0)
+void amg_smooth(Ctx *c, AmgLevel &L, const double *b, double *out, int degree, const int *gate) {
+  double it;
+  std::vector<double> c1, c2;
+  amg_cheb_coeffs(L.lmax, degree, it, c1, c2);
+  const Sell A{L.soff, L.sci, L.sva};
+  {
+    TimeScope ts(c, VEM_K_PRECOND_VEC, 40.0 * L.n);
+    k_amg_cheb_init<<<grid_stream(c, L.n), NT, 0, c->stream>>>(L.n, L.dinv, b, it, L.sr, L.sd0, out, gate);
+  }
+  double *dold = L.sd0, *dnew = L.sd1;
+  for (int i = 1; i < degree; ++i) {
+    TimeScope ts(c, VEM_K_CHEB, 12.0 * L.nnz + 56.0 * L.n);
+    k_amg_cheb_step<<<grid_for(L.n), NT, 0, c->stream>>>(L.n, A, L.dinv, L.sr, dold, dnew, out, c1[i - 1],
+                                                         c2[i - 1], gate);
+    std::swap(dold, dnew);
+  }
+}
+
+void amg_vcycle(Ctx *c, size_t l, const int *gate) {
+  AmgLevel &L = c->amg[l];
+  if (l + 1 == c->amg.size()) {   // coarsest
+    if (c->amg_dense) {
+      TimeScope ts(c, VEM_K_PRECOND_VEC, 8.0 * L.n * L.n);
+      k_amg_dense_mv<<<grid_stream(c, L.n), NT, 0, c->stream>>>(L.n, c->amg_cinv, L.b, L.x, gate);
+    } else {
+      amg_smooth(c, L, L.b, L.x, AMG_COARSE_DEGREE, gate);
+    }
+    return;
+  }
+  AmgLevel &C = c->amg[l + 1];
+  const Sell A{L.soff, L.sci, L.sva};
+  amg_smooth(c, L, L.b, L.x, AMG_DEGREE, gate);
+  {
+    TimeScope ts(c, VEM_K_SPMV, 12.0 * L.nnz + 24.0 * L.n);
+    k_spmv<<<grid_for(L.n), NT, 0, c->stream>>>(0, L.n, A, L.x, L.t, L.b, 1, gate);
+  }
+  {
+    TimeScope ts(c, VEM_K_PRECOND_VEC, 8.0 * L.n * 2 + 8.0 * C.n);
+    k_amg_restrict<<<grid_stream(c, C.n), NT, 0, c->stream>>>(C.n, L.moff, L.mem, L.t, C.b, gate);
+  }
+  amg_vcycle(c, l + 1, gate);
+  {
+    TimeScope ts(c, VEM_K_PRECOND_VEC, 8.0 * L.n * 3);
+    k_amg_prolong_add<<<grid_stream(c, L.n), NT, 0, c->stream>>>(L.n, L.agg, C.x, L.x, gate);
+  }
+  {
+    TimeScope ts(c, VEM_K_SPMV, 12.0 * L.nnz + 24.0 * L.n);
+    k_spmv<<<grid_for(L.n), NT, 0, c->stream>>>(0, L.n, A, L.x, L.t, L.b, 1, gate);
+  }
+  amg_smooth(c, L, L.t, L.y, AMG_DEGREE, gate);
+}
+
+int enqueue_block_schur_amg(Ctx *c, const double *v, const double *scale, double *z, const int *gate) {
+  if (c->amg.empty()) return fail(c, VEM_ERR_PRECOND, "Block-Schur-AMG needs n_p_dof = 1 (k = 0)");
+  AmgLevel &L0 = c->amg[0];
+  {
+    TimeScope ts(c, VEM_K_PRECOND_VEC, 8.0 * (3 * c->nu + 2 * c->np));
+    k_amg_top<<<grid_stream(c, c->n), NT, 0, c->stream>>>(c->nu, c->np, v, scale, c->dMinv, z, L0.b, gate);
+  }
+  amg_vcycle(c, 0, gate);
+  {
+    TimeScope ts(c, VEM_K_PRECOND_VEC, 24.0 * c->np);
+    k_amg_add<<<grid_stream(c, c->np), NT, 0, c->stream>>>(c->np, L0.x, c->amg.size() == 1 ? nullptr : L0.y,
+                                                           -1.0, z + c->nu, gate);
+  }
+  CKL();
+  return 0;
+}
+
 int enqueue_precond(Ctx *c, int kind, const double *v, const double *scale, double *z, const int *gate,
                     int64_t *inner_its) {
+  if (kind == VEM_PRECOND_BLOCK_SCHUR_AMG) return enqueue_block_schur_amg(c, v, scale, z, gate);
   if (kind == VEM_PRECOND_BLOCK_SCHUR) return enqueue_block_schur(c, v, scale, z, gate);
   if (kind == VEM_PRECOND_BLOCK_REG) return enqueue_block_reg(c, v, scale, z, gate, inner_its);
   // NONE: z = scale * v
@@ -661,7 +775,7 @@ int ensure_work(Ctx *c, int kind) {
 int solve_impl(Ctx *c, const double *rhs, double tol, int maxit, int kind, double *out_u, double *out_p,
                vem_solve_report *rep) {
   vem_solve_report R{};
-  if (kind < 0 || kind > 2) return fail(c, VEM_ERR_PRECOND, "unsupported precond_kind %d", kind);
+  if (kind < 0 || kind > 3) return fail(c, VEM_ERR_PRECOND, "unsupported precond_kind %d", kind);
   if (kind == VEM_PRECOND_BLOCK_REG && !c->has_reg)
     return fail(c, VEM_ERR_PRECOND, "Block-Reg needs eps > 0 at upload");
   if (!rhs || !out_u || !out_p || maxit < 0 || !(tol > 0)) return fail(c, VEM_ERR_INVALID, "invalid solve arguments");
@@ -983,6 +1097,246 @@ int build_sell(Ctx *c, long nrows, const int *rp, const int *ci, const double *v
   return 0;
 }
 
+// ----------------------------------------------------------------------------
+// S_D aggregation hierarchy (upload; oracle/amg.py AMG.__init__)
+// ----------------------------------------------------------------------------
+template <typename T>
+int scan_excl(Ctx *c, const T *in, T *out, long n) {
+  size_t tb = 0;
+  CK(cub::DeviceScan::ExclusiveSum(nullptr, tb, in, out, (int)n, c->stream));
+  char *tmp = nullptr;
+  DA(tmp, tb);
+  CK(cub::DeviceScan::ExclusiveSum(tmp, tb, in, out, (int)n, c->stream));
+  CK(cudaStreamSynchronize(c->stream));
+  dfree(c, tmp);
+  return 0;
+}
+
+template <typename T>
+T read_back(Ctx *c, const T *p) {
+  T v{};
+  cudaMemcpyAsync(&v, p, sizeof(T), cudaMemcpyDeviceToHost, c->stream);
+  cudaStreamSynchronize(c->stream);
+  return v;
+}
+
+// aggregates of level L (device agg, returns nc); MIS-2 by repeated distance-2 maxima
+int amg_aggregate(Ctx *c, AmgLevel &L, double *diag, long &nc_out) {
+  const long n = L.n;
+  unsigned char *strong = nullptr;
+  signed char *state = nullptr;
+  long long *kv = nullptr, *k1 = nullptr, *k2 = nullptr;
+  int *flag = nullptr, *rank = nullptr, *agg0 = nullptr, *agg1 = nullptr;
+  unsigned *cnt = nullptr;
+  DA(strong, L.nnz);
+  DA(state, n);
+  DA(kv, n);
+  DA(k1, n);
+  DA(k2, n);
+  DA(flag, n + 1);
+  DA(rank, n + 1);
+  DA(agg0, n);
+  DA(agg1, n);
+  DA(cnt, 1);
+  DA(L.agg, n);
+  const int g = grid_stream(c, n);
+  k_amg_strong<<<g, NT, 0, c->stream>>>(n, L.rp, L.ci, L.va, diag, AMG_THETA, strong);
+  CK(cudaMemsetAsync(state, 0, n, c->stream));
+  for (int it = 0; it < 1000; ++it) {
+    k_amg_mis_keys<<<g, NT, 0, c->stream>>>(n, state, kv);
+    k_amg_nbr_max<<<g, NT, 0, c->stream>>>(n, L.rp, L.ci, strong, kv, k1);
+    k_amg_nbr_max<<<g, NT, 0, c->stream>>>(n, L.rp, L.ci, strong, k1, k2);
+    CK(cudaMemsetAsync(cnt, 0, sizeof(unsigned), c->stream));
+    k_amg_mis_update<<<g, NT, 0, c->stream>>>(n, state, k2, cnt);
+    CKL();
+    if (read_back(c, cnt) == 0u) break;
+  }
+  k_amg_flag<<<g, NT, 0, c->stream>>>(n, state, flag);
+  CK(cudaMemsetAsync(flag + n, 0, sizeof(int), c->stream));
+  {
+    int r = scan_excl(c, flag, rank, n + 1);
+    if (r) return r;
+  }
+  const int nroot = read_back(c, rank + n);
+  k_amg_roots<<<g, NT, 0, c->stream>>>(n, state, rank, agg0, kv);
+  k_amg_nbr_max<<<g, NT, 0, c->stream>>>(n, L.rp, L.ci, strong, kv, k1);
+  k_amg_join<<<g, NT, 0, c->stream>>>(n, agg0, k1, agg1);
+  k_amg_assigned_keys<<<g, NT, 0, c->stream>>>(n, agg1, kv);
+  k_amg_nbr_max<<<g, NT, 0, c->stream>>>(n, L.rp, L.ci, strong, kv, k1);
+  k_amg_join<<<g, NT, 0, c->stream>>>(n, agg1, k1, L.agg);
+  k_amg_free_flag<<<g, NT, 0, c->stream>>>(n, L.agg, flag);
+  CKL();
+  {
+    int r = scan_excl(c, flag, rank, n + 1);
+    if (r) return r;
+  }
+  const int nfree = read_back(c, rank + n);
+  k_amg_singletons<<<g, NT, 0, c->stream>>>(n, rank, nroot, L.agg);
+  CKL();
+  CK(cudaStreamSynchronize(c->stream));
+  for (void *p : {(void *)strong, (void *)state, (void *)kv, (void *)k1, (void *)k2, (void *)flag, (void *)rank,
+                  (void *)agg0, (void *)agg1, (void *)cnt})
+    dfree(c, p);
+  nc_out = (long)nroot + nfree;
+  return 0;
+}
+
+// Galerkin A_c = P^T A P (stable radix sort of (agg_i nc + agg_j) keys, in-order run sums)
+int amg_galerkin(Ctx *c, const AmgLevel &L, long nc, AmgLevel &C) {
+  const long m = L.nnz;
+  unsigned long long *k0 = nullptr, *k1 = nullptr;
+  double *v0 = nullptr, *v1 = nullptr;
+  int *flag = nullptr, *pos = nullptr, *crow = nullptr, *cnt = nullptr;
+  DA(k0, m);
+  DA(k1, m);
+  DA(v0, m);
+  DA(v1, m);
+  DA(flag, m + 1);
+  DA(pos, m + 1);
+  k_amg_expand<<<grid_stream(c, L.n), NT, 0, c->stream>>>(L.n, L.rp, L.ci, L.va, L.agg, nc, k0, v0);
+  CKL();
+  int bits = 1;
+  while ((1ULL << bits) < (unsigned long long)nc * (unsigned long long)nc) ++bits;
+  {
+    size_t tb = 0;
+    CK(cub::DeviceRadixSort::SortPairs(nullptr, tb, k0, k1, v0, v1, (int)m, 0, bits, c->stream));
+    char *tmp = nullptr;
+    DA(tmp, tb);
+    CK(cub::DeviceRadixSort::SortPairs(tmp, tb, k0, k1, v0, v1, (int)m, 0, bits, c->stream));
+    CK(cudaStreamSynchronize(c->stream));
+    dfree(c, tmp);
+  }
+  k_amg_run_flags<<<grid_stream(c, m), NT, 0, c->stream>>>(m, k1, flag);
+  CK(cudaMemsetAsync(flag + m, 0, sizeof(int), c->stream));
+  {
+    int r = scan_excl(c, flag, pos, m + 1);
+    if (r) return r;
+  }
+  const long nnzc = read_back(c, pos + m);
+  C.n = nc;
+  C.nnz = nnzc;
+  DA(crow, nnzc);
+  DA(C.ci, nnzc);
+  DA(C.va, nnzc);
+  DA(C.rp, nc + 1);
+  DA(cnt, nc + 1);
+  k_amg_run_reduce<<<grid_stream(c, m), NT, 0, c->stream>>>(m, k1, v1, flag, pos, nc, crow, C.ci, C.va);
+  CK(cudaMemsetAsync(cnt, 0, (nc + 1) * sizeof(int), c->stream));
+  k_amg_row_count<<<grid_stream(c, nnzc), NT, 0, c->stream>>>(nnzc, crow, cnt);
+  CKL();
+  {
+    int r = scan_excl(c, cnt, C.rp, nc + 1);
+    if (r) return r;
+  }
+  for (void *p : {(void *)k0, (void *)k1, (void *)v0, (void *)v1, (void *)flag, (void *)pos, (void *)crow,
+                  (void *)cnt})
+    dfree(c, p);
+  return 0;
+}
+
+int amg_members(Ctx *c, AmgLevel &L) {
+  int *cnt = nullptr, *fill = nullptr;
+  DA(cnt, L.nc + 1);
+  DA(fill, L.nc + 1);
+  DA(L.moff, L.nc + 1);
+  DA(L.mem, L.n);
+  CK(cudaMemsetAsync(cnt, 0, (L.nc + 1) * sizeof(int), c->stream));
+  CK(cudaMemsetAsync(fill, 0, (L.nc + 1) * sizeof(int), c->stream));
+  k_amg_row_count<<<grid_stream(c, L.n), NT, 0, c->stream>>>(L.n, L.agg, cnt);
+  CKL();
+  {
+    int r = scan_excl(c, cnt, L.moff, L.nc + 1);
+    if (r) return r;
+  }
+  k_amg_members<<<grid_stream(c, L.n), NT, 0, c->stream>>>(L.n, L.agg, L.moff, fill, L.mem);
+  k_amg_sort_members<<<grid_stream(c, L.nc), NT, 0, c->stream>>>(L.nc, L.moff, L.mem);
+  CKL();
+  CK(cudaStreamSynchronize(c->stream));
+  dfree(c, cnt);
+  dfree(c, fill);
+  return 0;
+}
+
+int amg_level_vectors(Ctx *c, AmgLevel &L) {
+  DA(L.b, L.n);
+  DA(L.x, L.n);
+  DA(L.t, L.n);
+  DA(L.y, L.n);
+  DA(L.sr, L.n);
+  DA(L.sd0, L.n);
+  DA(L.sd1, L.n);
+  return 0;
+}
+
+int build_amg(Ctx *c) {
+  c->amg.clear();
+  AmgLevel L0;
+  L0.n = c->np;
+  L0.nnz = c->nnzS;
+  L0.rp = c->s_rp;
+  L0.ci = c->s_ci;
+  L0.va = c->s_va;
+  L0.soff = c->s_soff;
+  L0.sci = c->s_sci;
+  L0.sva = c->s_sva;
+  L0.dinv = c->dSinv;
+  L0.lmax = c->lmax;
+  L0.owns_matrix = false;
+  c->amg.push_back(L0);
+  int r = amg_level_vectors(c, c->amg.back());
+  if (r) return r;
+  double *diag = c->sdiag;
+  while (true) {
+    AmgLevel &L = c->amg.back();
+    if (L.n <= AMG_COARSE_SIZE || (int)c->amg.size() >= AMG_MAX_LEVELS) break;
+    long nc = 0;
+    r = amg_aggregate(c, L, diag, nc);
+    if (r) return r;
+    if (nc > AMG_STAGNATION * L.n) {
+      dfree(c, L.agg);
+      L.agg = nullptr;
+      break;
+    }
+    L.nc = nc;
+    AmgLevel C;
+    r = amg_galerkin(c, L, nc, C);
+    if (r) return r;
+    r = amg_members(c, c->amg.back());
+    if (r) return r;
+    // coarse diagonal, Gershgorin bound, SELL copy, vectors
+    double *cdiag = nullptr;
+    DA(C.dinv, C.n);
+    DA(cdiag, C.n);
+    k_diag_inv<<<grid_stream(c, C.n), NT, 0, c->stream>>>(C.n, C.rp, C.ci, C.va, 0, C.dinv, cdiag, c->derr);
+    k_gershgorin<<<grid_stream(c, C.n), NT, 0, c->stream>>>(C.n, C.rp, C.ci, C.va, c->part, c->counter, c->st);
+    CKL();
+    C.lmax = read_back(c, &c->st->lmax);
+    if (read_back(c, c->derr)) return fail(c, VEM_ERR_DIAG_S, "non-positive diagonal in a coarse S_D level");
+    r = build_sell(c, C.n, C.rp, C.ci, C.va, &C.soff, &C.sci, &C.sva, &C.nnz_sell);
+    if (r) return r;
+    r = amg_level_vectors(c, C);
+    if (r) return r;
+    c->amg.push_back(C);
+    diag = cdiag;
+  }
+  AmgLevel &Lc = c->amg.back();
+  c->amg_dense = Lc.n <= AMG_COARSE_SIZE;
+  if (c->amg_dense) {
+    double *D = nullptr;
+    DA(D, (size_t)Lc.n * 2 * Lc.n);
+    DA(c->amg_cinv, (size_t)Lc.n * Lc.n);
+    k_amg_dense<<<grid_stream(c, Lc.n), NT, 0, c->stream>>>(Lc.n, Lc.rp, Lc.ci, Lc.va, D);
+    const int th = (int)std::min<long>(1024, std::max<long>(32, (Lc.n + 31) / 32 * 32));
+    k_amg_gauss_jordan<<<1, th, 2 * Lc.n * sizeof(double), c->stream>>>(Lc.n, D, c->amg_cinv, c->derr);
+    CKL();
+    CK(cudaStreamSynchronize(c->stream));
+    dfree(c, D);
+    if (read_back(c, c->derr)) return fail(c, VEM_ERR_DIAG_S, "coarsest S_D level not positive definite");
+  }
+  CK(cudaStreamSynchronize(c->stream));
+  return 0;
+}
+
 int upload_impl(Ctx *c, const vem_csr *M, const vem_csr *B, const vem_csr *W, double eps, const vem_layout *lay) {
   auto t0 = std::chrono::steady_clock::now();
   if (!M || !B) return fail(c, VEM_ERR_INVALID, "M and B are required");
@@ -1176,6 +1530,10 @@ int upload_impl(Ctx *c, const vem_csr *M, const vem_csr *B, const vem_csr *W, do
     if (rr) return rr;
   }
   CK(cudaStreamSynchronize(c->stream));
+  if (c->nb == 1) {   // S_D hierarchy for precond kind 3 (k = 0)
+    int rr = build_amg(c);
+    if (rr) return rr;
+  }
   {
     int rr = apply_l2_window(c);
     if (rr) return rr;
@@ -1348,7 +1706,7 @@ int vem_mixed_schur_spmv(vem_ctx *h, const double *x, double *y) {
 int vem_mixed_precond_apply(vem_ctx *h, int32_t kind, const double *v, double *z, int64_t *inner_its) {
   if (!h || !v || !z) return VEM_ERR_INVALID;
   Ctx *c = h->impl;
-  if (kind < 0 || kind > 2) return fail(c, VEM_ERR_PRECOND, "unsupported precond_kind %d", kind);
+  if (kind < 0 || kind > 3) return fail(c, VEM_ERR_PRECOND, "unsupported precond_kind %d", kind);
   if (kind == VEM_PRECOND_BLOCK_REG && !c->has_reg) return fail(c, VEM_ERR_PRECOND, "Block-Reg needs eps > 0");
   int64_t its = 0;
   int r = enter(c);
@@ -1405,6 +1763,8 @@ int vem_mixed_get_info(vem_ctx *h, vem_info *info) {
   info->sm_count = c->sm_count;
   info->device_bytes = c->device_bytes;
   info->l2_window_bytes = (int64_t)c->l2_window_bytes;
+  info->amg_levels = (int32_t)c->amg.size();
+  info->amg_coarsest = c->amg.empty() ? 0 : c->amg.back().n;
   return VEM_OK;
 }
 
@@ -1427,6 +1787,15 @@ int vem_mixed_kernel_stats(vem_ctx *h, vem_kernel_stats *s, int32_t reset) {
   flush_timing(c);
   *s = c->stats;
   if (reset) memset(&c->stats, 0, sizeof(c->stats));
+  return VEM_OK;
+}
+
+int vem_mixed_amg_level(vem_ctx *h, int32_t level, int64_t *n, int64_t *nnz) {
+  if (!h || !n || !nnz) return VEM_ERR_INVALID;
+  Ctx *c = h->impl;
+  if (level < 0 || level >= (int)c->amg.size()) return VEM_ERR_INVALID;
+  *n = c->amg[level].n;
+  *nnz = c->amg[level].nnz;
   return VEM_OK;
 }
 

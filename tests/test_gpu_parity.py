@@ -173,6 +173,32 @@ def test_cgs2_option_parity(name):
     sv.close()
 
 
+@pytest.mark.parametrize("name", ["C1", "C3s"])
+def test_amg_hierarchy_matches_oracle(name):
+    """Block-Schur-AMG (kind 3): the device aggregation reproduces the oracle's
+    hierarchy (rows and nnz of every level, integers), the V-cycle apply agrees
+    to 1e-10, and the solve is within the iteration band."""
+    from oracle.amg import AMG
+    s = system(name)
+    cfg = configs.CONFIGS[name]
+    SD = O.schur_diag(s.M, s.B)
+    h = AMG(SD)
+    sv = solver_for(s, restart=cfg.restart)
+    assert sv.amg_levels() == [(lev.A.shape[0], lev.A.nnz) for lev in h.levels]
+    v = RNG.normal(size=s.n)
+    z, _ = sv.precond_apply(pkg.PRECOND_BLOCK_SCHUR_AMG, torch.from_numpy(v).cuda())
+    nu = s.layout.n_u
+    zo = np.concatenate([v[:nu] / s.M.diagonal(), -h.vcycle(v[nu:])])
+    assert rel_inf(z.cpu().numpy()[:nu], zo[:nu]) <= 1e-12
+    assert rel_inf(z.cpu().numpy()[nu:], zo[nu:]) <= 1e-10
+    ref, lo, hi = oracle_iteration_band(s, 3, cfg.restart, 0.0)
+    res = sv.solve(torch.from_numpy(s.rhs).cuda(), 1e-10, 10000, 3)
+    assert res.report["converged"] == 1
+    assert lo - 2 <= res.report["iterations"] <= hi + 2, (res.report["iterations"], lo, hi)
+    assert rel_inf(res.u.cpu().numpy(), ref.x[:nu]) <= 1e-8 and rel_inf(res.p.cpu().numpy(), ref.x[nu:]) <= 1e-8
+    sv.close()
+
+
 def test_solve_host_matches_device_and_is_deterministic():
     s = system("C3s")
     sv = solver_for(s, restart=50)

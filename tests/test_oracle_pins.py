@@ -176,3 +176,65 @@ def test_spmv_definition():
     x = RNG.normal(size=s.n)
     A = sp.bmat([[s.M, s.B.T], [s.B, None]]).toarray()
     assert np.abs(O.spmv_saddle(s.M, s.B, x) - A @ x).max() < 1e-13 * np.abs(A @ x).max()
+
+
+# ---------------------------------------------------------------------------
+# aggregation multigrid for S_D (oracle/amg.py, precond kind 3)
+# ---------------------------------------------------------------------------
+def _c3s_sd():
+    s = configs.CONFIGS["C3s"].build()
+    return s, O.schur_diag(s.M, s.B)
+
+
+def test_amg_aggregates_are_a_valid_mis2_partition():
+    from oracle import amg
+    s, SD = _c3s_sd()
+    agg, nc, is_root = amg.aggregate(SD)
+    assert agg.min() == 0 and agg.max() == nc - 1 and np.unique(agg).size == nc
+    G = amg.strong_graph(SD)
+    roots = np.nonzero(is_root)[0]
+    assert np.array_equal(agg[roots], np.arange(roots.size))
+    # MIS-2: no two roots within strong distance 2
+    G2 = (G @ G).tocsr()
+    sub = G2[roots][:, roots]
+    assert sub.nnz == roots.size  # only the diagonal
+    # every non-singleton node is within distance 2 of its aggregate's root
+    root_of = np.full(nc, -1)
+    root_of[agg[roots]] = roots
+    for i in range(0, SD.shape[0], 7):
+        r = root_of[agg[i]]
+        if r >= 0:
+            assert G2[i, r] != 0
+
+
+def test_amg_galerkin_conserves_row_sums():
+    from oracle import amg
+    s, SD = _c3s_sd()
+    agg, nc, _ = amg.aggregate(SD)
+    Ac = amg.galerkin(SD, agg, nc)
+    rs = np.asarray(SD.sum(axis=1)).ravel()
+    assert np.allclose(np.asarray(Ac.sum(axis=1)).ravel(), np.bincount(agg, weights=rs, minlength=nc),
+                       rtol=1e-12, atol=1e-14 * abs(rs).max())
+    assert abs(Ac - Ac.T).max() <= 1e-14 * abs(Ac).max()
+
+
+def test_amg_one_level_is_exact_and_vcycle_symmetric():
+    from oracle import amg
+    s, SD = _c3s_sd()
+    one = amg.AMG(SD, coarse_size=SD.shape[0])
+    b = RNG.normal(size=SD.shape[0])
+    assert np.abs(SD @ one.vcycle(b) - b).max() < 1e-9 * np.abs(b).max()
+    h = amg.AMG(SD)
+    assert len(h.levels) >= 2
+    u, v = RNG.normal(size=SD.shape[0]), RNG.normal(size=SD.shape[0])
+    assert abs(u @ h.vcycle(v) - v @ h.vcycle(u)) <= 1e-10 * abs(u @ h.vcycle(v))
+
+
+def test_block_schur_amg_gmres_vs_lu():
+    for name in ("C1", "C3s"):
+        s = configs.CONFIGS[name].build()
+        xd = O.dense_solve(s.M, s.B, s.rhs) if s.n < 6000 else None
+        r = O.solve(s.M, s.B, s.rhs, O.PRECOND_BLOCK_SCHUR_AMG, 1e-10, configs.CONFIGS[name].restart)
+        assert r.converged
+        if xd is not None:
+            assert np.abs(r.x - xd).max() <= 1e-8 * np.abs(xd).max()
