@@ -632,6 +632,10 @@ void amg_vcycle(Ctx *c, size_t l, const int *gate) {
     k_spmv<<<grid_for(L.n), NT, 0, c->stream>>>(0, L.n, A, L.x, L.t, L.b, 1, gate);
   }
   amg_smooth(c, L, L.t, L.y, AMG_DEGREE, gate);
+  if (l > 0) {   // level result x + y (the top level folds this into z_p = -(x + y))
+    TimeScope ts(c, VEM_K_PRECOND_VEC, 24.0 * L.n);
+    k_amg_add<<<grid_stream(c, L.n), NT, 0, c->stream>>>(L.n, L.x, L.y, 1.0, L.x, gate);
+  }
 }
 
 int enqueue_block_schur_amg(Ctx *c, const double *v, const double *scale, double *z, const int *gate) {
