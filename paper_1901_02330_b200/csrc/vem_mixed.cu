@@ -113,6 +113,8 @@ struct Ctx {
   // is bracketed by its own event pair (captured as event-record graph nodes);
   // the host reads the pairs of the executed steps after every cycle.
   int sample_slot = -1;
+  bool sample_recorded = false;        // set when an enqueue recorded a sample pair
+  bool sample_recorded_kind[4] = {false, false, false, false};
   std::vector<cudaEvent_t> samp_a, samp_b;
   // misc
   std::string err;
@@ -230,13 +232,15 @@ int ensure_samples(Ctx *c) {
 }
 // after a cycle that executed `steps` Arnoldi steps (stream synchronised)
 void collect_samples(Ctx *c, int steps, double bytes) {
-  if (c->opts.timing != 2) return;
+  if (c->opts.timing != 2 || !c->sample_recorded) return;
   for (int j = 0; j < steps && j < (int)c->samp_a.size(); ++j) {
     float ms = 0.f;
     if (cudaEventElapsedTime(&ms, c->samp_a[j], c->samp_b[j]) == cudaSuccess) {
       c->stats.launches[VEM_K_CHEB] += 1;
       c->stats.ms[VEM_K_CHEB] += ms;
       c->stats.bytes[VEM_K_CHEB] += bytes;
+    } else {
+      (void)cudaGetLastError();   // never leave a query error for the next launch check
     }
   }
 }
@@ -400,6 +404,7 @@ int enqueue_block_schur(Ctx *c, const double *v, const double *scale, double *z,
     // k = 0: init fused into the first Chebyshev step (one launch over all n rows)
     const bool sample = c->opts.timing == 2 && c->sample_slot >= 0 && deg / 2 == 1;
     if (sample) cudaEventRecordWithFlags(c->samp_a[c->sample_slot], c->stream, cudaEventRecordExternal);
+    c->sample_recorded |= sample;
     {
       TimeScope ts(c, VEM_K_CHEB, bytes_cheb(c) - 16.0 * c->np + 24.0 * c->nu);
       k_cheb_first<<<grid_for(c->n), NT, 0, c->stream>>>(c->nu, c->np, sellS(c), v, scale, c->dMinv, c->dSinv,
@@ -413,6 +418,7 @@ int enqueue_block_schur(Ctx *c, const double *v, const double *scale, double *z,
       const int last = i == deg - 1 ? 1 : 0;
       const bool smp = c->opts.timing == 2 && c->sample_slot >= 0 && i == deg / 2;
       if (smp) cudaEventRecordWithFlags(c->samp_a[c->sample_slot], c->stream, cudaEventRecordExternal);
+      c->sample_recorded |= smp;
       {
         TimeScope ts(c, VEM_K_CHEB, bytes_cheb(c));
         launch_cheb(c, dold, dnew, c1[i - 1], c2[i - 1], last, z + c->nu, gate);
@@ -449,6 +455,7 @@ int enqueue_block_schur(Ctx *c, const double *v, const double *scale, double *z,
       const bool sample = c->opts.timing == 2 && c->sample_slot >= 0 && i == deg / 2;
       // cudaEventRecordExternal: inside a capture this becomes a real event-record node
       if (sample) cudaEventRecordWithFlags(c->samp_a[c->sample_slot], c->stream, cudaEventRecordExternal);
+      c->sample_recorded |= sample;
       {
         TimeScope ts(c, VEM_K_CHEB, bytes_cheb(c));
         launch_cheb(c, dold, dnew, c1[i - 1], c2[i - 1], last, z + c->nu, gate);
@@ -820,6 +827,8 @@ int solve_impl(Ctx *c, const double *rhs, double tol, int maxit, int kind, doubl
       int rs = ensure_samples(c);
       if (rs) return rs;
     }
+    // a replayed graph records its samples only if its capture did (kind 1, k = 0)
+    c->sample_recorded = c->cycle_exec[kind] ? c->sample_recorded_kind[kind] : false;
     int restarts = 0, cycles = 0;
     int its_before = c->hst->g.its;
     while (c->hst->g.its < maxit || cycles == 0) {
@@ -836,6 +845,7 @@ int solve_impl(Ctx *c, const double *rhs, double tol, int maxit, int kind, doubl
           if (e != cudaSuccess) return fail(c, VEM_ERR_CUDA, "cycle capture failed: %s", cudaGetErrorString(e));
           CK(cudaGraphInstantiate(&c->cycle_exec[kind], gr, 0));
           cudaGraphDestroy(gr);
+          c->sample_recorded_kind[kind] = c->sample_recorded;
         }
         CK(cudaGraphLaunch(c->cycle_exec[kind], c->stream));
       } else {
