@@ -219,6 +219,46 @@ __global__ void __launch_bounds__(256) k_amg_cheb_step(long n, Sell A, const dou
   d_new[i] = dn;
   x[i] += dn;
 }
+// warp-per-row CSR variants for the coarse levels, whose Galerkin rows are long
+// (tens to hundreds of entries): one warp per row, lane-strided, xor-tree sum.
+__device__ __forceinline__ double warp_row_dot(const int *__restrict__ rp, const int *__restrict__ ci,
+                                               const double *__restrict__ va, const double *__restrict__ x,
+                                               long row) {
+  const int lane = threadIdx.x & 31;
+  double acc = 0.0;
+  for (int k = rp[row] + lane; k < rp[row + 1]; k += 32) acc = fma(va[k], x[ci[k]], acc);
+  return warp_sum(acc);
+}
+__global__ void __launch_bounds__(256) k_amg_cheb_step_w(long n, const int *__restrict__ rp,
+                                                         const int *__restrict__ ci, const double *__restrict__ va,
+                                                         const double *__restrict__ dinv, double *__restrict__ r,
+                                                         const double *__restrict__ d_old, double *__restrict__ d_new,
+                                                         double *__restrict__ x, double c1, double c2,
+                                                         const int *gate) {
+  if (!*gate) return;
+  const long i = ((long)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  if (i >= n) return;
+  const double ad = warp_row_dot(rp, ci, va, d_old, i);
+  if ((threadIdx.x & 31) == 0) {
+    const double rn = r[i] - ad;
+    const double dn = c1 * d_old[i] + c2 * (dinv[i] * rn);
+    r[i] = rn;
+    d_new[i] = dn;
+    x[i] += dn;
+  }
+}
+// t = b - A x, warp per row
+__global__ void __launch_bounds__(256) k_amg_resid_w(long n, const int *__restrict__ rp, const int *__restrict__ ci,
+                                                     const double *__restrict__ va, const double *__restrict__ x,
+                                                     const double *__restrict__ b, double *__restrict__ t,
+                                                     const int *gate) {
+  if (!*gate) return;
+  const long i = ((long)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  if (i >= n) return;
+  const double ax = warp_row_dot(rp, ci, va, x, i);
+  if ((threadIdx.x & 31) == 0) t[i] = b[i] - ax;
+}
+
 // bc[a] = sum over members of r (index order)
 __global__ void k_amg_restrict(long nc, const int *__restrict__ moff, const int *__restrict__ mem,
                                const double *__restrict__ r, double *__restrict__ bc, const int *gate) {

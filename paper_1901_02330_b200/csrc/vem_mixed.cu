@@ -51,6 +51,7 @@ struct AmgLevel {
   long nc = 0;
   double *b = nullptr, *x = nullptr, *t = nullptr, *y = nullptr, *sr = nullptr, *sd0 = nullptr, *sd1 = nullptr;
   bool owns_matrix = true;
+  bool warp_rows = false;                      // coarse levels: long Galerkin rows -> warp per row
 };
 
 struct Ctx {
@@ -571,7 +572,7 @@ int run_pcg(Ctx *c, int64_t *inner_its) {
 // (oracle/amg.py AMG.vcycle, reading R22)
 // ----------------------------------------------------------------------------
 constexpr double AMG_THETA = 0.08, AMG_RATIO = 30.0, AMG_STAGNATION = 0.75;
-constexpr int AMG_COARSE_SIZE = 512, AMG_MAX_LEVELS = 12, AMG_DEGREE = 3, AMG_COARSE_DEGREE = 8;
+constexpr int AMG_COARSE_SIZE = 1024, AMG_MAX_LEVELS = 12, AMG_DEGREE = 3, AMG_COARSE_DEGREE = 8;
 
 void amg_cheb_coeffs(double lmax, int degree, double &inv_theta, std::vector<double> &c1, std::vector<double> &c2) {
   const double b = lmax, a = lmax / AMG_RATIO;
@@ -601,9 +602,24 @@ void amg_smooth(Ctx *c, AmgLevel &L, const double *b, double *out, int degree, c
   double *dold = L.sd0, *dnew = L.sd1;
   for (int i = 1; i < degree; ++i) {
     TimeScope ts(c, VEM_K_CHEB, 12.0 * L.nnz + 56.0 * L.n);
-    k_amg_cheb_step<<<grid_for(L.n), NT, 0, c->stream>>>(L.n, A, L.dinv, L.sr, dold, dnew, out, c1[i - 1],
-                                                         c2[i - 1], gate);
+    if (L.warp_rows)
+      k_amg_cheb_step_w<<<grid_for(L.n * 32), NT, 0, c->stream>>>(L.n, L.rp, L.ci, L.va, L.dinv, L.sr, dold, dnew,
+                                                                   out, c1[i - 1], c2[i - 1], gate);
+    else
+      k_amg_cheb_step<<<grid_for(L.n), NT, 0, c->stream>>>(L.n, A, L.dinv, L.sr, dold, dnew, out, c1[i - 1],
+                                                           c2[i - 1], gate);
     std::swap(dold, dnew);
+  }
+}
+
+// t = b - A x on level L
+void amg_residual(Ctx *c, AmgLevel &L, const int *gate) {
+  TimeScope ts(c, VEM_K_SPMV, 12.0 * L.nnz + 24.0 * L.n);
+  if (L.warp_rows) {
+    k_amg_resid_w<<<grid_for(L.n * 32), NT, 0, c->stream>>>(L.n, L.rp, L.ci, L.va, L.x, L.b, L.t, gate);
+  } else {
+    const Sell A{L.soff, L.sci, L.sva};
+    k_spmv<<<grid_for(L.n), NT, 0, c->stream>>>(0, L.n, A, L.x, L.t, L.b, 1, gate);
   }
 }
 
@@ -621,10 +637,7 @@ void amg_vcycle(Ctx *c, size_t l, const int *gate) {
   AmgLevel &C = c->amg[l + 1];
   const Sell A{L.soff, L.sci, L.sva};
   amg_smooth(c, L, L.b, L.x, AMG_DEGREE, gate);
-  {
-    TimeScope ts(c, VEM_K_SPMV, 12.0 * L.nnz + 24.0 * L.n);
-    k_spmv<<<grid_for(L.n), NT, 0, c->stream>>>(0, L.n, A, L.x, L.t, L.b, 1, gate);
-  }
+  amg_residual(c, L, gate);
   {
     TimeScope ts(c, VEM_K_PRECOND_VEC, 8.0 * L.n * 2 + 8.0 * C.n);
     k_amg_restrict<<<grid_stream(c, C.n), NT, 0, c->stream>>>(C.n, L.moff, L.mem, L.t, C.b, gate);
@@ -634,10 +647,7 @@ void amg_vcycle(Ctx *c, size_t l, const int *gate) {
     TimeScope ts(c, VEM_K_PRECOND_VEC, 8.0 * L.n * 3);
     k_amg_prolong_add<<<grid_stream(c, L.n), NT, 0, c->stream>>>(L.n, L.agg, C.x, L.x, gate);
   }
-  {
-    TimeScope ts(c, VEM_K_SPMV, 12.0 * L.nnz + 24.0 * L.n);
-    k_spmv<<<grid_for(L.n), NT, 0, c->stream>>>(0, L.n, A, L.x, L.t, L.b, 1, gate);
-  }
+  amg_residual(c, L, gate);
   amg_smooth(c, L, L.t, L.y, AMG_DEGREE, gate);
   if (l > 0) {   // level result x + y (the top level folds this into z_p = -(x + y))
     TimeScope ts(c, VEM_K_PRECOND_VEC, 24.0 * L.n);
@@ -1328,6 +1338,7 @@ int build_amg(Ctx *c) {
     if (read_back(c, c->derr)) return fail(c, VEM_ERR_DIAG_S, "non-positive diagonal in a coarse S_D level");
     r = build_sell(c, C.n, C.rp, C.ci, C.va, &C.soff, &C.sci, &C.sva, &C.nnz_sell);
     if (r) return r;
+    C.warp_rows = (double)C.nnz / (double)C.n > 16.0;
     r = amg_level_vectors(c, C);
     if (r) return r;
     c->amg.push_back(C);
