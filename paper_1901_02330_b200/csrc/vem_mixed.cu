@@ -1338,7 +1338,7 @@ int build_amg(Ctx *c) {
     if (read_back(c, c->derr)) return fail(c, VEM_ERR_DIAG_S, "non-positive diagonal in a coarse S_D level");
     r = build_sell(c, C.n, C.rp, C.ci, C.va, &C.soff, &C.sci, &C.sva, &C.nnz_sell);
     if (r) return r;
-    C.warp_rows = (double)C.nnz / (double)C.n > 16.0;
+    C.warp_rows = true;   // coarse Galerkin rows: irregular lengths, warp per row
     r = amg_level_vectors(c, C);
     if (r) return r;
     c->amg.push_back(C);
