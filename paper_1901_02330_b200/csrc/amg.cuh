@@ -282,14 +282,42 @@ __global__ void k_amg_add(long n, const double *__restrict__ x, const double *__
   for (long i = (long)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (long)gridDim.x * blockDim.x)
     out[i] = sgn * (y ? x[i] + y[i] : x[i]);
 }
-__global__ void k_amg_dense_mv(long n, const double *__restrict__ inv, const double *__restrict__ b,
-                               double *__restrict__ x, const int *gate) {
+// x = inv b, one warp per row (coalesced row reads)
+__global__ void __launch_bounds__(256) k_amg_dense_mv(long n, const double *__restrict__ inv,
+                                                      const double *__restrict__ b, double *__restrict__ x,
+                                                      const int *gate) {
   if (!*gate) return;
-  for (long i = (long)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (long)gridDim.x * blockDim.x) {
-    double s = 0.0;
-    for (long j = 0; j < n; ++j) s = fma(inv[i * n + j], b[j], s);
-    x[i] = s;
-  }
+  const long i = ((long)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  if (i >= n) return;
+  const int lane = threadIdx.x & 31;
+  double s = 0.0;
+  for (long j = lane; j < n; j += 32) s = fma(inv[i * n + j], b[j], s);
+  s = warp_sum(s);
+  if (lane == 0) x[i] = s;
+}
+
+// first smoother step fused with the init (SELL levels): d0 = D^-1 b / theta gathered
+// on the fly; r = b - A d0; d1 = c1 d0 + c2 D^-1 r; x = d0 + d1
+struct GatherD0b {
+  const double *__restrict__ b, *__restrict__ dinv;
+  double it;
+  __device__ __forceinline__ double operator()(int c) const { return dinv[c] * b[c] * it; }
+};
+__global__ void __launch_bounds__(256) k_amg_cheb_first(long n, Sell A, const double *__restrict__ dinv,
+                                                        const double *__restrict__ b, double inv_theta, double c1,
+                                                        double c2, double *__restrict__ r, double *__restrict__ d_new,
+                                                        double *__restrict__ x, const int *gate) {
+  if (!*gate) return;
+  const long i = (long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  const double ad = sell_dot(A, i, GatherD0b{b, dinv, inv_theta});
+  const double bi = b[i];
+  const double d0 = dinv[i] * bi * inv_theta;
+  const double rn = bi - ad;
+  const double dn = c1 * d0 + c2 * (dinv[i] * rn);
+  r[i] = rn;
+  d_new[i] = dn;
+  x[i] = d0 + dn;
 }
 // Block-Schur-AMG top: z_u = s v_u ./ diag(M), b0 = s v_p
 __global__ void k_amg_top(long nu, long np, const double *__restrict__ v, const double *scale,

@@ -178,7 +178,7 @@ inline int grid_for(long work, int per_block = NT) {
 }
 inline int grid_stream(Ctx *c, long n) {   // grid-stride kernels: a few waves of 148 SMs
   long g = (n + NT - 1) / NT;
-  return (int)std::max<long>(1, std::min<long>(g, (long)c->sm_count * 8));
+  return (int)std::max<long>(1, std::min<long>(g, (long)c->sm_count * 32));
 }
 int pick_group(double avg) {
   if (avg < 3) return 2;
@@ -595,6 +595,19 @@ void amg_smooth(Ctx *c, AmgLevel &L, const double *b, double *out, int degree, c
   std::vector<double> c1, c2;
   amg_cheb_coeffs(L.lmax, degree, it, c1, c2);
   const Sell A{L.soff, L.sci, L.sva};
+  if (!L.warp_rows && degree > 1) {   // init fused into the first step
+    TimeScope ts(c, VEM_K_CHEB, 12.0 * L.nnz + 48.0 * L.n);
+    k_amg_cheb_first<<<grid_for(L.n), NT, 0, c->stream>>>(L.n, A, L.dinv, b, it, c1[0], c2[0], L.sr, L.sd1, out,
+                                                          gate);
+    double *dold = L.sd1, *dnew = L.sd0;
+    for (int i = 2; i < degree; ++i) {
+      TimeScope ts2(c, VEM_K_CHEB, 12.0 * L.nnz + 56.0 * L.n);
+      k_amg_cheb_step<<<grid_for(L.n), NT, 0, c->stream>>>(L.n, A, L.dinv, L.sr, dold, dnew, out, c1[i - 1],
+                                                           c2[i - 1], gate);
+      std::swap(dold, dnew);
+    }
+    return;
+  }
   {
     TimeScope ts(c, VEM_K_PRECOND_VEC, 40.0 * L.n);
     k_amg_cheb_init<<<grid_stream(c, L.n), NT, 0, c->stream>>>(L.n, L.dinv, b, it, L.sr, L.sd0, out, gate);
@@ -628,7 +641,7 @@ void amg_vcycle(Ctx *c, size_t l, const int *gate) {
   if (l + 1 == c->amg.size()) {   // coarsest
     if (c->amg_dense) {
       TimeScope ts(c, VEM_K_PRECOND_VEC, 8.0 * L.n * L.n);
-      k_amg_dense_mv<<<grid_stream(c, L.n), NT, 0, c->stream>>>(L.n, c->amg_cinv, L.b, L.x, gate);
+      k_amg_dense_mv<<<grid_for(L.n * 32), NT, 0, c->stream>>>(L.n, c->amg_cinv, L.b, L.x, gate);
     } else {
       amg_smooth(c, L, L.b, L.x, AMG_COARSE_DEGREE, gate);
     }
@@ -1309,6 +1322,15 @@ int build_amg(Ctx *c) {
   c->amg.push_back(L0);
   int r = amg_level_vectors(c, c->amg.back());
   if (r) return r;
+  {  // the fine-level smoother works in the L2-resident Chebyshev pool (kinds 1 and 3 never overlap)
+    AmgLevel &F = c->amg.back();
+    dfree(c, F.sr);
+    dfree(c, F.sd0);
+    dfree(c, F.sd1);
+    F.sr = c->cr;
+    F.sd0 = c->cd0;
+    F.sd1 = c->cd1;
+  }
   double *diag = c->sdiag;
   while (true) {
     AmgLevel &L = c->amg.back();
@@ -1338,7 +1360,7 @@ int build_amg(Ctx *c) {
     if (read_back(c, c->derr)) return fail(c, VEM_ERR_DIAG_S, "non-positive diagonal in a coarse S_D level");
     r = build_sell(c, C.n, C.rp, C.ci, C.va, &C.soff, &C.sci, &C.sva, &C.nnz_sell);
     if (r) return r;
-    C.warp_rows = true;   // coarse Galerkin rows: irregular lengths, warp per row
+    C.warp_rows = C.n < 100000;   // small coarse levels: warp per row (latency), else SELL-32
     r = amg_level_vectors(c, C);
     if (r) return r;
     c->amg.push_back(C);
