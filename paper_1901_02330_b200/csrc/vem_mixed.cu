@@ -589,8 +589,10 @@ void amg_cheb_coeffs(double lmax, int degree, double &inv_theta, std::vector<dou
   }
 }
 
-// out = C_degree(b) on level L (x0 = 0)
-void amg_smooth(Ctx *c, AmgLevel &L, const double *b, double *out, int degree, const int *gate) {
+// out = C_degree(b) on level L (x0 = 0); `sample`: bracket the second step with the
+// sampled-timing events (fine-level pre-smoothing, timing = 2)
+void amg_smooth(Ctx *c, AmgLevel &L, const double *b, double *out, int degree, const int *gate,
+                bool sample = false) {
   double it;
   std::vector<double> c1, c2;
   amg_cheb_coeffs(L.lmax, degree, it, c1, c2);
@@ -601,9 +603,15 @@ void amg_smooth(Ctx *c, AmgLevel &L, const double *b, double *out, int degree, c
                                                           gate);
     double *dold = L.sd1, *dnew = L.sd0;
     for (int i = 2; i < degree; ++i) {
-      TimeScope ts2(c, VEM_K_CHEB, 12.0 * L.nnz + 56.0 * L.n);
-      k_amg_cheb_step<<<grid_for(L.n), NT, 0, c->stream>>>(L.n, A, L.dinv, L.sr, dold, dnew, out, c1[i - 1],
-                                                           c2[i - 1], gate);
+      const bool smp = sample && i == 2 && c->opts.timing == 2 && c->sample_slot >= 0;
+      if (smp) cudaEventRecordWithFlags(c->samp_a[c->sample_slot], c->stream, cudaEventRecordExternal);
+      c->sample_recorded |= smp;
+      {
+        TimeScope ts2(c, VEM_K_CHEB, 12.0 * L.nnz + 56.0 * L.n);
+        k_amg_cheb_step<<<grid_for(L.n), NT, 0, c->stream>>>(L.n, A, L.dinv, L.sr, dold, dnew, out, c1[i - 1],
+                                                             c2[i - 1], gate);
+      }
+      if (smp) cudaEventRecordWithFlags(c->samp_b[c->sample_slot], c->stream, cudaEventRecordExternal);
       std::swap(dold, dnew);
     }
     return;
@@ -648,8 +656,7 @@ void amg_vcycle(Ctx *c, size_t l, const int *gate) {
     return;
   }
   AmgLevel &C = c->amg[l + 1];
-  const Sell A{L.soff, L.sci, L.sva};
-  amg_smooth(c, L, L.b, L.x, AMG_DEGREE, gate);
+  amg_smooth(c, L, L.b, L.x, AMG_DEGREE, gate, l == 0);
   amg_residual(c, L, gate);
   {
     TimeScope ts(c, VEM_K_PRECOND_VEC, 8.0 * L.n * 2 + 8.0 * C.n);
