@@ -22,7 +22,8 @@ for name in names:
     t_asm = time.time() - t0
     sv = pkg.VemMixed(s.M, s.B, eps=eps_for(s), layout=s.layout, opts=pkg.default_options(restart=cfg.restart))
     rhs = torch.from_numpy(s.rhs).cuda()
-    for kind in cfg.precs:
+    kinds = list(cfg.precs) + ([3] if s.layout.n_p_dof == 1 and 1 in cfg.precs else [])
+    for kind in kinds:
         r = sv.solve(rhs, cfg.rtol, maxit, kind)
         u, p = r.u.cpu().numpy(), r.p.cpu().numpy()
         cons = float(np.abs(s.B @ u - s.f).max() / np.abs(s.f).max())
