@@ -895,22 +895,59 @@ __global__ void __launch_bounds__(256) k_cheb_resid(long np, Sell S, double *__r
   r[row] -= sell_dot(S, row, GatherX{d_old});
 }
 
-// block half of a Chebyshev step (mode 0) or the init (mode 1: d = D^-1 r * c2, x = d)
+// ---------------------------------------------------------------------------
+// Tiled element-block apply: a 256-thread block walks tiles of TE = 256 / NB
+// elements; the tile's inverse blocks (TE NB^2 doubles) and its vector rows are
+// staged in shared memory with coalesced loads, then thread t computes row t of
+// D_B^-1 v for the tile and every vector update is a coalesced row access.
+// ---------------------------------------------------------------------------
+template <int NB>
+struct BlkTile {
+  static constexpr int TE = 256 / NB;
+  static constexpr int ROWS = TE * NB;
+};
+
+// stage inverse blocks and one vector of the tile [e0, e0 + te) into shared memory
+template <int NB>
+__device__ __forceinline__ void stage_blk(const double *__restrict__ inv, const double *__restrict__ v, long e0,
+                                          int te, double *sinv, double *sv) {
+  const long base = e0 * NB;
+  for (int q = threadIdx.x; q < te * NB * NB; q += blockDim.x) sinv[q] = inv[base * NB + q];
+  for (int q = threadIdx.x; q < te * NB; q += blockDim.x) sv[q] = v[base + q];
+}
+template <int NB>
+__device__ __forceinline__ double row_blk(const double *sinv, const double *sv, int t) {
+  const int el = t / NB, i = t - el * NB;
+  const double *a = sinv + el * NB * NB + i * NB;
+  const double *x = sv + el * NB;
+  double s = 0.0;
+#pragma unroll
+  for (int j = 0; j < NB; ++j) s = fma(a[j], x[j], s);
+  return s;
+}
+
+// block half of a Chebyshev step (mode 0) or the init (mode 1: d = c2 D^-1 r, x = d)
 //   d_new = c1 d_old + c2 D_B^-1 r ; x += d_new ; last -> z_p = -x
 template <int NB>
-__global__ void k_cheb_block(long ne, const double *__restrict__ inv, const double *__restrict__ r,
-                             const double *__restrict__ d_old, double *__restrict__ d_new, double *__restrict__ x,
-                             double c1, double c2, int mode, int last, double *__restrict__ zp, const int *gate) {
+__global__ void __launch_bounds__(256) k_cheb_block(long ne, const double *__restrict__ inv,
+                                                    const double *__restrict__ r, const double *__restrict__ d_old,
+                                                    double *__restrict__ d_new, double *__restrict__ x, double c1,
+                                                    double c2, int mode, int last, double *__restrict__ zp,
+                                                    const int *gate) {
+  __shared__ double sinv[BlkTile<NB>::TE * NB * NB];
+  __shared__ double sv[BlkTile<NB>::ROWS];
   if (!*gate) return;
-  for (long e = (long)blockIdx.x * blockDim.x + threadIdx.x; e < ne; e += (long)gridDim.x * blockDim.x) {
-    double rv[NB], t[NB];
-#pragma unroll
-    for (int i = 0; i < NB; ++i) rv[i] = r[e * NB + i];
-    block_mv<NB>(inv, e, rv, t);
-#pragma unroll
-    for (int i = 0; i < NB; ++i) {
-      const long k = e * NB + i;
-      const double dn = mode ? c2 * t[i] : fma(c1, d_old[k], c2 * t[i]);
+  constexpr int TE = BlkTile<NB>::TE;
+  for (long e0 = (long)blockIdx.x * TE; e0 < ne; e0 += (long)gridDim.x * TE) {
+    const int te = (int)min((long)TE, ne - e0);
+    __syncthreads();
+    stage_blk<NB>(inv, r, e0, te, sinv, sv);
+    __syncthreads();
+    const int t = threadIdx.x;
+    if (t < te * NB) {
+      const long k = e0 * NB + t;
+      const double tv = row_blk<NB>(sinv, sv, t);
+      const double dn = mode ? c2 * tv : fma(c1, d_old[k], c2 * tv);
       const double xn = mode ? dn : x[k] + dn;
       if (last) {
         zp[k] = -xn;
@@ -924,28 +961,34 @@ __global__ void k_cheb_block(long ne, const double *__restrict__ inv, const doub
 
 // block PCG init: x = 0, r = b, p_prev = 0, z = D_B^-1 b; rz = r.z, bn = ||b||
 template <int NB>
-__global__ void k_pcg_init_blk(long ne, const double *__restrict__ inv, const double *__restrict__ b,
-                               double *__restrict__ x, double *__restrict__ r, double *__restrict__ z,
-                               double *__restrict__ p0, double *part, unsigned *counter, DevState *st, double rtol,
-                               int maxit, const int *gate) {
+__global__ void __launch_bounds__(256) k_pcg_init_blk(long ne, const double *__restrict__ inv,
+                                                      const double *__restrict__ b, double *__restrict__ x,
+                                                      double *__restrict__ r, double *__restrict__ z,
+                                                      double *__restrict__ p0, double *part, unsigned *counter,
+                                                      DevState *st, double rtol, int maxit, const int *gate) {
+  __shared__ double sinv[BlkTile<NB>::TE * NB * NB];
+  __shared__ double sv[BlkTile<NB>::ROWS];
   __shared__ double sh[64];
+  constexpr int TE = BlkTile<NB>::TE;
   const bool on = *gate != 0;
   double v[2] = {0.0, 0.0};
   if (on) {
-    for (long e = (long)blockIdx.x * blockDim.x + threadIdx.x; e < ne; e += (long)gridDim.x * blockDim.x) {
-      double rv[NB], t[NB];
-#pragma unroll
-      for (int i = 0; i < NB; ++i) rv[i] = b[e * NB + i];
-      block_mv<NB>(inv, e, rv, t);
-#pragma unroll
-      for (int i = 0; i < NB; ++i) {
-        const long k = e * NB + i;
+    for (long e0 = (long)blockIdx.x * TE; e0 < ne; e0 += (long)gridDim.x * TE) {
+      const int te = (int)min((long)TE, ne - e0);
+      __syncthreads();
+      stage_blk<NB>(inv, b, e0, te, sinv, sv);
+      __syncthreads();
+      const int t = threadIdx.x;
+      if (t < te * NB) {
+        const long k = e0 * NB + t;
+        const double tv = row_blk<NB>(sinv, sv, t);
+        const double bk = sv[t];
         x[k] = 0.0;
-        r[k] = rv[i];
-        z[k] = t[i];
+        r[k] = bk;
+        z[k] = tv;
         p0[k] = 0.0;
-        v[0] += rv[i] * t[i];
-        v[1] += rv[i] * rv[i];
+        v[0] += bk * tv;
+        v[1] += bk * bk;
       }
     }
   }
@@ -1010,28 +1053,37 @@ __global__ void __launch_bounds__(256) k_pcg_spmv_z(long n, Sell S, const double
 
 // block PCG step B: x += alpha p; r -= alpha q; z = D_B^-1 r; r.z, r.r -> beta, convergence
 template <int NB>
-__global__ void k_pcg_vec_blk(long ne, const double *__restrict__ inv, const double *__restrict__ p,
-                              const double *__restrict__ q, double *__restrict__ x, double *__restrict__ r,
-                              double *__restrict__ z, double *part, unsigned *counter, DevState *st) {
+__global__ void __launch_bounds__(256) k_pcg_vec_blk(long ne, const double *__restrict__ inv,
+                                                     const double *__restrict__ p, const double *__restrict__ q,
+                                                     double *__restrict__ x, double *__restrict__ r,
+                                                     double *__restrict__ z, double *part, unsigned *counter,
+                                                     DevState *st) {
+  __shared__ double sinv[BlkTile<NB>::TE * NB * NB];
+  __shared__ double sv[BlkTile<NB>::ROWS];
   __shared__ double sh[64];
+  constexpr int TE = BlkTile<NB>::TE;
   if (!st->p.active) return;
   const double alpha = st->p.alpha;
   double v[2] = {0.0, 0.0};
-  for (long e = (long)blockIdx.x * blockDim.x + threadIdx.x; e < ne; e += (long)gridDim.x * blockDim.x) {
-    double rv[NB], t[NB];
-#pragma unroll
-    for (int i = 0; i < NB; ++i) {
-      const long k = e * NB + i;
+  for (long e0 = (long)blockIdx.x * TE; e0 < ne; e0 += (long)gridDim.x * TE) {
+    const int te = (int)min((long)TE, ne - e0);
+    const int t = threadIdx.x;
+    const long k = e0 * NB + t;
+    __syncthreads();
+    for (int qq = threadIdx.x; qq < te * NB * NB; qq += blockDim.x) sinv[qq] = inv[e0 * NB * NB + qq];
+    double rk = 0.0;
+    if (t < te * NB) {
       x[k] = fma(alpha, p[k], x[k]);
-      rv[i] = fma(-alpha, q[k], r[k]);
-      r[k] = rv[i];
+      rk = fma(-alpha, q[k], r[k]);
+      r[k] = rk;
+      sv[t] = rk;
     }
-    block_mv<NB>(inv, e, rv, t);
-#pragma unroll
-    for (int i = 0; i < NB; ++i) {
-      z[e * NB + i] = t[i];
-      v[0] += rv[i] * t[i];
-      v[1] += rv[i] * rv[i];
+    __syncthreads();
+    if (t < te * NB) {
+      const double tv = row_blk<NB>(sinv, sv, t);
+      z[k] = tv;
+      v[0] += rk * tv;
+      v[1] += rk * rk;
     }
   }
   block_sum_n<2>(v, sh);

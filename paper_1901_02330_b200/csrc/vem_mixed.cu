@@ -346,6 +346,13 @@ double bytes_cheb(Ctx *c) { return 12.0 * c->nnzS + 56.0 * c->np; }
 double bytes_pcg_vec(Ctx *c) { return 64.0 * c->np; }
 double bytes_vecs(Ctx *c, double nvec) { return 8.0 * c->n * nvec; }
 
+// blocks for the tiled element-block kernels (a few waves over the tiles)
+template <int NB>
+int grid_blk(Ctx *c, long ne) {
+  const long tiles = (ne + BlkTile<NB>::TE - 1) / BlkTile<NB>::TE;
+  return (int)std::max<long>(1, std::min<long>(tiles, (long)c->sm_count * 16));
+}
+
 template <int NB>
 void BlkInvL<NB>::run(Ctx *c, double shift, double *out) {
   const long ne = c->np / NB;
@@ -356,20 +363,20 @@ template <int NB>
 void ChebBlkL<NB>::run(Ctx *c, const double *dold, double *dnew, double c1, double c2, int mode, int last, double *zp,
                        const int *gate) {
   const long ne = c->np / NB;
-  k_cheb_block<NB><<<grid_stream(c, ne), 128, 0, c->stream>>>(ne, c->dBinv, c->cr, dold, dnew, c->cx, c1, c2, mode,
+  k_cheb_block<NB><<<grid_blk<NB>(c, ne), 256, 0, c->stream>>>(ne, c->dBinv, c->cr, dold, dnew, c->cx, c1, c2, mode,
                                                               last, zp, gate);
 }
 template <int NB>
 void PcgInitBlkL<NB>::run(Ctx *c, const int *gate) {
   const long ne = c->np / NB;
-  k_pcg_init_blk<NB><<<grid_stream(c, ne), NT, 0, c->stream>>>(ne, c->dBeinv, c->pb, c->px, c->pr, c->pz, c->pp0,
+  k_pcg_init_blk<NB><<<grid_blk<NB>(c, ne), 256, 0, c->stream>>>(ne, c->dBeinv, c->pb, c->px, c->pr, c->pz, c->pp0,
                                                                c->part, c->counter, c->st, c->opts.inner_rtol,
                                                                c->opts.inner_maxit, gate);
 }
 template <int NB>
 void PcgVecBlkL<NB>::run(Ctx *c, const double *p) {
   const long ne = c->np / NB;
-  k_pcg_vec_blk<NB><<<grid_stream(c, ne), NT, 0, c->stream>>>(ne, c->dBeinv, p, c->pq, c->px, c->pr, c->pz, c->part,
+  k_pcg_vec_blk<NB><<<grid_blk<NB>(c, ne), 256, 0, c->stream>>>(ne, c->dBeinv, p, c->pq, c->px, c->pr, c->pz, c->part,
                                                               c->counter, c->st);
 }
 
