@@ -986,7 +986,7 @@ __global__ void __launch_bounds__(256) k_pcg_init_blk(long ne, const double *__r
         x[k] = 0.0;
         r[k] = bk;
         z[k] = tv;
-        p0[k] = 0.0;
+        p0[k] = tv;     // p_0 = z_0 (the block path materialises p, see k_pcg_pupd)
         v[0] += bk * tv;
         v[1] += bk * bk;
       }
@@ -1015,27 +1015,18 @@ __global__ void __launch_bounds__(256) k_pcg_init_blk(long ne, const double *__r
   }
 }
 
-// block PCG step A: p_new = z + beta p_prev (gathered), q = (S + eps W) p_new, p.q -> alpha
-struct GatherPz {
-  double beta;
-  const double *__restrict__ p_prev, *__restrict__ z;
-  __device__ __forceinline__ double operator()(int c) const { return fma(beta, p_prev[c], z[c]); }
-};
-__global__ void __launch_bounds__(256) k_pcg_spmv_z(long n, Sell S, const double *__restrict__ wdiag, double eps,
-                                                    const double *__restrict__ z, const double *__restrict__ p_prev,
-                                                    double *__restrict__ p_new, double *__restrict__ q, double *part,
-                                                    unsigned *counter, DevState *st) {
+// block PCG step A (single gather): q = (S + eps W) p, p.q -> alpha
+__global__ void __launch_bounds__(256) k_pcg_spmv_p(long n, Sell S, const double *__restrict__ wdiag, double eps,
+                                                    const double *__restrict__ p, double *__restrict__ q,
+                                                    double *part, unsigned *counter, DevState *st) {
   __shared__ double sh[32];
   if (!st->p.active) return;
-  const double beta = st->p.beta;
   const long row = (long)blockIdx.x * blockDim.x + threadIdx.x;
   double v[1] = {0.0};
   if (row < n) {
-    const double acc = sell_dot(S, row, GatherPz{beta, p_prev, z});
-    const double pi = fma(beta, p_prev[row], z[row]);
+    const double pi = p[row];
     const double w = wdiag ? wdiag[row] : 1.0;
-    const double qi = fma(eps * w, pi, acc);
-    p_new[row] = pi;
+    const double qi = fma(eps * w, pi, sell_dot(S, row, GatherX{p}));
     q[row] = qi;
     v[0] = pi * qi;
   }
@@ -1049,6 +1040,13 @@ __global__ void __launch_bounds__(256) k_pcg_spmv_z(long n, Sell S, const double
       *counter = 0u;
     }
   }
+}
+// block PCG step C: p = z + beta p (after step B decided beta; skipped once converged)
+__global__ void k_pcg_pupd(long n, const double *__restrict__ z, double *__restrict__ p, DevState *st) {
+  if (!st->p.active) return;
+  const double beta = st->p.beta;
+  for (long i = (long)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (long)gridDim.x * blockDim.x)
+    p[i] = fma(beta, p[i], z[i]);
 }
 
 // block PCG step B: x += alpha p; r -= alpha q; z = D_B^-1 r; r.z, r.r -> beta, convergence

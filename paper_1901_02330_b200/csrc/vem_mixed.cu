@@ -335,10 +335,6 @@ void launch_pcg_spmv(Ctx *c, const double *pprev, double *pnew) {
 void launch_cheb_resid(Ctx *c, const double *dold, const int *gate) {
   k_cheb_resid<<<grid_for(c->np), NT, 0, c->stream>>>(c->np, sellS(c), c->cr, dold, gate);
 }
-void launch_pcg_spmv_z(Ctx *c, const double *pprev, double *pnew) {
-  k_pcg_spmv_z<<<grid_for(c->np), NT, 0, c->stream>>>(c->np, sellS(c), c->wdiag, c->eps, c->pz, pprev, pnew, c->pq,
-                                                      c->part, c->counter, c->st);
-}
 
 // algorithmic bytes per launch (include/vem_mixed.h)
 double bytes_spmv(Ctx *c) { return 12.0 * c->nnzA + 16.0 * c->n; }
@@ -515,12 +511,18 @@ int enqueue_pcg_steps(Ctx *c, int nsteps) {
     double *pprev = (s % 2 == 0) ? c->pp0 : c->pp1;
     double *pnew = (s % 2 == 0) ? c->pp1 : c->pp0;
     if (c->nb > 1) {
+      // block path: p materialised, q = S p with one gather, then p = z + beta p
       {
-        TimeScope ts(c, VEM_K_PCG_SPMV, bytes_cheb(c));
-        launch_pcg_spmv_z(c, (const double *)pprev, pnew);
+        TimeScope ts(c, VEM_K_PCG_SPMV, 12.0 * c->nnzS + 32.0 * c->np);
+        k_pcg_spmv_p<<<grid_for(c->np), NT, 0, c->stream>>>(c->np, sellS(c), c->wdiag, c->eps, c->pp0, c->pq,
+                                                           c->part, c->counter, c->st);
       }
-      TimeScope ts(c, VEM_K_PCG_VEC, bytes_pcg_vec(c) + 8.0 * c->np * c->nb);
-      dispatch_nb<PcgVecBlkL>(c->nb, c, (const double *)pnew);
+      {
+        TimeScope ts(c, VEM_K_PCG_VEC, bytes_pcg_vec(c) + 8.0 * c->np * c->nb);
+        dispatch_nb<PcgVecBlkL>(c->nb, c, (const double *)c->pp0);
+      }
+      TimeScope ts(c, VEM_K_PCG_VEC, 24.0 * c->np);
+      k_pcg_pupd<<<grid_stream(c, c->np), NT, 0, c->stream>>>(c->np, c->pz, c->pp0, c->st);
     } else {
       {
         TimeScope ts(c, VEM_K_PCG_SPMV, bytes_cheb(c));
