@@ -535,7 +535,6 @@ __global__ void __launch_bounds__(256) k_mdot(long n, const double *__restrict__
   }
 }
 
-#define VEM_TILE 128
 
 // Givens step for column j, executed by one thread.
 __device__ void givens_column(DevState *st, int j, double hn) {
@@ -1113,8 +1112,4 @@ __global__ void __launch_bounds__(256) k_pcg_vec_blk(long ne, const double *__re
 __global__ void k_widen(long n, const int64_t *__restrict__ in, int *__restrict__ out) {
   for (long i = (long)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (long)gridDim.x * blockDim.x)
     out[i] = (int)in[i];
-}
-__global__ void k_i32_to_i64(long n, const int *__restrict__ in, int64_t *__restrict__ out) {
-  for (long i = (long)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (long)gridDim.x * blockDim.x)
-    out[i] = in[i];
 }

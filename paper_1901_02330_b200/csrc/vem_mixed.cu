@@ -66,7 +66,6 @@ struct Ctx {
   int sm_count = 148;
   double eps = 0.0;
   bool has_reg = false;
-  int gA = 4, gS = 4;
   int nb = 1;                          // pressure DOFs per element (block-Jacobi size)
   double lmax = 0.0;                   // Gershgorin bound of diag(S)^-1 S (reported)
   double lmax_cheb = 2.0;              // Chebyshev interval top: lambda_max(D_B^-1 S_D) <= 2 (R15)
@@ -180,13 +179,6 @@ inline int grid_stream(Ctx *c, long n) {   // grid-stride kernels: a few waves o
   long g = (n + NT - 1) / NT;
   return (int)std::max<long>(1, std::min<long>(g, (long)c->sm_count * 32));
 }
-int pick_group(double avg) {
-  if (avg < 3) return 2;
-  if (avg < 6) return 4;
-  if (avg < 12) return 8;
-  if (avg < 24) return 16;
-  return 32;
-}
 
 // ----------------------------------------------------------------------------
 // timing: events around each launch when opts.timing (never inside a capture)
@@ -263,16 +255,6 @@ void flush_timing(Ctx *c) {   // call after a stream sync
 // ----------------------------------------------------------------------------
 // launch helpers (templated on the CSR lanes-per-row)
 // ----------------------------------------------------------------------------
-template <template <int> class F, typename... Args>
-void dispatch_g(int g, Args... a) {
-  switch (g) {
-    case 2: F<2>::run(a...); break;
-    case 4: F<4>::run(a...); break;
-    case 8: F<8>::run(a...); break;
-    case 16: F<16>::run(a...); break;
-    default: F<32>::run(a...); break;
-  }
-}
 
 template <template <int> class F, typename... Args>
 bool dispatch_nb(int nb, Args... a) {
@@ -1429,7 +1411,7 @@ int upload_impl(Ctx *c, const vem_csr *M, const vem_csr *B, const vem_csr *W, do
       if (W->indptr[i + 1] - W->indptr[i] != 1 || W->indices[W->indptr[i]] != i || !(W->values[W->indptr[i]] > 0))
         return fail(c, VEM_ERR_INVALID, "W must be diagonal with positive entries");
   }
-  c->ldv = (c->n + VEM_TILE - 1) / VEM_TILE * VEM_TILE;   // tiles of the CGS passes never leave a vector
+  c->ldv = (c->n + 127) / 128 * 128;   // 1 KB-aligned basis vectors
   cudaDeviceProp prop;
   int dev = 0;
   CK(cudaGetDevice(&dev));
@@ -1584,8 +1566,6 @@ int upload_impl(Ctx *c, const vem_csr *M, const vem_csr *B, const vem_csr *W, do
     DA(c->pq, c->np);
     DA(c->pb, c->np);
   }
-  c->gA = pick_group((double)c->nnzA / c->n);
-  c->gS = pick_group((double)c->nnzS / c->np);
   {
     int rr = build_sell(c, c->n, c->a_rp, c->a_ci, c->a_va, &c->a_soff, &c->a_sci, &c->a_sva, &c->nnzA_sell);
     if (rr) return rr;
@@ -1821,8 +1801,8 @@ int vem_mixed_get_info(vem_ctx *h, vem_info *info) {
   info->nnz_S = c->nnzS;
   info->lambda_max = c->lmax;
   info->eps = c->eps;
-  info->spmv_group = c->gA;
-  info->schur_group = c->gS;
+  info->spmv_group = 1;      // SELL-32: one row per thread
+  info->schur_group = 1;
   info->sm_count = c->sm_count;
   info->device_bytes = c->device_bytes;
   info->l2_window_bytes = (int64_t)c->l2_window_bytes;
