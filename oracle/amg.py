@@ -19,7 +19,7 @@ Definition (the GPU follows it step by step):
     the rest become singletons in index order
   * P piecewise constant, A_c = P^T A P; stop when n <= COARSE_SIZE, at
     MAX_LEVELS, or when a level coarsens by less than 1/0.75
-  * coarsest level (COARSE_SIZE = 1024): dense inverse applied as a matvec, else
+  * coarsest level (COARSE_SIZE = 2048): dense inverse applied as a matvec, else
     (stagnated coarsening) a degree-COARSE_DEGREE Chebyshev smoother
   * smoother C_l(b): degree-DEGREE point-Jacobi Chebyshev from x0 = 0 (Saad
     Alg. 12.1, exactly oracle.solver.chebyshev) on [lmax/RATIO, lmax] with the
@@ -39,7 +39,7 @@ import scipy.sparse as sp
 from .solver import chebyshev
 
 THETA = 0.08
-COARSE_SIZE = 1024
+COARSE_SIZE = 2048
 MAX_LEVELS = 12
 DEGREE = 3
 RATIO = 30.0

@@ -193,16 +193,17 @@ __global__ void k_amg_gauss_jordan(long n, double *__restrict__ D, double *__res
 // V-cycle kernels (all gated)
 // ---------------------------------------------------------------------------
 // Chebyshev smoother init from x0 = 0: r = b, d = D^-1 b / theta, x = d
+// acc = 1: x += C(b) (post-smoothing on the residual equation accumulates into x)
 __global__ void k_amg_cheb_init(long n, const double *__restrict__ dinv, const double *__restrict__ b,
                                 double inv_theta, double *__restrict__ r, double *__restrict__ d,
-                                double *__restrict__ x, const int *gate) {
+                                double *__restrict__ x, int acc, const int *gate) {
   if (!*gate) return;
   for (long i = (long)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (long)gridDim.x * blockDim.x) {
     const double bi = b[i];
     const double di = dinv[i] * bi * inv_theta;
     r[i] = bi;
     d[i] = di;
-    x[i] = di;
+    x[i] = acc ? x[i] + di : di;
   }
 }
 // r -= A d_old; d_new = c1 d_old + c2 D^-1 r; x += d_new   (x_out may alias x)
@@ -306,7 +307,7 @@ struct GatherD0b {
 __global__ void __launch_bounds__(256) k_amg_cheb_first(long n, Sell A, const double *__restrict__ dinv,
                                                         const double *__restrict__ b, double inv_theta, double c1,
                                                         double c2, double *__restrict__ r, double *__restrict__ d_new,
-                                                        double *__restrict__ x, const int *gate) {
+                                                        double *__restrict__ x, int acc, const int *gate) {
   if (!*gate) return;
   const long i = (long)blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= n) return;
@@ -317,7 +318,35 @@ __global__ void __launch_bounds__(256) k_amg_cheb_first(long n, Sell A, const do
   const double dn = c1 * d0 + c2 * (dinv[i] * rn);
   r[i] = rn;
   d_new[i] = dn;
-  x[i] = d0 + dn;
+  x[i] = acc ? x[i] + (d0 + dn) : d0 + dn;
+}
+
+// warp-per-row version of the fused first smoother step (small coarse levels)
+__global__ void __launch_bounds__(256) k_amg_cheb_first_w(long n, const int *__restrict__ rp,
+                                                          const int *__restrict__ ci, const double *__restrict__ va,
+                                                          const double *__restrict__ dinv, const double *__restrict__ b,
+                                                          double inv_theta, double c1, double c2,
+                                                          double *__restrict__ r, double *__restrict__ d_new,
+                                                          double *__restrict__ x, int acc, const int *gate) {
+  if (!*gate) return;
+  const long i = ((long)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  if (i >= n) return;
+  const int lane = threadIdx.x & 31;
+  double acc_d = 0.0;
+  for (int k = rp[i] + lane; k < rp[i + 1]; k += 32) {
+    const int c = ci[k];
+    acc_d = fma(va[k], dinv[c] * b[c] * inv_theta, acc_d);
+  }
+  acc_d = warp_sum(acc_d);
+  if (lane == 0) {
+    const double bi = b[i];
+    const double d0 = dinv[i] * bi * inv_theta;
+    const double rn = bi - acc_d;
+    const double dn = c1 * d0 + c2 * (dinv[i] * rn);
+    r[i] = rn;
+    d_new[i] = dn;
+    x[i] = acc ? x[i] + (d0 + dn) : d0 + dn;
+  }
 }
 // Block-Schur-AMG top: z_u = s v_u ./ diag(M), b0 = s v_p
 __global__ void k_amg_top(long nu, long np, const double *__restrict__ v, const double *scale,

@@ -563,7 +563,7 @@ int run_pcg(Ctx *c, int64_t *inner_its) {
 // (oracle/amg.py AMG.vcycle, reading R22)
 // ----------------------------------------------------------------------------
 constexpr double AMG_THETA = 0.08, AMG_RATIO = 30.0, AMG_STAGNATION = 0.75;
-constexpr int AMG_COARSE_SIZE = 1024, AMG_MAX_LEVELS = 12, AMG_DEGREE = 3, AMG_COARSE_DEGREE = 8;
+constexpr int AMG_COARSE_SIZE = 2048, AMG_MAX_LEVELS = 12, AMG_DEGREE = 3, AMG_COARSE_DEGREE = 8;
 
 void amg_cheb_coeffs(double lmax, int degree, double &inv_theta, std::vector<double> &c1, std::vector<double> &c2) {
   const double b = lmax, a = lmax / AMG_RATIO;
@@ -583,43 +583,42 @@ void amg_cheb_coeffs(double lmax, int degree, double &inv_theta, std::vector<dou
 // out = C_degree(b) on level L (x0 = 0); `sample`: bracket the second step with the
 // sampled-timing events (fine-level pre-smoothing, timing = 2)
 void amg_smooth(Ctx *c, AmgLevel &L, const double *b, double *out, int degree, const int *gate,
-                bool sample = false) {
+                bool sample = false, int acc = 0) {
   double it;
   std::vector<double> c1, c2;
   amg_cheb_coeffs(L.lmax, degree, it, c1, c2);
   const Sell A{L.soff, L.sci, L.sva};
-  if (!L.warp_rows && degree > 1) {   // init fused into the first step
+  double *dold = L.sd0, *dnew = L.sd1;
+  int first = 1;
+  if (degree > 1) {   // init fused into the first step
     TimeScope ts(c, VEM_K_CHEB, 12.0 * L.nnz + 48.0 * L.n);
-    k_amg_cheb_first<<<grid_for(L.n), NT, 0, c->stream>>>(L.n, A, L.dinv, b, it, c1[0], c2[0], L.sr, L.sd1, out,
-                                                          gate);
-    double *dold = L.sd1, *dnew = L.sd0;
-    for (int i = 2; i < degree; ++i) {
-      const bool smp = sample && i == 2 && c->opts.timing == 2 && c->sample_slot >= 0;
-      if (smp) cudaEventRecordWithFlags(c->samp_a[c->sample_slot], c->stream, cudaEventRecordExternal);
-      c->sample_recorded |= smp;
-      {
-        TimeScope ts2(c, VEM_K_CHEB, 12.0 * L.nnz + 56.0 * L.n);
+    if (L.warp_rows)
+      k_amg_cheb_first_w<<<grid_for(L.n * 32), NT, 0, c->stream>>>(L.n, L.rp, L.ci, L.va, L.dinv, b, it, c1[0],
+                                                                    c2[0], L.sr, L.sd1, out, acc, gate);
+    else
+      k_amg_cheb_first<<<grid_for(L.n), NT, 0, c->stream>>>(L.n, A, L.dinv, b, it, c1[0], c2[0], L.sr, L.sd1, out,
+                                                            acc, gate);
+    dold = L.sd1;
+    dnew = L.sd0;
+    first = 2;
+  } else {
+    TimeScope ts(c, VEM_K_PRECOND_VEC, 40.0 * L.n);
+    k_amg_cheb_init<<<grid_stream(c, L.n), NT, 0, c->stream>>>(L.n, L.dinv, b, it, L.sr, L.sd0, out, acc, gate);
+  }
+  for (int i = first; i < degree; ++i) {
+    const bool smp = sample && i == 2 && c->opts.timing == 2 && c->sample_slot >= 0 && !L.warp_rows;
+    if (smp) cudaEventRecordWithFlags(c->samp_a[c->sample_slot], c->stream, cudaEventRecordExternal);
+    c->sample_recorded |= smp;
+    {
+      TimeScope ts(c, VEM_K_CHEB, 12.0 * L.nnz + 56.0 * L.n);
+      if (L.warp_rows)
+        k_amg_cheb_step_w<<<grid_for(L.n * 32), NT, 0, c->stream>>>(L.n, L.rp, L.ci, L.va, L.dinv, L.sr, dold, dnew,
+                                                                     out, c1[i - 1], c2[i - 1], gate);
+      else
         k_amg_cheb_step<<<grid_for(L.n), NT, 0, c->stream>>>(L.n, A, L.dinv, L.sr, dold, dnew, out, c1[i - 1],
                                                              c2[i - 1], gate);
-      }
-      if (smp) cudaEventRecordWithFlags(c->samp_b[c->sample_slot], c->stream, cudaEventRecordExternal);
-      std::swap(dold, dnew);
     }
-    return;
-  }
-  {
-    TimeScope ts(c, VEM_K_PRECOND_VEC, 40.0 * L.n);
-    k_amg_cheb_init<<<grid_stream(c, L.n), NT, 0, c->stream>>>(L.n, L.dinv, b, it, L.sr, L.sd0, out, gate);
-  }
-  double *dold = L.sd0, *dnew = L.sd1;
-  for (int i = 1; i < degree; ++i) {
-    TimeScope ts(c, VEM_K_CHEB, 12.0 * L.nnz + 56.0 * L.n);
-    if (L.warp_rows)
-      k_amg_cheb_step_w<<<grid_for(L.n * 32), NT, 0, c->stream>>>(L.n, L.rp, L.ci, L.va, L.dinv, L.sr, dold, dnew,
-                                                                   out, c1[i - 1], c2[i - 1], gate);
-    else
-      k_amg_cheb_step<<<grid_for(L.n), NT, 0, c->stream>>>(L.n, A, L.dinv, L.sr, dold, dnew, out, c1[i - 1],
-                                                           c2[i - 1], gate);
+    if (smp) cudaEventRecordWithFlags(c->samp_b[c->sample_slot], c->stream, cudaEventRecordExternal);
     std::swap(dold, dnew);
   }
 }
@@ -659,11 +658,7 @@ void amg_vcycle(Ctx *c, size_t l, const int *gate) {
     k_amg_prolong_add<<<grid_stream(c, L.n), NT, 0, c->stream>>>(L.n, L.agg, C.x, L.x, gate);
   }
   amg_residual(c, L, gate);
-  amg_smooth(c, L, L.t, L.y, AMG_DEGREE, gate);
-  if (l > 0) {   // level result x + y (the top level folds this into z_p = -(x + y))
-    TimeScope ts(c, VEM_K_PRECOND_VEC, 24.0 * L.n);
-    k_amg_add<<<grid_stream(c, L.n), NT, 0, c->stream>>>(L.n, L.x, L.y, 1.0, L.x, gate);
-  }
+  amg_smooth(c, L, L.t, L.x, AMG_DEGREE, gate, false, 1);   // x += C(b - A x)
 }
 
 int enqueue_block_schur_amg(Ctx *c, const double *v, const double *scale, double *z, const int *gate) {
@@ -676,8 +671,7 @@ int enqueue_block_schur_amg(Ctx *c, const double *v, const double *scale, double
   amg_vcycle(c, 0, gate);
   {
     TimeScope ts(c, VEM_K_PRECOND_VEC, 24.0 * c->np);
-    k_amg_add<<<grid_stream(c, c->np), NT, 0, c->stream>>>(c->np, L0.x, c->amg.size() == 1 ? nullptr : L0.y,
-                                                           -1.0, z + c->nu, gate);
+    k_amg_add<<<grid_stream(c, c->np), NT, 0, c->stream>>>(c->np, L0.x, nullptr, -1.0, z + c->nu, gate);
   }
   CKL();
   return 0;
@@ -1296,7 +1290,6 @@ int amg_level_vectors(Ctx *c, AmgLevel &L) {
   DA(L.b, L.n);
   DA(L.x, L.n);
   DA(L.t, L.n);
-  DA(L.y, L.n);
   DA(L.sr, L.n);
   DA(L.sd0, L.n);
   DA(L.sd1, L.n);
