@@ -1318,9 +1318,11 @@ int build_amg(Ctx *c) {
     dfree(c, F.sr);
     dfree(c, F.sd0);
     dfree(c, F.sd1);
+    dfree(c, F.x);
     F.sr = c->cr;
     F.sd0 = c->cd0;
     F.sd1 = c->cd1;
+    F.x = c->cx;
   }
   double *diag = c->sdiag;
   while (true) {
