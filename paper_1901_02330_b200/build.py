@@ -7,8 +7,8 @@ import sys
 
 HERE = os.path.dirname(os.path.abspath(__file__))
 SRC = os.path.join(HERE, "csrc", "vem_mixed.cu")
-DEPS = [SRC, os.path.join(HERE, "csrc", "kernels.cuh"),
-        os.path.join(os.path.dirname(HERE), "include", "vem_mixed.h")]
+DEPS = [os.path.join(HERE, "csrc", f) for f in sorted(os.listdir(os.path.join(HERE, "csrc")))] + [
+    os.path.join(os.path.dirname(HERE), "include", "vem_mixed.h")]
 LIB = os.path.join(HERE, "libvem_mixed.so")
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 FLAGS = ["-gencode", "arch=compute_100a,code=sm_100a", "-O3", "-lineinfo", "-std=c++17",

@@ -164,29 +164,36 @@ __global__ void k_amg_dense(long n, const int *__restrict__ rp, const int *__res
     for (int k = rp[i]; k < rp[i + 1]; ++k) row[ci[k]] = va[k];
   }
 }
-// Gauss-Jordan without pivoting (SPD), one block, one thread per row
-__global__ void k_amg_gauss_jordan(long n, double *__restrict__ D, double *__restrict__ inv, int *err) {
-  extern __shared__ double piv[];   // pivot row (2n)
-  for (long k = 0; k < n; ++k) {
-    __syncthreads();
-    const double p = D[k * 2 * n + k];
-    if (threadIdx.x == 0 && !(p > 0.0)) atomicExch(err, 1);
-    for (long j = threadIdx.x; j < 2 * n; j += blockDim.x) piv[j] = D[k * 2 * n + j] / p;
-    __syncthreads();
-    for (long i = threadIdx.x; i < n; i += blockDim.x) {
-      double *row = D + i * 2 * n;
-      if (i == k) {
-        for (long j = 0; j < 2 * n; ++j) row[j] = piv[j];
-      } else {
-        const double f = row[k];
-        if (f != 0.0)
-          for (long j = 0; j < 2 * n; ++j) row[j] = fma(-f, piv[j], row[j]);
-      }
-    }
+// Gauss-Jordan without pivoting (SPD) on the augmented [A | I] (n x 2n, row-major),
+// one pivot per launch pair: k_amg_gj_pivot copies the scaled pivot row and the
+// pivot column into side buffers, k_amg_gj_update eliminates every other row from
+// them (no reads of D that another thread writes in the same launch).
+__global__ void k_amg_gj_pivot(long n, long k, const double *__restrict__ D, double *__restrict__ piv,
+                               double *__restrict__ col, int *err) {
+  const double p = D[k * 2 * n + k];
+  const long i = (long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i == 0 && !(p > 0.0)) atomicExch(err, 1);
+  if (i < 2 * n) piv[i] = D[k * 2 * n + i] / p;
+  if (i < n) col[i] = D[i * 2 * n + k];
+}
+__global__ void k_amg_gj_update(long n, long k, double *__restrict__ D, const double *__restrict__ piv,
+                                const double *__restrict__ col) {
+  const long i = blockIdx.y;
+  // columns < k of the left half are already eliminated and columns > n + k of the
+  // right half are still zero in every row: only [k, n + k] changes
+  const long j = k + (long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (j > n + k) return;
+  double *row = D + i * 2 * n;
+  if (i == k)
+    row[j] = piv[j];
+  else
+    row[j] = fma(-col[i], piv[j], row[j]);
+}
+__global__ void k_amg_gj_extract(long n, const double *__restrict__ D, double *__restrict__ inv) {
+  for (long t = (long)blockIdx.x * blockDim.x + threadIdx.x; t < n * n; t += (long)gridDim.x * blockDim.x) {
+    const long i = t / n, j = t % n;
+    inv[t] = D[i * 2 * n + n + j];
   }
-  __syncthreads();
-  for (long i = threadIdx.x; i < n; i += blockDim.x)
-    for (long j = 0; j < n; ++j) inv[i * n + j] = D[i * 2 * n + n + j];
 }
 
 // ---------------------------------------------------------------------------

@@ -18,6 +18,7 @@
 #include <cmath>
 #include <cstdarg>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <string>
 #include <vector>
@@ -1366,9 +1367,23 @@ int build_amg(Ctx *c) {
     DA(D, (size_t)Lc.n * 2 * Lc.n);
     DA(c->amg_cinv, (size_t)Lc.n * Lc.n);
     k_amg_dense<<<grid_stream(c, Lc.n), NT, 0, c->stream>>>(Lc.n, Lc.rp, Lc.ci, Lc.va, D);
-    const int th = (int)std::min<long>(1024, std::max<long>(32, (Lc.n + 31) / 32 * 32));
-    k_amg_gauss_jordan<<<1, th, 2 * Lc.n * sizeof(double), c->stream>>>(Lc.n, D, c->amg_cinv, c->derr);
+    auto tg = std::chrono::steady_clock::now();
+    double *piv = nullptr, *col = nullptr;
+    DA(piv, 2 * Lc.n);
+    DA(col, Lc.n);
+    const long n = Lc.n;
+    for (long k = 0; k < n; ++k) {
+      k_amg_gj_pivot<<<(unsigned)((2 * n + NT - 1) / NT), NT, 0, c->stream>>>(n, k, D, piv, col, c->derr);
+      k_amg_gj_update<<<dim3((unsigned)((n + 1 + NT - 1) / NT), (unsigned)n), NT, 0, c->stream>>>(n, k, D, piv, col);
+    }
+    k_amg_gj_extract<<<grid_stream(c, n * n), NT, 0, c->stream>>>(n, D, c->amg_cinv);
     CKL();
+    CK(cudaStreamSynchronize(c->stream));
+    dfree(c, piv);
+    dfree(c, col);
+    if (getenv("VEM_SETUP_TRACE"))
+      fprintf(stderr, "[vem setup] coarsest Gauss-Jordan n=%ld %9.1f ms\n", n,
+              std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - tg).count());
     CK(cudaStreamSynchronize(c->stream));
     dfree(c, D);
     if (read_back(c, c->derr)) return fail(c, VEM_ERR_DIAG_S, "coarsest S_D level not positive definite");
@@ -1379,6 +1394,13 @@ int build_amg(Ctx *c) {
 
 int upload_impl(Ctx *c, const vem_csr *M, const vem_csr *B, const vem_csr *W, double eps, const vem_layout *lay) {
   auto t0 = std::chrono::steady_clock::now();
+  const bool trace = getenv("VEM_SETUP_TRACE") != nullptr;
+  auto phase = [&](const char *what) {
+    if (!trace) return;
+    cudaStreamSynchronize(c->stream);
+    fprintf(stderr, "[vem setup] %-28s %9.1f ms\n", what,
+            std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count());
+  };
   if (!M || !B) return fail(c, VEM_ERR_INVALID, "M and B are required");
   c->nu = M->n_rows;
   c->np = B->n_rows;
@@ -1429,6 +1451,7 @@ int upload_impl(Ctx *c, const vem_csr *M, const vem_csr *B, const vem_csr *W, do
     if ((r = upload_array(c, &c->wdiag, wd.data(), c->np))) return r;
     CK(cudaStreamSynchronize(c->stream));
   }
+  phase("validate + upload");
   // B^T (CSR over velocity rows), deterministic order
   int *btrp = nullptr, *btci = nullptr, *fill = nullptr;
   double *btva = nullptr;
@@ -1500,9 +1523,11 @@ int upload_impl(Ctx *c, const vem_csr *M, const vem_csr *B, const vem_csr *W, do
   CK(cudaMemcpyAsync(&herr, c->derr, sizeof(int), cudaMemcpyDeviceToHost, c->stream));
   CK(cudaStreamSynchronize(c->stream));
   if (herr) return fail(c, VEM_ERR_DIAG_M, "non-positive diagonal entry in M");
+  phase("merged A, diag(M)");
   // S_D
   r = build_schur(c, brp, bci, bva, btrp, btci, btva);
   if (r) return r;
+  phase("S_D spgemm");
   {  // Chebyshev working set in one contiguous pool: D^-1, r, d0, d1, x (L2-persisting window)
     const long npad = (c->np + 31) / 32 * 32;
     DA(c->cheb_pool, 5 * npad);
@@ -1568,10 +1593,12 @@ int upload_impl(Ctx *c, const vem_csr *M, const vem_csr *B, const vem_csr *W, do
     if (rr) return rr;
   }
   CK(cudaStreamSynchronize(c->stream));
+  phase("block inverses, SELL");
   if (c->nb == 1) {   // S_D hierarchy for precond kind 3 (k = 0)
     int rr = build_amg(c);
     if (rr) return rr;
   }
+  phase("AMG hierarchy");
   {
     int rr = apply_l2_window(c);
     if (rr) return rr;
@@ -1586,6 +1613,7 @@ int upload_impl(Ctx *c, const vem_csr *M, const vem_csr *B, const vem_csr *W, do
                   (void *)btci, (void *)btva, (void *)fill, (void *)brp32, (void *)len})
     dfree(c, p);
   c->setup_ms = std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count();
+  phase("done");
   return 0;
 }
 
