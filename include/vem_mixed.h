@@ -86,6 +86,11 @@ typedef struct {
   int32_t reorth;         /* -1 auto (default): CGS1 for GMRES (Block-Schur / none), CGS2
                              for FGMRES (Block-Reg); 1: CGS2 always; 0: CGS1 always        */
   int32_t l2_persist;     /* 1 (default): persisting L2 window over the Chebyshev vectors  */
+  int32_t reorder;        /* 1 (default): SELL-C-sigma symmetric reordering of the unknowns
+                             at upload when n_p_dof > 1 and it removes >= 5% slice padding
+                             (rows sorted by length in 4096-row windows, element blocks
+                             kept whole); invisible to the caller (rhs, u, p and every
+                             operator entry point stay in the caller's numbering); 0: off */
 } vem_opts;
 
 typedef struct {
@@ -112,6 +117,9 @@ typedef struct {
   int64_t l2_window_bytes;        /* bytes under the persisting L2 access window          */
   int32_t amg_levels;             /* levels of the S_D hierarchy (0: kind 3 unavailable)   */
   int64_t amg_coarsest;           /* rows of its coarsest level                            */
+  int32_t reordered;              /* 1 if the SELL-C-sigma reordering is active            */
+  int32_t pad3;
+  int64_t nnz_A_stored, nnz_S_stored; /* stored SELL-32 slots (nonzeros + slice padding)   */
 } vem_info;
 
 /* Kernel classes for the per-launch CUDA-event statistics (opts.timing = 1). */

@@ -41,7 +41,7 @@ class vem_opts(C.Structure):
     _fields_ = [("restart", C.c_int32), ("cheb_degree", C.c_int32), ("cheb_ratio", C.c_double),
                 ("inner_rtol", C.c_double), ("inner_maxit", C.c_int32), ("use_graphs", C.c_int32),
                 ("timing", C.c_int32), ("pcg_chunk", C.c_int32), ("reorth", C.c_int32),
-                ("l2_persist", C.c_int32)]
+                ("l2_persist", C.c_int32), ("reorder", C.c_int32)]
 
 
 class vem_solve_report(C.Structure):
@@ -59,7 +59,8 @@ class vem_info(C.Structure):
                 ("nnz_A", C.c_int64), ("nnz_S", C.c_int64), ("lambda_max", C.c_double),
                 ("eps", C.c_double), ("spmv_group", C.c_int32), ("schur_group", C.c_int32),
                 ("sm_count", C.c_int32), ("device_bytes", C.c_int64), ("l2_window_bytes", C.c_int64),
-                ("amg_levels", C.c_int32), ("amg_coarsest", C.c_int64)]
+                ("amg_levels", C.c_int32), ("amg_coarsest", C.c_int64), ("reordered", C.c_int32),
+                ("pad3", C.c_int32), ("nnz_A_stored", C.c_int64), ("nnz_S_stored", C.c_int64)]
 
     def as_dict(self):
         return {f: getattr(self, f) for f, _ in self._fields_}

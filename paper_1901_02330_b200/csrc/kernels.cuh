@@ -129,7 +129,10 @@ struct Sell {
   const long long *__restrict__ soff;
   const int *__restrict__ ci;
   const double *__restrict__ va;
+  const int *__restrict__ perm;   // slot -> row (rows sorted by length in windows); nullptr: identity.
+                                  // Only S_D at k >= 1 carries one (k_spmv, k_cheb_resid, k_pcg_spmv_p).
 };
+__device__ __forceinline__ long sell_row(const Sell &A, long slot) { return A.perm ? (long)A.perm[slot] : slot; }
 
 template <typename Gather>
 __device__ __forceinline__ double sell_dot(const Sell &A, long row, Gather g) {
@@ -157,8 +160,9 @@ __global__ void __launch_bounds__(256) k_spmv(long row0, long nrows, Sell A, con
   if (!*gate) return;
   const long t = (long)blockIdx.x * blockDim.x + threadIdx.x;
   if (t >= nrows) return;
-  const long row = row0 + t;
-  const double acc = sell_dot(A, row, GatherX{x});
+  const long slot = row0 + t;
+  const long row = sell_row(A, slot);
+  const double acc = sell_dot(A, slot, GatherX{x});
   y[row] = mode ? b[row] - acc : acc;
 }
 
@@ -204,30 +208,60 @@ __global__ void __launch_bounds__(256) k_residual_start(long n, Sell A, const do
 }
 
 // CSR -> SELL-32 conversion (upload only)
-__global__ void k_sell_width(long nrows, const int *__restrict__ rp, long long *__restrict__ wslice) {
+// SELL-C-sigma (C = 32): slot r of the stored matrix holds CSR row perm[r]
+// (perm == nullptr: identity) with its columns renumbered through cmap
+// (cmap == nullptr: unchanged), so a symmetric reordering that sorts rows by
+// length inside sigma-row windows (upload_impl) removes the slice padding.
+__global__ void k_sell_width(long nrows, const int *__restrict__ rp, const int *__restrict__ perm,
+                             long long *__restrict__ wslice) {
   const long nsl = (nrows + 31) / 32;
   for (long s = (long)blockIdx.x * blockDim.x + threadIdx.x; s < nsl; s += (long)gridDim.x * blockDim.x) {
     int w = 0;
-    for (long r = s * 32; r < s * 32 + 32 && r < nrows; ++r) w = max(w, rp[r + 1] - rp[r]);
+    for (long r = s * 32; r < s * 32 + 32 && r < nrows; ++r) {
+      const long o = perm ? perm[r] : r;
+      w = max(w, rp[o + 1] - rp[o]);
+    }
     wslice[s] = 32LL * w;
   }
 }
 __global__ void k_sell_fill(long nrows, const int *__restrict__ rp, const int *__restrict__ ci,
-                            const double *__restrict__ va, const long long *__restrict__ soff, int *__restrict__ sci,
-                            double *__restrict__ sva) {
+                            const double *__restrict__ va, const int *__restrict__ perm,
+                            const int *__restrict__ cmap, const long long *__restrict__ soff,
+                            int *__restrict__ sci, double *__restrict__ sva) {
   const long nsl = (nrows + 31) / 32;
   for (long r = (long)blockIdx.x * blockDim.x + threadIdx.x; r < nsl * 32; r += (long)gridDim.x * blockDim.x) {
     const long s = r >> 5;
     const int lane = (int)(r & 31);
     const long long b = soff[s];
     const int w = (int)((soff[s + 1] - b) >> 5);
-    const int st = r < nrows ? rp[r] : 0, len = r < nrows ? rp[r + 1] - rp[r] : 0;
+    const long o = r < nrows ? (perm ? perm[r] : r) : 0;
+    const int st = r < nrows ? rp[o] : 0, len = r < nrows ? rp[o + 1] - rp[o] : 0;
     const int padc = len > 0 ? ci[st + len - 1] : 0;
     for (int j = 0; j < w; ++j) {
-      const long long o = b + 32LL * j + lane;
-      sci[o] = j < len ? ci[st + j] : padc;
-      sva[o] = j < len ? va[st + j] : 0.0;
+      const long long q = b + 32LL * j + lane;
+      const int col = j < len ? ci[st + j] : padc;
+      sci[q] = cmap ? cmap[col] : col;
+      sva[q] = j < len ? va[st + j] : 0.0;
     }
+  }
+}
+// out[i w + b] = in[perm[i] w + b]  (row gather of a row-major n x w array)
+__global__ void k_gather_rows(long n, int w, const int *__restrict__ perm, const double *__restrict__ in,
+                              double *__restrict__ out) {
+  for (long t = (long)blockIdx.x * blockDim.x + threadIdx.x; t < n * w; t += (long)gridDim.x * blockDim.x) {
+    const long i = t / w;
+    out[t] = in[(long)perm[i] * w + (t - i * w)];
+  }
+}
+// out[perm[i]] = in[i] for i < n, split at nu into out0 (rows < nu) and out1
+__global__ void k_scatter_split(long n, long nu, const int *__restrict__ perm, const double *__restrict__ in,
+                                double *__restrict__ out0, double *__restrict__ out1) {
+  for (long i = (long)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (long)gridDim.x * blockDim.x) {
+    const long o = perm[i];
+    if (o < nu)
+      out0[o] = in[i];
+    else
+      out1[o - nu] = in[i];
   }
 }
 
@@ -428,7 +462,7 @@ __global__ void __launch_bounds__(256) k_pcg_spmv(long n, Sell S, const double *
     const double qi = fma(eps * w, pi, acc);
     p_new[row] = pi;
     q[row] = qi;
-    v[0] = pi * qi;
+    v[0] += pi * qi;
   }
   block_sum_n<1>(v, sh);
   if (threadIdx.x == 0) part[blockIdx.x] = v[0];
@@ -889,9 +923,9 @@ __device__ __forceinline__ void block_mv(const double *__restrict__ inv, long e,
 __global__ void __launch_bounds__(256) k_cheb_resid(long np, Sell S, double *__restrict__ r,
                                                     const double *__restrict__ d_old, const int *gate) {
   if (!*gate) return;
-  const long row = (long)blockIdx.x * blockDim.x + threadIdx.x;
-  if (row >= np) return;
-  r[row] -= sell_dot(S, row, GatherX{d_old});
+  const long slot = (long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (slot >= np) return;
+  r[sell_row(S, slot)] -= sell_dot(S, slot, GatherX{d_old});
 }
 
 // ---------------------------------------------------------------------------
@@ -925,6 +959,40 @@ __device__ __forceinline__ double row_blk(const double *sinv, const double *sv, 
   return s;
 }
 
+// Element blocks inside a warp: EPW = 32 / NB whole elements per warp (lane
+// l -> element l / NB, row l % NB; lanes >= EPW NB idle).  The NB values of an
+// element's vector are exchanged with shuffles, and each lane streams its own
+// contiguous row of the block inverse, so a warp reads one contiguous span of
+// the inverses and of every vector: no shared-memory staging, no barriers.
+template <int NB>
+struct BlkWarp {
+  static constexpr int EPW = 32 / NB;
+  long e, k;      // element, row
+  int a, base;    // row inside the element, first lane of the element group
+  bool valid;
+  __device__ __forceinline__ BlkWarp(long gw, long ne) {
+    const int lane = threadIdx.x & 31;
+    a = lane % NB;
+    base = lane - a;
+    e = gw * EPW + lane / NB;
+    valid = lane < EPW * NB && e < ne;
+    k = e * NB + a;
+  }
+  // sum_b inv[e][a][b] v[e NB + b], v given per lane (vk = v[k])
+  __device__ __forceinline__ double apply(const double *__restrict__ inv, double vk) const {
+    const double *row = inv + k * NB;
+    double s = 0.0;
+#pragma unroll
+    for (int b = 0; b < NB; ++b) {
+      const double vb = __shfl_sync(0xffffffffu, vk, (base + b) & 31);
+      if (valid) s = fma(__ldcs(row + b), vb, s);
+    }
+    return s;
+  }
+};
+template <int NB>
+__host__ __device__ __forceinline__ long blk_warps(long ne) { return (ne + BlkWarp<NB>::EPW - 1) / BlkWarp<NB>::EPW; }
+
 // block half of a Chebyshev step (mode 0) or the init (mode 1: d = c2 D^-1 r, x = d)
 //   d_new = c1 d_old + c2 D_B^-1 r ; x += d_new ; last -> z_p = -x
 template <int NB>
@@ -933,19 +1001,14 @@ __global__ void __launch_bounds__(256) k_cheb_block(long ne, const double *__res
                                                     double *__restrict__ d_new, double *__restrict__ x, double c1,
                                                     double c2, int mode, int last, double *__restrict__ zp,
                                                     const int *gate) {
-  __shared__ double sinv[BlkTile<NB>::TE * NB * NB];
-  __shared__ double sv[BlkTile<NB>::ROWS];
   if (!*gate) return;
-  constexpr int TE = BlkTile<NB>::TE;
-  for (long e0 = (long)blockIdx.x * TE; e0 < ne; e0 += (long)gridDim.x * TE) {
-    const int te = (int)min((long)TE, ne - e0);
-    __syncthreads();
-    stage_blk<NB>(inv, r, e0, te, sinv, sv);
-    __syncthreads();
-    const int t = threadIdx.x;
-    if (t < te * NB) {
-      const long k = e0 * NB + t;
-      const double tv = row_blk<NB>(sinv, sv, t);
+  const long nw = blk_warps<NB>(ne);
+  for (long gw = ((long)blockIdx.x * blockDim.x + threadIdx.x) >> 5; gw < nw; gw += ((long)gridDim.x * blockDim.x) >> 5) {
+    const BlkWarp<NB> w(gw, ne);
+    const double rk = w.valid ? r[w.k] : 0.0;
+    const double tv = w.apply(inv, rk);
+    if (w.valid) {
+      const long k = w.k;
       const double dn = mode ? c2 * tv : fma(c1, d_old[k], c2 * tv);
       const double xn = mode ? dn : x[k] + dn;
       if (last) {
@@ -965,23 +1028,18 @@ __global__ void __launch_bounds__(256) k_pcg_init_blk(long ne, const double *__r
                                                       double *__restrict__ r, double *__restrict__ z,
                                                       double *__restrict__ p0, double *part, unsigned *counter,
                                                       DevState *st, double rtol, int maxit, const int *gate) {
-  __shared__ double sinv[BlkTile<NB>::TE * NB * NB];
-  __shared__ double sv[BlkTile<NB>::ROWS];
   __shared__ double sh[64];
-  constexpr int TE = BlkTile<NB>::TE;
   const bool on = *gate != 0;
   double v[2] = {0.0, 0.0};
   if (on) {
-    for (long e0 = (long)blockIdx.x * TE; e0 < ne; e0 += (long)gridDim.x * TE) {
-      const int te = (int)min((long)TE, ne - e0);
-      __syncthreads();
-      stage_blk<NB>(inv, b, e0, te, sinv, sv);
-      __syncthreads();
-      const int t = threadIdx.x;
-      if (t < te * NB) {
-        const long k = e0 * NB + t;
-        const double tv = row_blk<NB>(sinv, sv, t);
-        const double bk = sv[t];
+    const long nw = blk_warps<NB>(ne);
+    for (long gw = ((long)blockIdx.x * blockDim.x + threadIdx.x) >> 5; gw < nw;
+         gw += ((long)gridDim.x * blockDim.x) >> 5) {
+      const BlkWarp<NB> w(gw, ne);
+      const double bk = w.valid ? b[w.k] : 0.0;
+      const double tv = w.apply(inv, bk);
+      if (w.valid) {
+        const long k = w.k;
         x[k] = 0.0;
         r[k] = bk;
         z[k] = tv;
@@ -1017,17 +1075,23 @@ __global__ void __launch_bounds__(256) k_pcg_init_blk(long ne, const double *__r
 // block PCG step A (single gather): q = (S + eps W) p, p.q -> alpha
 __global__ void __launch_bounds__(256) k_pcg_spmv_p(long n, Sell S, const double *__restrict__ wdiag, double eps,
                                                     const double *__restrict__ p, double *__restrict__ q,
-                                                    double *part, unsigned *counter, DevState *st) {
+                                                    double *part, unsigned *counter, DevState *st, int split) {
   __shared__ double sh[32];
   if (!st->p.active) return;
-  const long row = (long)blockIdx.x * blockDim.x + threadIdx.x;
   double v[1] = {0.0};
-  if (row < n) {
+  const long slot = (long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (slot < n) {
+    const long row = sell_row(S, slot);
     const double pi = p[row];
     const double w = wdiag ? wdiag[row] : 1.0;
-    const double qi = fma(eps * w, pi, sell_dot(S, row, GatherX{p}));
+    const double qi = fma(eps * w, pi, sell_dot(S, slot, GatherX{p}));
     q[row] = qi;
     v[0] = pi * qi;
+  }
+  if (split) {   // partials only; k_pcg_alpha reduces them (no fence / atomic tail here)
+    block_sum_n<1>(v, sh);
+    if (threadIdx.x == 0) part[blockIdx.x] = v[0];
+    return;
   }
   block_sum_n<1>(v, sh);
   if (threadIdx.x == 0) part[blockIdx.x] = v[0];
@@ -1040,6 +1104,16 @@ __global__ void __launch_bounds__(256) k_pcg_spmv_p(long n, Sell S, const double
     }
   }
 }
+// alpha = rz / sum(part[0 .. nb)): one block, fixed order (split form of k_pcg_spmv_p)
+__global__ void __launch_bounds__(1024) k_pcg_alpha(int nb, const double *__restrict__ part, DevState *st) {
+  __shared__ double sh[32];
+  if (!st->p.active) return;
+  double v[1] = {0.0};
+  for (int b = threadIdx.x; b < nb; b += blockDim.x) v[0] += part[b];
+  block_sum_n<1>(v, sh);
+  if (threadIdx.x == 0) st->p.alpha = st->p.rz / v[0];
+}
+
 // block PCG step C: p = z + beta p (after step B decided beta; skipped once converged)
 __global__ void k_pcg_pupd(long n, const double *__restrict__ z, double *__restrict__ p, DevState *st) {
   if (!st->p.active) return;
@@ -1055,30 +1129,23 @@ __global__ void __launch_bounds__(256) k_pcg_vec_blk(long ne, const double *__re
                                                      double *__restrict__ x, double *__restrict__ r,
                                                      double *__restrict__ z, double *part, unsigned *counter,
                                                      DevState *st) {
-  __shared__ double sinv[BlkTile<NB>::TE * NB * NB];
-  __shared__ double sv[BlkTile<NB>::ROWS];
   __shared__ double sh[64];
-  constexpr int TE = BlkTile<NB>::TE;
   if (!st->p.active) return;
   const double alpha = st->p.alpha;
   double v[2] = {0.0, 0.0};
-  for (long e0 = (long)blockIdx.x * TE; e0 < ne; e0 += (long)gridDim.x * TE) {
-    const int te = (int)min((long)TE, ne - e0);
-    const int t = threadIdx.x;
-    const long k = e0 * NB + t;
-    __syncthreads();
-    for (int qq = threadIdx.x; qq < te * NB * NB; qq += blockDim.x) sinv[qq] = inv[e0 * NB * NB + qq];
+  const long nw = blk_warps<NB>(ne);
+  for (long gw = ((long)blockIdx.x * blockDim.x + threadIdx.x) >> 5; gw < nw; gw += ((long)gridDim.x * blockDim.x) >> 5) {
+    const BlkWarp<NB> w(gw, ne);
     double rk = 0.0;
-    if (t < te * NB) {
+    if (w.valid) {
+      const long k = w.k;
       x[k] = fma(alpha, p[k], x[k]);
       rk = fma(-alpha, q[k], r[k]);
       r[k] = rk;
-      sv[t] = rk;
     }
-    __syncthreads();
-    if (t < te * NB) {
-      const double tv = row_blk<NB>(sinv, sv, t);
-      z[k] = tv;
+    const double tv = w.apply(inv, rk);
+    if (w.valid) {
+      z[w.k] = tv;
       v[0] += rk * tv;
       v[1] += rk * rk;
     }

@@ -88,6 +88,15 @@ struct Ctx {
   int *a_sci = nullptr, *s_sci = nullptr;
   double *a_sva = nullptr, *s_sva = nullptr;
   long nnzA_sell = 0, nnzS_sell = 0;
+  // SELL-C-sigma reordering (build_reorder): perm[new] = old over [u; p], cmap = its inverse;
+  // perm_p / cmap_p the pressure part in pressure numbering.  nullptr: identity.
+  int *perm = nullptr, *cmap = nullptr, *perm_p = nullptr, *cmap_p = nullptr;
+  // S_D SELL slot -> row (internal numbering): S_D rows sorted by length at row level
+  // (element-block kernels need element-contiguous rows, so the symmetric permutation
+  // moves whole elements; the SELL slots of S_D add a row-level sort on top)
+  int *s_slot = nullptr, *s_slot_old = nullptr;
+  int pcg_split = 0;   // block PCG: q = S p with block partials, then a one-block alpha kernel
+  std::pair<long, long> reorder_pad{0, 0};
   double *dMinv = nullptr, *dSinv = nullptr, *dSepsinv = nullptr, *wdiag = nullptr, *sdiag = nullptr;
   // work vectors
   double *V = nullptr, *Z = nullptr;
@@ -292,7 +301,7 @@ struct PcgVecBlkL {
 };
 
 Sell sellA(Ctx *c) { return Sell{c->a_soff, c->a_sci, c->a_sva}; }
-Sell sellS(Ctx *c) { return Sell{c->s_soff, c->s_sci, c->s_sva}; }
+Sell sellS(Ctx *c) { return Sell{c->s_soff, c->s_sci, c->s_sva, c->s_slot}; }
 
 void launch_spmv(Ctx *c, long row0, long nrows, const double *x, double *y, const double *b, int mode,
                  const int *gate) {
@@ -325,11 +334,15 @@ double bytes_cheb(Ctx *c) { return 12.0 * c->nnzS + 56.0 * c->np; }
 double bytes_pcg_vec(Ctx *c) { return 64.0 * c->np; }
 double bytes_vecs(Ctx *c, double nvec) { return 8.0 * c->n * nvec; }
 
-// blocks for the tiled element-block kernels (a few waves over the tiles)
+// blocks for the element-block kernels (BlkWarp: 32 / NB elements per warp),
+// grid-stride over warps with at most one resident wave (8 blocks of 256 per SM)
 template <int NB>
 int grid_blk(Ctx *c, long ne) {
-  const long tiles = (ne + BlkTile<NB>::TE - 1) / BlkTile<NB>::TE;
-  return (int)std::max<long>(1, std::min<long>(tiles, (long)c->sm_count * 16));
+  const long blocks = (blk_warps<NB>(ne) * 32 + 255) / 256;
+  return (int)std::max<long>(1, std::min<long>(blocks, (long)c->sm_count * 8));
+}
+inline int grid_resident(Ctx *c, long n) {
+  return (int)std::max<long>(1, std::min<long>((n + NT - 1) / NT, (long)c->sm_count * 8));
 }
 
 template <int NB>
@@ -497,8 +510,10 @@ int enqueue_pcg_steps(Ctx *c, int nsteps) {
       // block path: p materialised, q = S p with one gather, then p = z + beta p
       {
         TimeScope ts(c, VEM_K_PCG_SPMV, 12.0 * c->nnzS + 32.0 * c->np);
-        k_pcg_spmv_p<<<grid_for(c->np), NT, 0, c->stream>>>(c->np, sellS(c), c->wdiag, c->eps, c->pp0, c->pq,
-                                                           c->part, c->counter, c->st);
+        const int g = grid_for(c->np);
+        k_pcg_spmv_p<<<g, NT, 0, c->stream>>>(c->np, sellS(c), c->wdiag, c->eps, c->pp0, c->pq, c->part,
+                                              c->counter, c->st, c->pcg_split);
+        if (c->pcg_split) k_pcg_alpha<<<1, 1024, 0, c->stream>>>(g, c->part, c->st);
       }
       {
         TimeScope ts(c, VEM_K_PCG_VEC, bytes_pcg_vec(c) + 8.0 * c->np * c->nb);
@@ -799,6 +814,22 @@ int ensure_work(Ctx *c, int kind) {
                             (long)c->sm_count * 64 * 2 + grid_for(c->n * 32) + 1024);
 }
 
+// caller numbering <-> internal (SELL-C-sigma reordered) numbering of [u; p]
+void to_internal(Ctx *c, const double *in, double *out) {
+  if (c->perm)
+    k_gather_rows<<<grid_stream(c, c->n), NT, 0, c->stream>>>(c->n, 1, c->perm, in, out);
+  else
+    cudaMemcpyAsync(out, in, c->n * sizeof(double), cudaMemcpyDeviceToDevice, c->stream);
+}
+void from_internal(Ctx *c, const double *in, double *out_u, double *out_p) {
+  if (c->perm) {
+    k_scatter_split<<<grid_stream(c, c->n), NT, 0, c->stream>>>(c->n, c->nu, c->perm, in, out_u, out_p);
+  } else {
+    cudaMemcpyAsync(out_u, in, c->nu * sizeof(double), cudaMemcpyDeviceToDevice, c->stream);
+    cudaMemcpyAsync(out_p, in + c->nu, c->np * sizeof(double), cudaMemcpyDeviceToDevice, c->stream);
+  }
+}
+
 int solve_impl(Ctx *c, const double *rhs, double tol, int maxit, int kind, double *out_u, double *out_p,
                vem_solve_report *rep) {
   vem_solve_report R{};
@@ -812,7 +843,7 @@ int solve_impl(Ctx *c, const double *rhs, double tol, int maxit, int kind, doubl
   CK(cudaEventCreate(&e0));
   CK(cudaEventCreate(&e1));
   CK(cudaEventRecord(e0, c->stream));
-  CK(cudaMemcpyAsync(c->b, rhs, c->n * sizeof(double), cudaMemcpyDeviceToDevice, c->stream));
+  to_internal(c, rhs, c->b);
   CK(cudaMemsetAsync(c->x, 0, c->n * sizeof(double), c->stream));
   // reset GMRES state
   GmresState g0{};
@@ -893,8 +924,7 @@ int solve_impl(Ctx *c, const double *rhs, double tol, int maxit, int kind, doubl
     R.restarts = restarts;
     R.cycles = cycles;
   }
-  CK(cudaMemcpyAsync(out_u, c->x, c->nu * sizeof(double), cudaMemcpyDeviceToDevice, c->stream));
-  CK(cudaMemcpyAsync(out_p, c->x + c->nu, c->np * sizeof(double), cudaMemcpyDeviceToDevice, c->stream));
+  from_internal(c, c->x, out_u, out_p);
   CK(cudaEventRecord(e1, c->stream));
   CK(cudaStreamSynchronize(c->stream));
   flush_timing(c);
@@ -1101,12 +1131,12 @@ int apply_l2_window(Ctx *c) {
 }
 
 int build_sell(Ctx *c, long nrows, const int *rp, const int *ci, const double *va, long long **soff, int **sci,
-               double **sva, long *nnz_sell) {
+               double **sva, long *nnz_sell, const int *perm = nullptr, const int *cmap = nullptr) {
   const long nsl = (nrows + 31) / 32;
   long long *w = nullptr;
   DA(w, nsl + 1);
   DA(*soff, nsl + 1);
-  k_sell_width<<<grid_stream(c, nsl), NT, 0, c->stream>>>(nrows, rp, w);
+  k_sell_width<<<grid_stream(c, nsl), NT, 0, c->stream>>>(nrows, rp, perm, w);
   CKL();
   CK(cudaMemsetAsync(w + nsl, 0, sizeof(long long), c->stream));
   size_t tb = 0;
@@ -1121,9 +1151,131 @@ int build_sell(Ctx *c, long nrows, const int *rp, const int *ci, const double *v
   dfree(c, w);
   DA(*sci, tot);
   DA(*sva, tot);
-  k_sell_fill<<<grid_stream(c, nsl * 32), NT, 0, c->stream>>>(nrows, rp, ci, va, *soff, *sci, *sva);
+  k_sell_fill<<<grid_stream(c, nsl * 32), NT, 0, c->stream>>>(nrows, rp, ci, va, perm, cmap, *soff, *sci, *sva);
   CKL();
   *nnz_sell = (long)tot;
+  return 0;
+}
+
+// ----------------------------------------------------------------------------
+// SELL-C-sigma reordering (k >= 1 layouts, no AMG): rows of different lengths
+// (face / interior velocity rows, pair / cube elements) share SELL-32 slices and
+// pad every slice to its longest row (C5: 1.8x the nonzeros of A, 2.1x of S_D).
+// The unknowns are renumbered once at upload by a symmetric permutation that
+// sorts velocity rows of A, and elements (all n_p DOFs together, so the
+// element-block Jacobi structure is kept), by row length inside windows of
+// REORDER_WINDOW rows (stable: equal lengths keep their order, locality of the
+// column gathers is kept within a window).  The solve gathers rhs into the new
+// order and scatters u, p back; every hot kernel is unchanged.
+// ----------------------------------------------------------------------------
+constexpr long REORDER_WINDOW = 4096;
+
+long sell_padded(const std::vector<int> &len, const std::vector<int> &perm) {
+  long tot = 0;
+  const long n = (long)len.size();
+  for (long s = 0; s < n; s += 32) {
+    int w = 0;
+    for (long r = s; r < std::min(n, s + 32); ++r) w = std::max(w, len[perm.empty() ? r : perm[r]]);
+    tot += 32L * w;
+  }
+  return tot;
+}
+
+// stable sort of [first, last) of idx by key descending, in windows of `win` entries
+void window_sort(std::vector<int> &idx, const std::vector<long long> &key, long win) {
+  const long n = (long)idx.size();
+  for (long w0 = 0; w0 < n; w0 += win) {
+    auto b = idx.begin() + w0, e = idx.begin() + std::min(n, w0 + win);
+    std::stable_sort(b, e, [&](int a, int c) { return key[a] > key[c]; });
+  }
+}
+
+int build_reorder(Ctx *c) {
+  if (c->nb <= 1 || c->opts.reorder == 0) return 0;
+  const long nu = c->nu, np = c->np, n = c->n, nb = c->nb, ne = np / nb;
+  std::vector<int> arp(n + 1), srp(np + 1);
+  CK(cudaMemcpyAsync(arp.data(), c->a_rp, (n + 1) * sizeof(int), cudaMemcpyDeviceToHost, c->stream));
+  CK(cudaMemcpyAsync(srp.data(), c->s_rp, (np + 1) * sizeof(int), cudaMemcpyDeviceToHost, c->stream));
+  CK(cudaStreamSynchronize(c->stream));
+  std::vector<int> alen(n), slen(np);
+  for (long i = 0; i < n; ++i) alen[i] = arp[i + 1] - arp[i];
+  for (long i = 0; i < np; ++i) slen[i] = srp[i + 1] - srp[i];
+  // velocity rows: key = A row length
+  std::vector<int> pu(nu);
+  std::vector<long long> ku(nu);
+  for (long i = 0; i < nu; ++i) {
+    pu[i] = (int)i;
+    ku[i] = alen[i];
+  }
+  window_sort(pu, ku, REORDER_WINDOW);
+  // elements: key = (max B row length, max S_D row length) of the element's DOFs
+  std::vector<int> pe(ne);
+  std::vector<long long> ke(ne);
+  for (long e = 0; e < ne; ++e) {
+    int ls = 0, lb = 0;
+    for (long a = 0; a < nb; ++a) {
+      ls = std::max(ls, slen[e * nb + a]);
+      lb = std::max(lb, alen[nu + e * nb + a]);
+    }
+    pe[e] = (int)e;
+    ke[e] = ((long long)lb << 32) | (long long)ls;
+  }
+  window_sort(pe, ke, std::max(1L, REORDER_WINDOW / nb));
+  std::vector<int> perm(n), cmap(n);
+  for (long i = 0; i < nu; ++i) perm[i] = pu[i];
+  for (long e = 0; e < ne; ++e)
+    for (long a = 0; a < nb; ++a) perm[nu + e * nb + a] = (int)(nu + (long)pe[e] * nb + a);
+  for (long i = 0; i < n; ++i) cmap[perm[i]] = (int)i;
+  // keep it only where it removes padding
+  const long pad0 = sell_padded(alen, {}) + sell_padded(slen, {});
+  std::vector<int> permp(np);
+  for (long i = 0; i < np; ++i) permp[i] = perm[nu + i] - (int)nu;
+  // S_D slots: rows (internal numbering) sorted by length in windows; slot_old = the CSR row
+  std::vector<int> sslot(np), sslot_old(np);
+  {
+    std::vector<long long> ks(np);
+    for (long i = 0; i < np; ++i) {
+      sslot[i] = (int)i;
+      ks[i] = slen[permp[i]];
+    }
+    window_sort(sslot, ks, REORDER_WINDOW);
+    for (long i = 0; i < np; ++i) sslot_old[i] = permp[sslot[i]];
+  }
+  const long pad1 = sell_padded(alen, perm) + sell_padded(slen, sslot_old);
+  if ((double)pad0 < 1.05 * (double)pad1) return 0;
+  std::vector<int> cmapp(np);
+  for (long i = 0; i < np; ++i) cmapp[i] = cmap[nu + i] - (int)nu;
+  int r;
+  if ((r = upload_array(c, &c->perm, perm.data(), n))) return r;
+  if ((r = upload_array(c, &c->cmap, cmap.data(), n))) return r;
+  if ((r = upload_array(c, &c->perm_p, permp.data(), np))) return r;
+  if ((r = upload_array(c, &c->cmap_p, cmapp.data(), np))) return r;
+  if ((r = upload_array(c, &c->s_slot, sslot.data(), np))) return r;
+  if ((r = upload_array(c, &c->s_slot_old, sslot_old.data(), np))) return r;
+  // permute the per-row vectors built in the original order
+  double *tmp = nullptr;
+  DA(tmp, np * nb);
+  auto permute = [&](double *v, long len, const int *pm, int w) {
+    k_gather_rows<<<grid_stream(c, len * w), NT, 0, c->stream>>>(len, w, pm, v, tmp);
+    cudaMemcpyAsync(v, tmp, len * w * sizeof(double), cudaMemcpyDeviceToDevice, c->stream);
+  };
+  {
+    double *tu = nullptr;
+    DA(tu, nu);
+    k_gather_rows<<<grid_stream(c, nu), NT, 0, c->stream>>>(nu, 1, c->perm, c->dMinv, tu);
+    CK(cudaMemcpyAsync(c->dMinv, tu, nu * sizeof(double), cudaMemcpyDeviceToDevice, c->stream));
+    CK(cudaStreamSynchronize(c->stream));
+    dfree(c, tu);
+  }
+  permute(c->dSinv, np, c->perm_p, 1);
+  if (c->wdiag) permute(c->wdiag, np, c->perm_p, 1);
+  if (c->dSepsinv) permute(c->dSepsinv, np, c->perm_p, 1);
+  if (c->dBinv) permute(c->dBinv, np, c->perm_p, (int)nb);
+  if (c->dBeinv) permute(c->dBeinv, np, c->perm_p, (int)nb);
+  CKL();
+  CK(cudaStreamSynchronize(c->stream));
+  dfree(c, tmp);
+  c->reorder_pad = {pad0, pad1};
   return 0;
 }
 
@@ -1395,6 +1547,7 @@ int build_amg(Ctx *c) {
 int upload_impl(Ctx *c, const vem_csr *M, const vem_csr *B, const vem_csr *W, double eps, const vem_layout *lay) {
   auto t0 = std::chrono::steady_clock::now();
   const bool trace = getenv("VEM_SETUP_TRACE") != nullptr;
+  c->pcg_split = getenv("VEM_PCG_SPLIT") ? atoi(getenv("VEM_PCG_SPLIT")) : 0;
   auto phase = [&](const char *what) {
     if (!trace) return;
     cudaStreamSynchronize(c->stream);
@@ -1587,9 +1740,13 @@ int upload_impl(Ctx *c, const vem_csr *M, const vem_csr *B, const vem_csr *W, do
     DA(c->pb, c->np);
   }
   {
-    int rr = build_sell(c, c->n, c->a_rp, c->a_ci, c->a_va, &c->a_soff, &c->a_sci, &c->a_sva, &c->nnzA_sell);
+    int rr = build_reorder(c);
     if (rr) return rr;
-    rr = build_sell(c, c->np, c->s_rp, c->s_ci, c->s_va, &c->s_soff, &c->s_sci, &c->s_sva, &c->nnzS_sell);
+    rr = build_sell(c, c->n, c->a_rp, c->a_ci, c->a_va, &c->a_soff, &c->a_sci, &c->a_sva, &c->nnzA_sell, c->perm,
+                    c->cmap);
+    if (rr) return rr;
+    rr = build_sell(c, c->np, c->s_rp, c->s_ci, c->s_va, &c->s_soff, &c->s_sci, &c->s_sva, &c->nnzS_sell,
+                    c->s_slot_old, c->cmap_p);
     if (rr) return rr;
   }
   CK(cudaStreamSynchronize(c->stream));
@@ -1667,6 +1824,7 @@ void vem_mixed_default_options(vem_opts *o) {
   o->pcg_chunk = 16;
   o->reorth = -1;
   o->l2_persist = 1;
+  o->reorder = 1;
 }
 
 static int validate_opts(Ctx *c, const vem_opts *o) {
@@ -1675,6 +1833,7 @@ static int validate_opts(Ctx *c, const vem_opts *o) {
   if (!(o->cheb_ratio > 1.0)) return fail(c, VEM_ERR_INVALID, "cheb_ratio must be > 1");
   if (!(o->inner_rtol > 0.0) || o->inner_maxit < 1) return fail(c, VEM_ERR_INVALID, "bad inner PCG options");
   if (o->reorth < -1 || o->reorth > 1) return fail(c, VEM_ERR_INVALID, "reorth must be -1, 0 or 1");
+  if (o->reorder < 0 || o->reorder > 1) return fail(c, VEM_ERR_INVALID, "reorder must be 0 or 1");
   return 0;
 }
 
@@ -1752,7 +1911,13 @@ int vem_mixed_spmv(vem_ctx *h, const double *x, double *y) {
   Ctx *c = h->impl;
   int r = enter(c);
   if (r) return r;
-  launch_spmv(c, 0L, c->n, x, y, nullptr, 0, gate_one(c));
+  if (c->perm) {   // x, y in the caller's numbering
+    to_internal(c, x, c->t);
+    launch_spmv(c, 0L, c->n, c->t, c->z, nullptr, 0, gate_one(c));
+    from_internal(c, c->z, y, y + c->nu);
+  } else {
+    launch_spmv(c, 0L, c->n, x, y, nullptr, 0, gate_one(c));
+  }
   CKL();
   CK(cudaStreamSynchronize(c->stream));
   return leave(c, VEM_OK);
@@ -1763,7 +1928,13 @@ int vem_mixed_schur_spmv(vem_ctx *h, const double *x, double *y) {
   Ctx *c = h->impl;
   int r = enter(c);
   if (r) return r;
-  launch_schur_spmv(c, x, y, gate_one(c));
+  if (c->perm) {   // pressure vectors in the caller's numbering
+    k_gather_rows<<<grid_stream(c, c->np), NT, 0, c->stream>>>(c->np, 1, c->perm_p, x, c->t);
+    launch_schur_spmv(c, c->t, c->z, gate_one(c));
+    k_gather_rows<<<grid_stream(c, c->np), NT, 0, c->stream>>>(c->np, 1, c->cmap_p, c->z, y);
+  } else {
+    launch_schur_spmv(c, x, y, gate_one(c));
+  }
   CKL();
   CK(cudaStreamSynchronize(c->stream));
   return leave(c, VEM_OK);
@@ -1777,8 +1948,15 @@ int vem_mixed_precond_apply(vem_ctx *h, int32_t kind, const double *v, double *z
   int64_t its = 0;
   int r = enter(c);
   if (r) return r;
-  r = enqueue_precond(c, kind, v, &c->st->one, z, gate_one(c), &its);
-  if (r) return leave(c, r);
+  if (c->perm) {   // v, z in the caller's numbering (staged through the solve vectors b, x)
+    to_internal(c, v, c->b);
+    r = enqueue_precond(c, kind, c->b, &c->st->one, c->x, gate_one(c), &its);
+    if (r) return leave(c, r);
+    from_internal(c, c->x, z, z + c->nu);
+  } else {
+    r = enqueue_precond(c, kind, v, &c->st->one, z, gate_one(c), &its);
+    if (r) return leave(c, r);
+  }
   CK(cudaStreamSynchronize(c->stream));
   flush_timing(c);
   if (inner_its) *inner_its = its;
@@ -1831,6 +2009,9 @@ int vem_mixed_get_info(vem_ctx *h, vem_info *info) {
   info->l2_window_bytes = (int64_t)c->l2_window_bytes;
   info->amg_levels = (int32_t)c->amg.size();
   info->amg_coarsest = c->amg.empty() ? 0 : c->amg.back().n;
+  info->reordered = c->perm ? 1 : 0;
+  info->nnz_A_stored = c->nnzA_sell;
+  info->nnz_S_stored = c->nnzS_sell;
   return VEM_OK;
 }
 

@@ -159,6 +159,48 @@ def test_block_reg_fixed_budget_c5s():
     sv.close()
 
 
+@pytest.mark.parametrize("name", ["C4s", "C5s", "C2s"])
+def test_sell_sigma_reordering(name):
+    """SELL-C-sigma reordering (opts.reorder, k >= 1): active where it removes
+    slice padding (C4s, C5s mix row lengths), invisible to the caller: every
+    entry point returns the same numbers as the identity numbering up to the
+    summation order, and a solve lands in the same iteration band."""
+    s = system(name)
+    cfg = configs.CONFIGS[name]
+    a = solver_for(s, restart=cfg.restart)
+    b = solver_for(s, restart=cfg.restart, reorder=0)
+    ia, ib = a.info(), b.info()
+    assert ib["reordered"] == 0
+    if name != "C2s":
+        assert ia["reordered"] == 1
+        assert ia["nnz_A_stored"] + ia["nnz_S_stored"] < 0.95 * (ib["nnz_A_stored"] + ib["nnz_S_stored"])
+    x = RNG.normal(size=s.n)
+    ya = a.spmv(torch.from_numpy(x).cuda()).cpu().numpy()
+    assert rel_inf(ya, O.spmv_saddle(s.M, s.B, x)) <= 1e-12
+    xp = RNG.normal(size=s.layout.n_p)
+    ysa = a.schur_spmv(torch.from_numpy(xp).cuda()).cpu().numpy()
+    assert rel_inf(ysa, O.schur_diag(s.M, s.B) @ xp) <= 1e-12
+    for kind in cfg.precs:
+        za, _ = a.precond_apply(kind, torch.from_numpy(x).cuda())
+        zb, _ = b.precond_apply(kind, torch.from_numpy(x).cuda())
+        assert rel_inf(za.cpu().numpy(), zb.cpu().numpy()) <= 1e-8
+    kind = cfg.precs[0]
+    if name == "C5s":   # fixed budget (see test_block_reg_fixed_budget_c5s)
+        ra = a.solve(torch.from_numpy(s.rhs).cuda(), 1e-10, 50, kind)
+        rb = b.solve(torch.from_numpy(s.rhs).cuda(), 1e-10, 50, kind)
+        assert rel_inf(ra.u.cpu().numpy(), rb.u.cpu().numpy()) <= 1e-6
+        assert rel_inf(ra.p.cpu().numpy(), rb.p.cpu().numpy()) <= 1e-6
+    else:               # a reordering is an ulp-level perturbation: compare with the oracle band (R20)
+        ref, lo, hi = oracle_iteration_band(s, kind, cfg.restart, configs.eps_for(s))
+        ra = a.solve(torch.from_numpy(s.rhs).cuda(), 1e-10, 10000, kind)
+        assert ra.report["converged"] == 1
+        assert lo - 2 <= ra.report["iterations"] <= hi + 2, (ra.report["iterations"], lo, hi)
+        nu = s.layout.n_u
+        assert rel_inf(ra.u.cpu().numpy(), ref.x[:nu]) <= 1e-8 and rel_inf(ra.p.cpu().numpy(), ref.x[nu:]) <= 1e-8
+    a.close()
+    b.close()
+
+
 @pytest.mark.parametrize("name", ["C1", "C3s", "C2s"])
 def test_cgs2_option_parity(name):
     """opts.reorth = 1 (CGS2 for every preconditioner) against the oracle's CGS2."""
