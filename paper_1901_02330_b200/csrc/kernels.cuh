@@ -1114,6 +1114,33 @@ __global__ void __launch_bounds__(1024) k_pcg_alpha(int nb, const double *__rest
   if (threadIdx.x == 0) st->p.alpha = st->p.rz / v[0];
 }
 
+// split form of the k_pcg_vec_blk tail: one block sums the (r.z, r.r) partials in a
+// fixed order, then its++, convergence ||r|| <= rtol ||b||, beta = rz_new / rz
+__global__ void __launch_bounds__(1024) k_pcg_beta(int nb, const double *__restrict__ part, DevState *st) {
+  __shared__ double sh[64];
+  if (!st->p.active) return;
+  double v[2] = {0.0, 0.0};
+  for (int b = threadIdx.x; b < nb; b += blockDim.x) {
+    v[0] += part[2 * b];
+    v[1] += part[2 * b + 1];
+  }
+  block_sum_n<2>(v, sh);
+  if (threadIdx.x == 0) {
+    PcgState &pp = st->p;
+    pp.its += 1;
+    pp.rr = v[1];
+    if (sqrt(v[1]) <= pp.tol_abs) {
+      pp.active = 0;
+    } else if (pp.its >= pp.maxit) {
+      pp.active = 0;
+      pp.failed = 1;
+    } else {
+      pp.beta = v[0] / pp.rz;
+      pp.rz = v[0];
+    }
+  }
+}
+
 // block PCG step C: p = z + beta p (after step B decided beta; skipped once converged)
 __global__ void k_pcg_pupd(long n, const double *__restrict__ z, double *__restrict__ p, DevState *st) {
   if (!st->p.active) return;
@@ -1128,7 +1155,7 @@ __global__ void __launch_bounds__(256) k_pcg_vec_blk(long ne, const double *__re
                                                      const double *__restrict__ p, const double *__restrict__ q,
                                                      double *__restrict__ x, double *__restrict__ r,
                                                      double *__restrict__ z, double *part, unsigned *counter,
-                                                     DevState *st) {
+                                                     DevState *st, int split) {
   __shared__ double sh[64];
   if (!st->p.active) return;
   const double alpha = st->p.alpha;
@@ -1155,6 +1182,7 @@ __global__ void __launch_bounds__(256) k_pcg_vec_blk(long ne, const double *__re
     part[blockIdx.x * 2 + 0] = v[0];
     part[blockIdx.x * 2 + 1] = v[1];
   }
+  if (split) return;   // k_pcg_beta reduces the partials
   if (elect_last_block(counter)) {
     __shared__ double tot[2];
     reduce_partials<2>(part, gridDim.x, 2, tot);

@@ -368,8 +368,15 @@ void PcgInitBlkL<NB>::run(Ctx *c, const int *gate) {
 template <int NB>
 void PcgVecBlkL<NB>::run(Ctx *c, const double *p) {
   const long ne = c->np / NB;
-  k_pcg_vec_blk<NB><<<grid_blk<NB>(c, ne), 256, 0, c->stream>>>(ne, c->dBeinv, p, c->pq, c->px, c->pr, c->pz, c->part,
-                                                              c->counter, c->st);
+  if (c->pcg_split) {   // full grid (one element group per warp), partials reduced by k_pcg_beta
+    const int g = (int)((blk_warps<NB>(ne) * 32 + 255) / 256);
+    k_pcg_vec_blk<NB><<<g, 256, 0, c->stream>>>(ne, c->dBeinv, p, c->pq, c->px, c->pr, c->pz, c->part, c->counter,
+                                                c->st, 1);
+    k_pcg_beta<<<1, 1024, 0, c->stream>>>(g, c->part, c->st);
+  } else {
+    k_pcg_vec_blk<NB><<<grid_blk<NB>(c, ne), 256, 0, c->stream>>>(ne, c->dBeinv, p, c->pq, c->px, c->pr, c->pz,
+                                                                c->part, c->counter, c->st, 0);
+  }
 }
 
 const int *gate_one(Ctx *c) { return &c->st->one_i; }
@@ -1547,7 +1554,7 @@ int build_amg(Ctx *c) {
 int upload_impl(Ctx *c, const vem_csr *M, const vem_csr *B, const vem_csr *W, double eps, const vem_layout *lay) {
   auto t0 = std::chrono::steady_clock::now();
   const bool trace = getenv("VEM_SETUP_TRACE") != nullptr;
-  c->pcg_split = getenv("VEM_PCG_SPLIT") ? atoi(getenv("VEM_PCG_SPLIT")) : 0;
+  c->pcg_split = getenv("VEM_PCG_SPLIT") ? atoi(getenv("VEM_PCG_SPLIT")) : 1;
   auto phase = [&](const char *what) {
     if (!trace) return;
     cudaStreamSynchronize(c->stream);
