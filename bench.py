@@ -5,7 +5,9 @@ saddle-point system (BASELINE.json metric: time-to-solution & GMRES iters/s at
 
 One step = one vem_mixed_solve of the configured system from x0 = 0 to
 rtol 1e-10 (upload and S_D build happen once, before timing: reported as
-setup_ms).  value = GMRES iterations / s over the K timed steps, all ranks.
+setup_ms).  value = solves / s over the K timed steps, all ranks (the inverse of
+the time to solution, summed over replicas); the GMRES iteration rate is reported
+beside it (gmres_it_per_s), as are the per-kernel HBM rates.
 
   python bench.py [--gpus N] [--steps K] [--warmup W] [--config C3] [--impl ours|reference]
 
@@ -26,7 +28,17 @@ ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
 METRIC = "time-to-solution & GMRES iters/s at 1 B200; SpMV/precond HBM GB/s vs peak"
-UNIT = "GMRES it/s"
+UNIT = "solves/s"
+ORACLE_ITS = os.path.join(ROOT, "profiles", "oracle_iterations.json")
+
+
+def oracle_iterations(name, kind):
+    """GMRES iterations the oracle itself needs for this workload (full-length CPU
+    solve written by tools/oracle_iterations.py, oracle/ only); None if not recorded."""
+    try:
+        return int(json.load(open(ORACLE_ITS))[name][str(kind)]["iterations"])
+    except Exception:
+        return None
 
 
 def parse():
@@ -169,9 +181,13 @@ def cpu_baseline(system, cfg, kind, eps, its):
     res = O.gmres(lambda x: O.spmv_saddle(system.M, system.B, x), P.apply, system.rhs, 1e-10, cfg.restart, its,
                   P.flexible, 1 if P.flexible else 0)
     t2 = time.perf_counter()
-    return {"value": res.iterations / (t2 - t1), "unit": UNIT, "cores": int(cores), "kind": "oracle",
+    itps = res.iterations / (t2 - t1)
+    full = oracle_iterations(cfg.name, kind)
+    return {"value": (itps / full) if full else None, "unit": UNIT, "cores": int(cores), "kind": "oracle",
+            "gmres_it_per_s": itps, "iterations_per_solve": full,
             "sample": f"{res.iterations} GMRES iterations of {cfg.name} (precond {kind}) from x0=0, "
-                      f"{t2 - t1:.1f} s (+{t1 - t0:.1f} s preconditioner setup, untimed)",
+                      f"{t2 - t1:.1f} s (+{t1 - t0:.1f} s preconditioner setup, untimed); solves/s = "
+                      f"it/s / {full} (the oracle's own full-solve count, profiles/oracle_iterations.json)",
             "setup_s": t1 - t0}
 
 
@@ -182,8 +198,8 @@ def run_reference(args):
         return
     from vemgen.configs import CONFIGS, eps_for
     cfg = CONFIGS[args.config]
-    kind = args.precond or cfg.precs[0]
     s = cfg.build()
+    kind = headline_kind(cfg, s, args)   # the same preconditioner as our arm
     eps = eps_for(s)
     vals = []
     for _ in range(args.warmup):
@@ -196,14 +212,15 @@ def run_reference(args):
         vals.append(last["value"])
         tot_its += args.cpu_sample_its
     dt = time.perf_counter() - t0
-    value = sum(vals) / len(vals)
+    value = sum(vals) / len(vals) if all(v is not None for v in vals) else None
     line = {"impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * dt / args.steps,
             "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
             "data": "synthetic (seeded vemgen assembly)",
             "config": {"workload": f"{cfg.name}: {cfg.describe}", "rtol": cfg.rtol, "restart": cfg.restart,
                        "precond": kind, "n_dofs": s.n},
-            "cpu_baseline": {k: last[k] for k in ("kind", "cores", "sample")} | {"value": value, "unit": UNIT},
+            "cpu_baseline": {k: last[k] for k in ("kind", "cores", "sample", "gmres_it_per_s", "iterations_per_solve")}
+            | {"value": value, "unit": UNIT},
             "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
 
@@ -267,7 +284,9 @@ def main():
     its = sum(r["iterations"] for r in reports)
     # max over ranks of the time, sum of the work
     ms, its_all = reduce_over_ranks(ms, its, device="cuda")
-    value = its_all / (ms / 1e3)
+    solves_all = float(args.steps * ws)   # every rank solves its own replica K times
+    value = solves_all / (ms / 1e3)
+    it_rate = its_all / (ms / 1e3)
 
     # kernel breakdown: one more solve with every launch timed (after the timed region)
     sv.set_options(timing=1, use_graphs=0)
@@ -339,7 +358,8 @@ def main():
                 "share": round(v["ms"] / max(sum(x["ms"] for x in per.values()), 1e-9), 4)}
             for k, v in per.items()}
     launches = launches_per_solve * args.steps
-    line = {"metric": METRIC, "value": round(value, 2), "unit": UNIT, "n_gpus": ws, "steps": args.steps,
+    line = {"metric": METRIC, "value": round(value, 3), "unit": UNIT, "time_to_solution_ms": round(ms / args.steps, 2),
+            "gmres_it_per_s": round(it_rate, 1), "n_gpus": ws, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": ms / args.steps, "higher_is_better": True, "scaling": "weak",
             "vs_baseline": None, "dtype": "f64", "data": "synthetic (seeded vemgen assembly, no dataset)",
             "config": {"workload": f"{cfg.name}: {cfg.describe}", "n_dofs": s.n, "n_u": s.layout.n_u,
@@ -361,7 +381,8 @@ def main():
                                   else "per-launch CUDA events, no graphs"),
                        "kernels_source": "per-launch CUDA events over one extra solve after the timed region"},
             "roofline": roof, "kernels": kern, "gpu_launches": launches, "variant": variant,
-            "e2e": {"value": round(e2e_graph_its / e2e_s, 2), "unit": UNIT,
+            "e2e": {"value": round(args.steps / e2e_s, 3), "unit": UNIT, "time_to_solution_ms": round(1e3 * e2e_s / args.steps, 2),
+                    "gmres_it_per_s": round(e2e_graph_its / e2e_s, 1),
                     "h2d_bytes_per_step": 8 * s.n, "d2h_bytes_per_step": 8 * s.n,
                     "path": "vem_mixed_solve_host (pinned host rhs -> solve -> u, p to host), CUDA graphs"},
             "clocks": clk.summary()}

@@ -8,6 +8,8 @@ on S_D (reading R22), a fixed linear operator, so plain GMRES applies.
 
 Definition (the GPU follows it step by step):
   * strength: off-diagonal (i, j) is strong iff |A_ij| >= theta sqrt(A_ii A_jj), theta = 0.08
+    on the finest level, THETA_COARSE = 0.04 below it (the smoothed-aggregation
+    operator of level 1 has many weak entries; 0.08 stalls its coarsening)
   * keys: key(i) = ((splitmix64(i) >> 33) << 30) | i  (distinct, index recoverable)
   * MIS-2 (Luby, deterministic): repeat { k1 = max key over N[i], k2 = max k1 over
     N[i] (N = strong neighbours incl. i; roots count as +inf, excluded as -1);
@@ -17,14 +19,18 @@ Definition (the GPU follows it step by step):
     root of largest key among its strong neighbours; pass 2: a still free node
     joins the aggregate of its largest-key assigned strong neighbour; pass 3:
     the rest become singletons in index order
-  * P piecewise constant, A_c = P^T A P; stop when n <= COARSE_SIZE, at
-    MAX_LEVELS, or when a level coarsens by less than 1/0.75
+  * prolongator: on the first SA_LEVELS = 1 level(s) the smoothed aggregation
+    prolongator P = (I - omega D^-1 A) T with T piecewise constant on the
+    aggregates and omega = 4 / (3 lmax) (Vanek, Mandel & Brezina 1996: one damped
+    Jacobi step on the tentative prolongator); below, P = T.  A_c = P^T A P; stop
+    when n <= COARSE_SIZE, at MAX_LEVELS, or when a level coarsens by less than 1/0.75
   * coarsest level (COARSE_SIZE = 2048): dense inverse applied as a matvec, else
     (stagnated coarsening) a degree-COARSE_DEGREE Chebyshev smoother
   * smoother C_l(b): degree-DEGREE point-Jacobi Chebyshev from x0 = 0 (Saad
     Alg. 12.1, exactly oracle.solver.chebyshev) on [lmax/RATIO, lmax] with the
     Gershgorin bound lmax = max_i sum_j |A_ij| / A_ii
   * V(b) at level l: x = C(b); r = b - A x; x += P V(P^T r); x += C(b - A x)
+    (restriction P^T r is the aggregate sum of r when P = T)
 Parity unpinned by the paper (iteration counts).  Pinned in
 tests/test_oracle_pins.py: MIS-2 property, aggregate validity, Galerkin identity,
 a one-level hierarchy is an exact solve, symmetry of the V-cycle operator.
@@ -39,6 +45,8 @@ import scipy.sparse as sp
 from .solver import chebyshev
 
 THETA = 0.08
+THETA_COARSE = 0.04
+SA_LEVELS = 1
 COARSE_SIZE = 2048
 MAX_LEVELS = 12
 DEGREE = 3
@@ -124,6 +132,16 @@ def galerkin(A, agg, nc):
     return Ac
 
 
+def smoothed_prolongator(A, agg, nc, lmax):
+    """P = (I - omega D^-1 A) T, omega = 4 / (3 lmax), T_{i, agg_i} = 1."""
+    n = A.shape[0]
+    T = sp.csr_matrix((np.ones(n), (np.arange(n), agg)), shape=(n, nc))
+    omega = 4.0 / (3.0 * lmax)
+    P = (T - omega * (sp.diags(1.0 / A.diagonal()) @ (A.tocsr() @ T))).tocsr()
+    P.sort_indices()
+    return P
+
+
 def gershgorin(A):
     a = abs(A).sum(axis=1).A1
     return float(np.max(a / A.diagonal()))
@@ -136,6 +154,7 @@ class Level:
     lmax: float
     agg: np.ndarray | None = None
     nc: int = 0
+    P: sp.csr_matrix | None = None     # smoothed prolongator (None: piecewise constant on agg)
 
 
 class AMG:
@@ -149,11 +168,17 @@ class AMG:
             self.levels.append(lev)
             if A.shape[0] <= coarse_size or len(self.levels) >= max_levels:
                 break
-            agg, nc, _ = aggregate(A, theta)
+            agg, nc, _ = aggregate(A, theta if len(self.levels) == 1 else THETA_COARSE)
             if nc > STAGNATION * A.shape[0]:
                 break
             lev.agg, lev.nc = agg, nc
-            A = galerkin(A, agg, nc)
+            if len(self.levels) <= SA_LEVELS:
+                lev.P = smoothed_prolongator(A, agg, nc, lev.lmax)
+                A = (lev.P.T @ A @ lev.P).tocsr()
+                A.sum_duplicates()
+                A.sort_indices()
+            else:
+                A = galerkin(A, agg, nc)
         last = self.levels[-1]
         self.coarse_inv = np.linalg.inv(last.A.toarray()) if last.A.shape[0] <= coarse_size else None
 
@@ -168,8 +193,11 @@ class AMG:
             return self.smooth(lev, b, COARSE_DEGREE)
         x = self.smooth(lev, b)
         r = b - lev.A @ x
-        bc = np.bincount(lev.agg, weights=r, minlength=lev.nc)
-        xc = self.vcycle(bc, level + 1)
-        x = x + xc[lev.agg]
+        if lev.P is not None:
+            x = x + lev.P @ self.vcycle(lev.P.T @ r, level + 1)
+        else:
+            bc = np.bincount(lev.agg, weights=r, minlength=lev.nc)
+            xc = self.vcycle(bc, level + 1)
+            x = x + xc[lev.agg]
         x = x + self.smooth(lev, b - lev.A @ x)
         return x

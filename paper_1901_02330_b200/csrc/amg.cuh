@@ -368,3 +368,106 @@ __global__ void k_amg_top(long nu, long np, const double *__restrict__ v, const 
       b0[i - nu] = s * v[i];
   }
 }
+
+// ---------------------------------------------------------------------------
+// Smoothed aggregation (level 0, oracle/amg.py smoothed_prolongator):
+//   P = (I - omega D^-1 A) T,  A_c = P^T (A P); every product is expanded into
+//   (key, value) pairs in a fixed order, stable-radix-sorted and run-reduced.
+// ---------------------------------------------------------------------------
+// A T: (i nc + agg_j, a_ij)
+__global__ void k_sa_expand_at(long n, const int *__restrict__ rp, const int *__restrict__ ci,
+                               const double *__restrict__ va, const int *__restrict__ agg, long long nc,
+                               unsigned long long *__restrict__ keys, double *__restrict__ vals) {
+  for (long i = (long)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (long)gridDim.x * blockDim.x) {
+    for (int k = rp[i]; k < rp[i + 1]; ++k) {
+      keys[k] = (unsigned long long)(i * nc + agg[ci[k]]);
+      vals[k] = va[k];
+    }
+  }
+}
+// P values from (A T) entries in place: p = [col == agg_row] - omega dinv_row (A T)
+__global__ void k_sa_pvals(long nnz, const int *__restrict__ row, const int *__restrict__ col,
+                           const int *__restrict__ agg, const double *__restrict__ dinv, double omega,
+                           double *__restrict__ va) {
+  for (long k = (long)blockIdx.x * blockDim.x + threadIdx.x; k < nnz; k += (long)gridDim.x * blockDim.x) {
+    const int i = row[k];
+    va[k] = (col[k] == agg[i] ? 1.0 : 0.0) - omega * dinv[i] * va[k];
+  }
+}
+// count / fill of the expansion of A P: row i emits sum_{j in A_i} |P_j| products
+__global__ void k_sa_count_ap(long n, const int *__restrict__ arp, const int *__restrict__ aci,
+                              const int *__restrict__ prp, long long *__restrict__ cnt) {
+  for (long i = (long)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (long)gridDim.x * blockDim.x) {
+    long long s = 0;
+    for (int k = arp[i]; k < arp[i + 1]; ++k) s += prp[aci[k] + 1] - prp[aci[k]];
+    cnt[i] = s;
+  }
+}
+__global__ void k_sa_fill_ap(long n, const int *__restrict__ arp, const int *__restrict__ aci,
+                             const double *__restrict__ ava, const int *__restrict__ prp,
+                             const int *__restrict__ pci, const double *__restrict__ pva,
+                             const long long *__restrict__ off, long long nc, unsigned long long *__restrict__ keys,
+                             double *__restrict__ vals) {
+  for (long i = (long)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (long)gridDim.x * blockDim.x) {
+    long long o = off[i];
+    for (int k = arp[i]; k < arp[i + 1]; ++k) {
+      const int j = aci[k];
+      const double a = ava[k];
+      for (int q = prp[j]; q < prp[j + 1]; ++q) {
+        keys[o] = (unsigned long long)(i * nc + pci[q]);
+        vals[o] = a * pva[q];
+        ++o;
+      }
+    }
+  }
+}
+// count / fill of the expansion of P^T Q (Q = A P): row i emits |P_i| |Q_i| products (a nc + b, p_ia q_ib)
+__global__ void k_sa_count_ptq(long n, const int *__restrict__ prp, const int *__restrict__ qrp,
+                               long long *__restrict__ cnt) {
+  for (long i = (long)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (long)gridDim.x * blockDim.x)
+    cnt[i] = (long long)(prp[i + 1] - prp[i]) * (qrp[i + 1] - qrp[i]);
+}
+__global__ void k_sa_fill_ptq(long n, const int *__restrict__ prp, const int *__restrict__ pci,
+                              const double *__restrict__ pva, const int *__restrict__ qrp,
+                              const int *__restrict__ qci, const double *__restrict__ qva,
+                              const long long *__restrict__ off, long long nc, unsigned long long *__restrict__ keys,
+                              double *__restrict__ vals) {
+  for (long i = (long)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (long)gridDim.x * blockDim.x) {
+    long long o = off[i];
+    for (int a = prp[i]; a < prp[i + 1]; ++a)
+      for (int b = qrp[i]; b < qrp[i + 1]; ++b) {
+        keys[o] = (unsigned long long)((long long)pci[a] * nc + qci[b]);
+        vals[o] = pva[a] * qva[b];
+        ++o;
+      }
+  }
+}
+// P^T as (col n + row, p) pairs
+__global__ void k_sa_expand_pt(long n, const int *__restrict__ prp, const int *__restrict__ pci,
+                               const double *__restrict__ pva, unsigned long long *__restrict__ keys,
+                               double *__restrict__ vals) {
+  for (long i = (long)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (long)gridDim.x * blockDim.x)
+    for (int k = prp[i]; k < prp[i + 1]; ++k) {
+      keys[k] = (unsigned long long)((long long)pci[k] * n + i);
+      vals[k] = pva[k];
+    }
+}
+// restriction b_c = P^T r, warp per coarse row (lane-strided, xor tree: fixed order)
+__global__ void __launch_bounds__(256) k_sa_restrict(long nc, const int *__restrict__ trp, const int *__restrict__ tci,
+                                                     const double *__restrict__ tva, const double *__restrict__ r,
+                                                     double *__restrict__ bc, const int *gate) {
+  if (!*gate) return;
+  const long a = ((long)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  if (a >= nc) return;
+  const double s = warp_row_dot(trp, tci, tva, r, a);
+  if ((threadIdx.x & 31) == 0) bc[a] = s;
+}
+// prolongation x += P xc (SELL-32)
+__global__ void __launch_bounds__(256) k_sa_prolong_add(long n, Sell P, const double *__restrict__ xc,
+                                                        double *__restrict__ x, const int *gate) {
+  if (!*gate) return;
+  const long i = (long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  x[i] += sell_dot(P, i, GatherX{xc});
+}
+

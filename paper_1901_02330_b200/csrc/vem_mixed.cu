@@ -53,6 +53,12 @@ struct AmgLevel {
   double *b = nullptr, *x = nullptr, *t = nullptr, *y = nullptr, *sr = nullptr, *sd0 = nullptr, *sd1 = nullptr;
   bool owns_matrix = true;
   bool warp_rows = false;                      // coarse levels: long Galerkin rows -> warp per row
+  // smoothed aggregation (level 0): P CSR (setup), P SELL (prolongation), P^T CSR (restriction)
+  bool sa = false;
+  int *prp = nullptr, *pci = nullptr, *ptrp = nullptr, *ptci = nullptr, *psci = nullptr;
+  double *pva = nullptr, *ptva = nullptr, *psva = nullptr;
+  long long *psoff = nullptr;
+  long pnnz = 0;
 };
 
 struct Ctx {
@@ -585,7 +591,8 @@ int run_pcg(Ctx *c, int64_t *inner_its) {
 // Block-Schur-AMG apply (kind 3): z_u = s v_u ./ diag(M), z_p = -V(s v_p)
 // (oracle/amg.py AMG.vcycle, reading R22)
 // ----------------------------------------------------------------------------
-constexpr double AMG_THETA = 0.08, AMG_RATIO = 30.0, AMG_STAGNATION = 0.75;
+constexpr double AMG_THETA = 0.08, AMG_THETA_COARSE = 0.04, AMG_RATIO = 30.0, AMG_STAGNATION = 0.75;
+constexpr int AMG_SA_LEVELS = 1;   // levels with the smoothed prolongator (oracle/amg.py SA_LEVELS)
 constexpr int AMG_COARSE_SIZE = 2048, AMG_MAX_LEVELS = 12, AMG_DEGREE = 3, AMG_COARSE_DEGREE = 8;
 
 void amg_cheb_coeffs(double lmax, int degree, double &inv_theta, std::vector<double> &c1, std::vector<double> &c2) {
@@ -671,12 +678,18 @@ void amg_vcycle(Ctx *c, size_t l, const int *gate) {
   AmgLevel &C = c->amg[l + 1];
   amg_smooth(c, L, L.b, L.x, AMG_DEGREE, gate, l == 0);
   amg_residual(c, L, gate);
-  {
+  if (L.sa) {
+    TimeScope ts(c, VEM_K_PRECOND_VEC, 12.0 * L.pnnz + 8.0 * L.n + 8.0 * C.n);
+    k_sa_restrict<<<grid_for(C.n * 32), NT, 0, c->stream>>>(C.n, L.ptrp, L.ptci, L.ptva, L.t, C.b, gate);
+  } else {
     TimeScope ts(c, VEM_K_PRECOND_VEC, 8.0 * L.n * 2 + 8.0 * C.n);
     k_amg_restrict<<<grid_stream(c, C.n), NT, 0, c->stream>>>(C.n, L.moff, L.mem, L.t, C.b, gate);
   }
   amg_vcycle(c, l + 1, gate);
-  {
+  if (L.sa) {
+    TimeScope ts(c, VEM_K_PRECOND_VEC, 12.0 * L.pnnz + 16.0 * L.n + 8.0 * C.n);
+    k_sa_prolong_add<<<grid_for(L.n), NT, 0, c->stream>>>(L.n, Sell{L.psoff, L.psci, L.psva}, C.x, L.x, gate);
+  } else {
     TimeScope ts(c, VEM_K_PRECOND_VEC, 8.0 * L.n * 3);
     k_amg_prolong_add<<<grid_stream(c, L.n), NT, 0, c->stream>>>(L.n, L.agg, C.x, L.x, gate);
   }
@@ -1310,7 +1323,7 @@ T read_back(Ctx *c, const T *p) {
 }
 
 // aggregates of level L (device agg, returns nc); MIS-2 by repeated distance-2 maxima
-int amg_aggregate(Ctx *c, AmgLevel &L, double *diag, long &nc_out) {
+int amg_aggregate(Ctx *c, AmgLevel &L, double *diag, double theta, long &nc_out) {
   const long n = L.n;
   unsigned char *strong = nullptr;
   signed char *state = nullptr;
@@ -1329,7 +1342,7 @@ int amg_aggregate(Ctx *c, AmgLevel &L, double *diag, long &nc_out) {
   DA(cnt, 1);
   DA(L.agg, n);
   const int g = grid_stream(c, n);
-  k_amg_strong<<<g, NT, 0, c->stream>>>(n, L.rp, L.ci, L.va, diag, AMG_THETA, strong);
+  k_amg_strong<<<g, NT, 0, c->stream>>>(n, L.rp, L.ci, L.va, diag, theta, strong);
   CK(cudaMemsetAsync(state, 0, n, c->stream));
   for (int it = 0; it < 1000; ++it) {
     k_amg_mis_keys<<<g, NT, 0, c->stream>>>(n, state, kv);
@@ -1370,22 +1383,20 @@ int amg_aggregate(Ctx *c, AmgLevel &L, double *diag, long &nc_out) {
   return 0;
 }
 
-// Galerkin A_c = P^T A P (stable radix sort of (agg_i nc + agg_j) keys, in-order run sums)
-int amg_galerkin(Ctx *c, const AmgLevel &L, long nc, AmgLevel &C) {
-  const long m = L.nnz;
-  unsigned long long *k0 = nullptr, *k1 = nullptr;
-  double *v0 = nullptr, *v1 = nullptr;
+// (key, value) pairs with key = row * ncols + col -> CSR (nrows x ncols): stable radix
+// sort, flags at run starts, in-order run sums (deterministic).  k0 / v0 are consumed
+// (freed).  *row_out (optional) receives the row of every stored entry.
+int sort_reduce_csr(Ctx *c, unsigned long long *k0, double *v0, long m, long nrows, long ncols, int **rp_out,
+                    int **ci_out, double **va_out, long *nnz_out, int **row_out = nullptr) {
+  unsigned long long *k1 = nullptr;
+  double *v1 = nullptr;
   int *flag = nullptr, *pos = nullptr, *crow = nullptr, *cnt = nullptr;
-  DA(k0, m);
   DA(k1, m);
-  DA(v0, m);
   DA(v1, m);
   DA(flag, m + 1);
   DA(pos, m + 1);
-  k_amg_expand<<<grid_stream(c, L.n), NT, 0, c->stream>>>(L.n, L.rp, L.ci, L.va, L.agg, nc, k0, v0);
-  CKL();
   int bits = 1;
-  while ((1ULL << bits) < (unsigned long long)nc * (unsigned long long)nc) ++bits;
+  while ((1ULL << bits) < (unsigned long long)nrows * (unsigned long long)ncols) ++bits;
   {
     size_t tb = 0;
     CK(cub::DeviceRadixSort::SortPairs(nullptr, tb, k0, k1, v0, v1, (int)m, 0, bits, c->stream));
@@ -1395,31 +1406,134 @@ int amg_galerkin(Ctx *c, const AmgLevel &L, long nc, AmgLevel &C) {
     CK(cudaStreamSynchronize(c->stream));
     dfree(c, tmp);
   }
+  dfree(c, k0);
+  dfree(c, v0);
   k_amg_run_flags<<<grid_stream(c, m), NT, 0, c->stream>>>(m, k1, flag);
   CK(cudaMemsetAsync(flag + m, 0, sizeof(int), c->stream));
   {
     int r = scan_excl(c, flag, pos, m + 1);
     if (r) return r;
   }
-  const long nnzc = read_back(c, pos + m);
-  C.n = nc;
-  C.nnz = nnzc;
-  DA(crow, nnzc);
-  DA(C.ci, nnzc);
-  DA(C.va, nnzc);
-  DA(C.rp, nc + 1);
-  DA(cnt, nc + 1);
-  k_amg_run_reduce<<<grid_stream(c, m), NT, 0, c->stream>>>(m, k1, v1, flag, pos, nc, crow, C.ci, C.va);
-  CK(cudaMemsetAsync(cnt, 0, (nc + 1) * sizeof(int), c->stream));
-  k_amg_row_count<<<grid_stream(c, nnzc), NT, 0, c->stream>>>(nnzc, crow, cnt);
+  const long nnz = read_back(c, pos + m);
+  DA(crow, nnz);
+  DA(*ci_out, nnz);
+  DA(*va_out, nnz);
+  DA(*rp_out, nrows + 1);
+  DA(cnt, nrows + 1);
+  k_amg_run_reduce<<<grid_stream(c, m), NT, 0, c->stream>>>(m, k1, v1, flag, pos, ncols, crow, *ci_out, *va_out);
+  CK(cudaMemsetAsync(cnt, 0, (nrows + 1) * sizeof(int), c->stream));
+  k_amg_row_count<<<grid_stream(c, nnz), NT, 0, c->stream>>>(nnz, crow, cnt);
   CKL();
   {
-    int r = scan_excl(c, cnt, C.rp, nc + 1);
+    int r = scan_excl(c, cnt, *rp_out, nrows + 1);
     if (r) return r;
   }
-  for (void *p : {(void *)k0, (void *)k1, (void *)v0, (void *)v1, (void *)flag, (void *)pos, (void *)crow,
-                  (void *)cnt})
-    dfree(c, p);
+  for (void *p : {(void *)k1, (void *)v1, (void *)flag, (void *)pos, (void *)cnt}) dfree(c, p);
+  if (row_out)
+    *row_out = crow;
+  else
+    dfree(c, crow);
+  *nnz_out = nnz;
+  return 0;
+}
+
+// Galerkin A_c = T^T A T for the piecewise-constant T (keys agg_i nc + agg_j)
+int amg_galerkin(Ctx *c, const AmgLevel &L, long nc, AmgLevel &C) {
+  const long m = L.nnz;
+  unsigned long long *k0 = nullptr;
+  double *v0 = nullptr;
+  DA(k0, m);
+  DA(v0, m);
+  k_amg_expand<<<grid_stream(c, L.n), NT, 0, c->stream>>>(L.n, L.rp, L.ci, L.va, L.agg, nc, k0, v0);
+  CKL();
+  C.n = nc;
+  return sort_reduce_csr(c, k0, v0, m, nc, nc, &C.rp, &C.ci, &C.va, &C.nnz);
+}
+
+// exclusive scan of per-row 64-bit counts -> offsets, returns the total
+long long scan_counts(Ctx *c, long long *cnt, long long *off, long n) {
+  CK(cudaMemsetAsync(cnt + n, 0, sizeof(long long), c->stream));
+  if (scan_excl(c, cnt, off, n + 1)) return -1;
+  return read_back(c, off + n);
+}
+
+// Smoothed aggregation level (oracle/amg.py smoothed_prolongator, SA_LEVELS = 1):
+// P = T - omega D^-1 (A T), omega = 4 / (3 lmax); A_c = P^T (A P); P^T for the restriction.
+int amg_sa_level(Ctx *c, AmgLevel &L, long nc, AmgLevel &C) {
+  const long n = L.n;
+  // A T
+  {
+    unsigned long long *k0 = nullptr;
+    double *v0 = nullptr;
+    DA(k0, L.nnz);
+    DA(v0, L.nnz);
+    k_sa_expand_at<<<grid_stream(c, n), NT, 0, c->stream>>>(n, L.rp, L.ci, L.va, L.agg, nc, k0, v0);
+    CKL();
+    int *prow = nullptr;
+    int r = sort_reduce_csr(c, k0, v0, L.nnz, n, nc, &L.prp, &L.pci, &L.pva, &L.pnnz, &prow);
+    if (r) return r;
+    const double omega = 4.0 / (3.0 * L.lmax);
+    k_sa_pvals<<<grid_stream(c, L.pnnz), NT, 0, c->stream>>>(L.pnnz, prow, L.pci, L.agg, L.dinv, omega, L.pva);
+    CKL();
+    CK(cudaStreamSynchronize(c->stream));
+    dfree(c, prow);
+  }
+  // Q = A P
+  int *qrp = nullptr, *qci = nullptr;
+  double *qva = nullptr;
+  long qnnz = 0;
+  long long *cnt = nullptr, *off = nullptr;
+  DA(cnt, n + 1);
+  DA(off, n + 1);
+  {
+    k_sa_count_ap<<<grid_stream(c, n), NT, 0, c->stream>>>(n, L.rp, L.ci, L.prp, cnt);
+    CKL();
+    const long long m = scan_counts(c, cnt, off, n);
+    if (m < 0) return VEM_ERR_CUDA;
+    unsigned long long *k0 = nullptr;
+    double *v0 = nullptr;
+    DA(k0, m);
+    DA(v0, m);
+    k_sa_fill_ap<<<grid_stream(c, n), NT, 0, c->stream>>>(n, L.rp, L.ci, L.va, L.prp, L.pci, L.pva, off, nc, k0,
+                                                          v0);
+    CKL();
+    int r = sort_reduce_csr(c, k0, v0, m, n, nc, &qrp, &qci, &qva, &qnnz);
+    if (r) return r;
+  }
+  // A_c = P^T Q
+  {
+    k_sa_count_ptq<<<grid_stream(c, n), NT, 0, c->stream>>>(n, L.prp, qrp, cnt);
+    CKL();
+    const long long m = scan_counts(c, cnt, off, n);
+    if (m < 0) return VEM_ERR_CUDA;
+    unsigned long long *k0 = nullptr;
+    double *v0 = nullptr;
+    DA(k0, m);
+    DA(v0, m);
+    k_sa_fill_ptq<<<grid_stream(c, n), NT, 0, c->stream>>>(n, L.prp, L.pci, L.pva, qrp, qci, qva, off, nc, k0, v0);
+    CKL();
+    C.n = nc;
+    int r = sort_reduce_csr(c, k0, v0, m, nc, nc, &C.rp, &C.ci, &C.va, &C.nnz);
+    if (r) return r;
+  }
+  for (void *p : {(void *)qrp, (void *)qci, (void *)qva, (void *)cnt, (void *)off}) dfree(c, p);
+  // P^T (restriction) and the SELL copy of P (prolongation)
+  {
+    unsigned long long *k0 = nullptr;
+    double *v0 = nullptr;
+    DA(k0, L.pnnz);
+    DA(v0, L.pnnz);
+    k_sa_expand_pt<<<grid_stream(c, n), NT, 0, c->stream>>>(n, L.prp, L.pci, L.pva, k0, v0);
+    CKL();
+    long tn = 0;
+    int r = sort_reduce_csr(c, k0, v0, L.pnnz, nc, n, &L.ptrp, &L.ptci, &L.ptva, &tn);
+    if (r) return r;
+    long ps = 0;
+    r = build_sell(c, n, L.prp, L.pci, L.pva, &L.psoff, &L.psci, &L.psva, &ps);
+    if (r) return r;
+  }
+  L.sa = true;
+  CK(cudaStreamSynchronize(c->stream));
   return 0;
 }
 
@@ -1489,7 +1603,8 @@ int build_amg(Ctx *c) {
     AmgLevel &L = c->amg.back();
     if (L.n <= AMG_COARSE_SIZE || (int)c->amg.size() >= AMG_MAX_LEVELS) break;
     long nc = 0;
-    r = amg_aggregate(c, L, diag, nc);
+    const size_t lev = c->amg.size() - 1;
+    r = amg_aggregate(c, L, diag, lev == 0 ? AMG_THETA : AMG_THETA_COARSE, nc);
     if (r) return r;
     if (nc > AMG_STAGNATION * L.n) {
       dfree(c, L.agg);
@@ -1498,10 +1613,15 @@ int build_amg(Ctx *c) {
     }
     L.nc = nc;
     AmgLevel C;
-    r = amg_galerkin(c, L, nc, C);
-    if (r) return r;
-    r = amg_members(c, c->amg.back());
-    if (r) return r;
+    if ((int)lev < AMG_SA_LEVELS) {
+      r = amg_sa_level(c, c->amg.back(), nc, C);
+      if (r) return r;
+    } else {
+      r = amg_galerkin(c, L, nc, C);
+      if (r) return r;
+      r = amg_members(c, c->amg.back());
+      if (r) return r;
+    }
     // coarse diagonal, Gershgorin bound, SELL copy, vectors
     double *cdiag = nullptr;
     DA(C.dinv, C.n);

@@ -230,6 +230,37 @@ def test_amg_one_level_is_exact_and_vcycle_symmetric():
     assert abs(u @ h.vcycle(v) - v @ h.vcycle(u)) <= 1e-10 * abs(u @ h.vcycle(v))
 
 
+def test_amg_smoothed_prolongator():
+    """Level 0 uses the smoothed-aggregation prolongator P = (I - omega D^-1 S) T
+    (Vanek, Mandel & Brezina 1996).  Pinned by what the construction implies, not by
+    retyping it: P reproduces (I - omega D^-1 S) applied to the constant; damped
+    Jacobi with omega = 4 / (3 lmax) < 2 / lambda_max(D^-1 S) lowers the S-energy of
+    every coarse basis vector; the Galerkin operator is the S form restricted to
+    range(P); the two-grid correction I - P A_c^-1 P^T S is an S-orthogonal projector."""
+    from oracle import amg
+    s, SD = _c3s_sd()
+    h = amg.AMG(SD)
+    lev = h.levels[0]
+    assert lev.P is not None and amg.SA_LEVELS == 1
+    n, nc = SD.shape[0], lev.nc
+    d = SD.diagonal()
+    one = np.ones(n)
+    omega = 4.0 / (3.0 * lev.lmax)
+    assert np.abs(lev.P @ np.ones(nc) - (one - omega * (SD @ one) / d)).max() <= 1e-13
+    T = sp.csr_matrix((np.ones(n), (np.arange(n), lev.agg)), shape=(n, nc))
+    eP = ((lev.P.T @ SD @ lev.P).diagonal())
+    eT = ((T.T @ SD @ T).diagonal())
+    assert np.all(eP <= eT * (1 + 1e-12)) and eP.sum() < 0.9 * eT.sum()
+    Ac = h.levels[1].A
+    xc, yc = RNG.normal(size=nc), RNG.normal(size=nc)
+    assert abs(xc @ (Ac @ yc) - (lev.P @ xc) @ (SD @ (lev.P @ yc))) <= 1e-12 * abs(xc @ (Ac @ yc))
+    Acd = Ac.toarray()
+    E = np.eye(n) - lev.P.toarray() @ np.linalg.solve(Acd, lev.P.T.toarray() @ SD.toarray())
+    assert np.abs(E @ E - E).max() <= 1e-8
+    SE = SD.toarray() @ E
+    assert np.abs(SE - SE.T).max() <= 1e-8 * np.abs(SD.toarray()).max()
+
+
 def test_block_schur_amg_gmres_vs_lu():
     for name in ("C1", "C3s"):
         s = configs.CONFIGS[name].build()
