@@ -452,15 +452,21 @@ __global__ void k_sa_expand_pt(long n, const int *__restrict__ prp, const int *_
       vals[k] = pva[k];
     }
 }
-// restriction b_c = P^T r, warp per coarse row (lane-strided, xor tree: fixed order)
+// restriction b_c = P^T r: 8 lanes per coarse row (rows average ~36 entries),
+// lane-strided then a 3-level xor tree inside the group (fixed order)
 __global__ void __launch_bounds__(256) k_sa_restrict(long nc, const int *__restrict__ trp, const int *__restrict__ tci,
                                                      const double *__restrict__ tva, const double *__restrict__ r,
                                                      double *__restrict__ bc, const int *gate) {
   if (!*gate) return;
-  const long a = ((long)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
-  if (a >= nc) return;
-  const double s = warp_row_dot(trp, tci, tva, r, a);
-  if ((threadIdx.x & 31) == 0) bc[a] = s;
+  const long t = (long)blockIdx.x * blockDim.x + threadIdx.x;
+  const long a = t >> 3;
+  const int g = (int)(t & 7);
+  double acc = 0.0;
+  if (a < nc)
+    for (int k = trp[a] + g; k < trp[a + 1]; k += 8) acc = fma(tva[k], r[tci[k]], acc);
+#pragma unroll
+  for (int o = 4; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+  if (a < nc && g == 0) bc[a] = acc;
 }
 // prolongation x += P xc (SELL-32)
 __global__ void __launch_bounds__(256) k_sa_prolong_add(long n, Sell P, const double *__restrict__ xc,
@@ -471,3 +477,29 @@ __global__ void __launch_bounds__(256) k_sa_prolong_add(long n, Sell P, const do
   x[i] += sell_dot(P, i, GatherX{xc});
 }
 
+// Arnoldi-step form of the Block-Schur-AMG output (kind 3, GMRES): the preconditioned
+// vector z = [s v_u ./ diag(M); -x0] is never written; the saddle SpMV gathers it on
+// the fly (same floating-point operations as k_amg_top / k_amg_add, so w = A z is
+// bitwise the same), and the V-cycle reads b0 = s v_p from k_amg_top_p.
+struct GatherAmgZ {
+  long nu;
+  double s;
+  const double *__restrict__ v, *__restrict__ dMinv, *__restrict__ x0;
+  __device__ __forceinline__ double operator()(int c) const { return c < nu ? s * v[c] * dMinv[c] : -x0[c - nu]; }
+};
+__global__ void __launch_bounds__(256) k_spmv_amgz(long n, long nu, Sell A, const double *__restrict__ v,
+                                                   const double *scale, const double *__restrict__ dMinv,
+                                                   const double *__restrict__ x0, double *__restrict__ y,
+                                                   const int *gate) {
+  if (!*gate) return;
+  const long row = (long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (row >= n) return;
+  y[row] = sell_dot(A, row, GatherAmgZ{nu, *scale, v, dMinv, x0});
+}
+__global__ void k_amg_top_p(long nu, long np, const double *__restrict__ v, const double *scale,
+                            double *__restrict__ b0, const int *gate) {
+  if (!*gate) return;
+  const double s = *scale;
+  for (long i = (long)blockIdx.x * blockDim.x + threadIdx.x; i < np; i += (long)gridDim.x * blockDim.x)
+    b0[i] = s * v[nu + i];
+}

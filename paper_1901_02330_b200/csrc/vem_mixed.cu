@@ -680,7 +680,7 @@ void amg_vcycle(Ctx *c, size_t l, const int *gate) {
   amg_residual(c, L, gate);
   if (L.sa) {
     TimeScope ts(c, VEM_K_PRECOND_VEC, 12.0 * L.pnnz + 8.0 * L.n + 8.0 * C.n);
-    k_sa_restrict<<<grid_for(C.n * 32), NT, 0, c->stream>>>(C.n, L.ptrp, L.ptci, L.ptva, L.t, C.b, gate);
+    k_sa_restrict<<<grid_for(C.n * 8), NT, 0, c->stream>>>(C.n, L.ptrp, L.ptci, L.ptva, L.t, C.b, gate);
   } else {
     TimeScope ts(c, VEM_K_PRECOND_VEC, 8.0 * L.n * 2 + 8.0 * C.n);
     k_amg_restrict<<<grid_stream(c, C.n), NT, 0, c->stream>>>(C.n, L.moff, L.mem, L.t, C.b, gate);
@@ -697,14 +697,23 @@ void amg_vcycle(Ctx *c, size_t l, const int *gate) {
   amg_smooth(c, L, L.t, L.x, AMG_DEGREE, gate, false, 1);   // x += C(b - A x)
 }
 
-int enqueue_block_schur_amg(Ctx *c, const double *v, const double *scale, double *z, const int *gate) {
+// z_out = false: only the V-cycle runs (x0 = V(s v_p)); k_spmv_amgz forms z on the fly
+int enqueue_block_schur_amg(Ctx *c, const double *v, const double *scale, double *z, const int *gate,
+                            bool z_out = true) {
   if (c->amg.empty()) return fail(c, VEM_ERR_PRECOND, "Block-Schur-AMG needs n_p_dof = 1 (k = 0)");
   AmgLevel &L0 = c->amg[0];
-  {
+  if (z_out) {
     TimeScope ts(c, VEM_K_PRECOND_VEC, 8.0 * (3 * c->nu + 2 * c->np));
     k_amg_top<<<grid_stream(c, c->n), NT, 0, c->stream>>>(c->nu, c->np, v, scale, c->dMinv, z, L0.b, gate);
+  } else {
+    TimeScope ts(c, VEM_K_PRECOND_VEC, 16.0 * c->np);
+    k_amg_top_p<<<grid_stream(c, c->np), NT, 0, c->stream>>>(c->nu, c->np, v, scale, L0.b, gate);
   }
   amg_vcycle(c, 0, gate);
+  if (!z_out) {
+    CKL();
+    return 0;
+  }
   {
     TimeScope ts(c, VEM_K_PRECOND_VEC, 24.0 * c->np);
     k_amg_add<<<grid_stream(c, c->np), NT, 0, c->stream>>>(c->np, L0.x, nullptr, -1.0, z + c->nu, gate);
@@ -744,10 +753,17 @@ int enqueue_arnoldi_step(Ctx *c, int kind, int j, int64_t *inner_its) {
   double *w = c->V + (size_t)(j + 1) * c->ldv;
   double *zj = flex ? c->Z + (size_t)j * c->ldv : c->z;
   c->sample_slot = j;
-  int rc = enqueue_precond(c, kind, Vj, &c->st->vscale[j], zj, gate_active(c), inner_its);
-  c->sample_slot = -1;
-  if (rc) return rc;
-  {
+  if (kind == VEM_PRECOND_BLOCK_SCHUR_AMG) {   // z = P^-1 v_j formed inside the SpMV gather
+    int rc = enqueue_block_schur_amg(c, Vj, &c->st->vscale[j], nullptr, gate_active(c), false);
+    c->sample_slot = -1;
+    if (rc) return rc;
+    TimeScope ts(c, VEM_K_SPMV, bytes_spmv(c) + 8.0 * c->nu);
+    k_spmv_amgz<<<grid_for(c->n), NT, 0, c->stream>>>(c->n, c->nu, sellA(c), Vj, &c->st->vscale[j], c->dMinv,
+                                                      c->amg[0].x, w, gate_active(c));
+  } else {
+    int rc = enqueue_precond(c, kind, Vj, &c->st->vscale[j], zj, gate_active(c), inner_its);
+    c->sample_slot = -1;
+    if (rc) return rc;
     TimeScope ts(c, VEM_K_SPMV, bytes_spmv(c));
     launch_spmv(c, 0L, c->n, (const double *)zj, w, nullptr, 0, gate_active(c));
   }
