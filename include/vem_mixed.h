@@ -202,6 +202,54 @@ int vem_mixed_kernel_stats(vem_ctx *ctx, vem_kernel_stats *stats, int32_t reset)
  * nonzeros; VEM_ERR_INVALID if the level does not exist. */
 int vem_mixed_amg_level(vem_ctx *ctx, int32_t level, int64_t *n, int64_t *nnz);
 
+/* ---------------------------------------------------------------------------
+ * Element-parallel assembly on the device
+ * for classes of congruent cells (translates of one cell: cube grids, cube pairs),
+ * from each class's shape cache (host, vemgen.assemble.class_template).  Cell e of a
+ * class contributes
+ *   M[dof[e][ti[t]], dof[e][tj[t]]] += ((coef[e][0] tA[t] + coef[e][1] tA[n_t + t])
+ *                                       + coef[e][2] tA[2 n_t + t]) + coef[e][3] tS[t]
+ *   B[pdof[e][bi[t]], dof[e][bj[t]]] += tB[t]
+ *   f[pdof[e][a]] = -vol[e] sum_b Hinv[a][b] F[e][b]
+ * coef = (1/K_x, 1/K_y, 1/K_z, s_P) per cell (readings R4, R7); every product is
+ * rounded separately (no FMA); duplicates are summed in (class, cell, entry) order.
+ * All pointers are HOST arrays, copied during the call; row-major. */
+typedef struct {
+  int64_t n_cells;
+  int32_t n_loc, n_p;          /* local velocity DOFs, pressure DOFs per cell          */
+  const int32_t *dof;          /* n_cells x n_loc global velocity DOFs                 */
+  const int32_t *pdof;         /* n_cells x n_p global pressure DOFs                    */
+  int32_t n_t;                 /* M template entries                                    */
+  const int32_t *ti, *tj;      /* n_t local (row, col)                                  */
+  const double *tA;            /* 3 x n_t consistency components (K-independent)        */
+  const double *tS;            /* n_t stabilisation                                     */
+  const double *coef;          /* n_cells x 4                                           */
+  int32_t n_b;                 /* B template entries                                    */
+  const int32_t *bi, *bj;      /* n_b local (pressure row, velocity col)                */
+  const double *tB;            /* n_b                                                   */
+  const double *Hinv;          /* n_p x n_p inverse monomial mass (scaled coordinates)  */
+  const double *F;             /* n_cells x n_p source moments int_P f m_a              */
+  const double *vol;           /* n_cells                                               */
+} vem_cell_class;
+
+typedef struct vem_asm vem_asm;  /* opaque: device CSR of M (n_u x n_u), B (n_p x n_u), device f */
+
+/* Assemble on the device (stream semantics as vem_mixed_upload; synchronised before
+ * return).  Errors: VEM_ERR_INVALID (NULL pointer, DOF out of range, empty class),
+ * VEM_ERR_CUDA.  On success *out owns the device arrays. */
+int vem_mixed_assemble(vem_asm **out, const vem_cell_class *classes, int32_t n_classes, int64_t n_u,
+                       int64_t n_p, void *cuda_stream);
+/* nnz of the assembled M and B. */
+int vem_mixed_assembled_info(const vem_asm *a, int64_t *nnz_M, int64_t *nnz_B);
+/* Copy the assembled CSR (int64 indptr, int32 indices, fp64 values; sorted, unique
+ * columns) and f to caller-allocated HOST arrays sized from vem_mixed_assembled_info. */
+int vem_mixed_assembled_copy(const vem_asm *a, int64_t *m_indptr, int32_t *m_indices, double *m_values,
+                             int64_t *b_indptr, int32_t *b_indices, double *b_values, double *f);
+/* vem_mixed_upload from an assembled system (device to device; `a` may be freed after). */
+int vem_mixed_upload_assembled(vem_ctx **ctx, const vem_asm *a, const vem_csr *W, double eps,
+                               const vem_layout *layout, const vem_opts *opts, void *cuda_stream);
+void vem_mixed_assembled_free(vem_asm *a);
+
 void vem_mixed_destroy(vem_ctx *ctx);
 const char *vem_status_string(int status);
 const char *vem_last_error(vem_ctx *ctx);

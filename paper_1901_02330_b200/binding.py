@@ -66,6 +66,17 @@ class vem_info(C.Structure):
         return {f: getattr(self, f) for f, _ in self._fields_}
 
 
+_PI = C.POINTER(C.c_int32)
+_PD = C.POINTER(C.c_double)
+
+
+class vem_cell_class(C.Structure):
+    _fields_ = [("n_cells", C.c_int64), ("n_loc", C.c_int32), ("n_p", C.c_int32), ("dof", _PI), ("pdof", _PI),
+                ("n_t", C.c_int32), ("ti", _PI), ("tj", _PI), ("tA", _PD), ("tS", _PD), ("coef", _PD),
+                ("n_b", C.c_int32), ("bi", _PI), ("bj", _PI), ("tB", _PD), ("Hinv", _PD), ("F", _PD),
+                ("vol", _PD)]
+
+
 class vem_kernel_stats(C.Structure):
     _fields_ = [("launches", C.c_int64 * 8), ("ms", C.c_double * 8), ("bytes", C.c_double * 8)]
 
@@ -75,6 +86,8 @@ class vem_kernel_stats(C.Structure):
 
 
 EXPORTS = ["vem_mixed_default_options", "vem_mixed_upload", "vem_mixed_solve", "vem_mixed_solve_host",
+           "vem_mixed_assemble", "vem_mixed_assembled_info", "vem_mixed_assembled_copy",
+           "vem_mixed_upload_assembled", "vem_mixed_assembled_free",
            "vem_mixed_spmv", "vem_mixed_schur_spmv", "vem_mixed_precond_apply", "vem_mixed_set_options",
            "vem_mixed_get_options", "vem_mixed_get_info", "vem_mixed_get_schur", "vem_mixed_kernel_stats",
            "vem_mixed_amg_level", "vem_mixed_destroy", "vem_status_string", "vem_last_error"]
@@ -108,6 +121,14 @@ def load_library(path: str = LIB_PATH):
     lib.vem_mixed_get_schur.argtypes = [P, C.POINTER(C.c_int64), C.POINTER(C.c_int32), D]
     lib.vem_mixed_kernel_stats.argtypes = [P, C.POINTER(vem_kernel_stats), C.c_int32]
     lib.vem_mixed_amg_level.argtypes = [P, C.c_int32, C.POINTER(C.c_int64), C.POINTER(C.c_int64)]
+    lib.vem_mixed_assemble.argtypes = [C.POINTER(P), C.POINTER(vem_cell_class), C.c_int32, C.c_int64, C.c_int64, P]
+    lib.vem_mixed_assembled_info.argtypes = [P, C.POINTER(C.c_int64), C.POINTER(C.c_int64)]
+    lib.vem_mixed_assembled_copy.argtypes = [P, C.POINTER(C.c_int64), C.POINTER(C.c_int32), D,
+                                             C.POINTER(C.c_int64), C.POINTER(C.c_int32), D, D]
+    lib.vem_mixed_upload_assembled.argtypes = [C.POINTER(P), P, C.POINTER(vem_csr), C.c_double,
+                                               C.POINTER(vem_layout), C.POINTER(vem_opts), P]
+    lib.vem_mixed_assembled_free.argtypes = [P]
+    lib.vem_mixed_assembled_free.restype = None
     lib.vem_mixed_destroy.argtypes = [P]
     lib.vem_mixed_destroy.restype = None
     lib.vem_status_string.argtypes = [C.c_int]
@@ -190,6 +211,35 @@ class VemMixed:
                            f"{self._lib.vem_last_error(None).decode()}")
         self.n_u, self.n_p = M.shape[0], B.shape[0]
         self.n = self.n_u + self.n_p
+
+    @classmethod
+    def from_assembled(cls, asm, W=None, eps: float = 0.0, layout=None, opts: vem_opts | None = None,
+                       stream=None):
+        """vem_mixed_upload_assembled: the solver from a device-assembled system."""
+        import torch
+        self = cls.__new__(cls)
+        self._lib = load_library()
+        self._stream = stream if stream is not None else torch.cuda.current_stream()
+        ws, keep_w = (None, None)
+        if W is not None:
+            ws, keep_w = _csr_struct(W)
+        lay = None
+        if layout is not None:
+            lay = vem_layout(layout.k, layout.n_face_dof, layout.n_int_dof, layout.n_p_dof,
+                             layout.n_faces, layout.n_elems)
+        self._h = C.c_void_p()
+        rc = self._lib.vem_mixed_upload_assembled(C.byref(self._h), asm._h,
+                                                  C.byref(ws) if ws is not None else None, float(eps),
+                                                  C.byref(lay) if lay is not None else None,
+                                                  C.byref(opts) if opts is not None else None,
+                                                  C.c_void_p(self._stream.cuda_stream))
+        if rc != 0:
+            self._h = None
+            raise VemError(f"vem_mixed_upload_assembled: {STATUS.get(rc, rc)}: "
+                           f"{self._lib.vem_last_error(None).decode()}")
+        self.n_u, self.n_p = asm.n_u, asm.n_p
+        self.n = self.n_u + self.n_p
+        return self
 
     # -- helpers ---------------------------------------------------------
     def _check(self, rc, what, allow=(0,)):
@@ -304,3 +354,76 @@ class VemMixed:
         s = vem_kernel_stats()
         self._check(self._lib.vem_mixed_kernel_stats(self._h, C.byref(s), 1 if reset else 0), "kernel_stats")
         return s.as_dict()
+
+
+class Assembled:
+    """vem_mixed_assemble: element-parallel device assembly of M, B and f from the
+    per-class shape caches (vemgen.assemble.class_templates); marshalling only."""
+
+    def __init__(self, templates, n_u: int, n_p: int, stream=None):
+        import torch
+        self._lib = load_library()
+        if not torch.cuda.is_available():
+            raise VemError("no CUDA device: the VEM assembly has no CPU path")
+        stream = stream if stream is not None else torch.cuda.current_stream()
+        self._keep = []
+        arr = (vem_cell_class * len(templates))()
+
+        def i32(a):
+            a = np.ascontiguousarray(a, dtype=np.int32)
+            self._keep.append(a)
+            return a.ctypes.data_as(_PI)
+
+        def f64(a):
+            a = np.ascontiguousarray(a, dtype=np.float64)
+            self._keep.append(a)
+            return a.ctypes.data_as(_PD)
+
+        for q, t in enumerate(templates):
+            E, nloc = t["L"].shape
+            nk = t["P"].shape[1]
+            arr[q] = vem_cell_class(E, nloc, nk, i32(t["L"]), i32(t["P"]), len(t["ii"]), i32(t["ii"]),
+                                    i32(t["jj"]), f64(t["A"]), f64(t["S"]), f64(t["coef"]), len(t["bi"]),
+                                    i32(t["bi"]), i32(t["bj"]), f64(t["B"]), f64(t["Hinv"]), f64(t["F"]),
+                                    f64(t["vol"]))
+        self._h = C.c_void_p()
+        rc = self._lib.vem_mixed_assemble(C.byref(self._h), arr, len(templates), int(n_u), int(n_p),
+                                          C.c_void_p(stream.cuda_stream))
+        self._keep = []
+        if rc != 0:
+            self._h = None
+            raise VemError(f"vem_mixed_assemble: {STATUS.get(rc, rc)}: {self._lib.vem_last_error(None).decode()}")
+        self.n_u, self.n_p = int(n_u), int(n_p)
+
+    def nnz(self):
+        m, b = C.c_int64(), C.c_int64()
+        self._lib.vem_mixed_assembled_info(self._h, C.byref(m), C.byref(b))
+        return m.value, b.value
+
+    def to_host(self):
+        """(M, B, f) as scipy CSR / numpy, copied back from the device."""
+        import scipy.sparse as sp
+        nm, nb = self.nnz()
+        mrp, mci, mva = np.empty(self.n_u + 1, np.int64), np.empty(nm, np.int32), np.empty(nm)
+        brp, bci, bva = np.empty(self.n_p + 1, np.int64), np.empty(nb, np.int32), np.empty(nb)
+        f = np.empty(self.n_p)
+        rc = self._lib.vem_mixed_assembled_copy(
+            self._h, mrp.ctypes.data_as(C.POINTER(C.c_int64)), mci.ctypes.data_as(_PI), mva.ctypes.data_as(_PD),
+            brp.ctypes.data_as(C.POINTER(C.c_int64)), bci.ctypes.data_as(_PI), bva.ctypes.data_as(_PD),
+            f.ctypes.data_as(_PD))
+        if rc != 0:
+            raise VemError(f"vem_mixed_assembled_copy: {STATUS.get(rc, rc)}")
+        M = sp.csr_matrix((mva, mci, mrp), shape=(self.n_u, self.n_u))
+        B = sp.csr_matrix((bva, bci, brp), shape=(self.n_p, self.n_u))
+        return M, B, f
+
+    def close(self):
+        if getattr(self, "_h", None):
+            self._lib.vem_mixed_assembled_free(self._h)
+            self._h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass

@@ -26,6 +26,7 @@
 #include "../../include/vem_mixed.h"
 #include "kernels.cuh"
 #include "amg.cuh"
+#include "assembly.cuh"
 
 namespace {
 
@@ -157,6 +158,11 @@ int fail(Ctx *c, int code, const char *fmt, ...) {
                   __FILE__, __LINE__);                                                        \
   } while (0)
 
+// status-only check for extern "C" helpers without a context in scope
+#define CK_RET(call)                       \
+  do {                                     \
+    if ((call) != cudaSuccess) return VEM_ERR_CUDA; \
+  } while (0)
 #define CKL()                                                                                 \
   do {                                                                                        \
     cudaError_t e_ = cudaGetLastError();                                                      \
@@ -1687,7 +1693,17 @@ int build_amg(Ctx *c) {
   return 0;
 }
 
-int upload_impl(Ctx *c, const vem_csr *M, const vem_csr *B, const vem_csr *W, double eps, const vem_layout *lay) {
+// device CSR produced by vem_mixed_assemble (int64 row pointers, like vem_csr)
+struct DevCsr {
+  long nrows = 0, ncols = 0, nnz = 0;
+  int64_t *rp = nullptr;
+  int *ci = nullptr;
+  double *va = nullptr;
+};
+
+// M, B: host CSR (copied), or dM, dB: device CSR from vem_mixed_assemble (read, not owned)
+int upload_impl(Ctx *c, const vem_csr *M, const vem_csr *B, const vem_csr *W, double eps, const vem_layout *lay,
+                const DevCsr *dM = nullptr, const DevCsr *dB = nullptr) {
   auto t0 = std::chrono::steady_clock::now();
   const bool trace = getenv("VEM_SETUP_TRACE") != nullptr;
   c->pcg_split = getenv("VEM_PCG_SPLIT") ? atoi(getenv("VEM_PCG_SPLIT")) : 1;
@@ -1697,15 +1713,20 @@ int upload_impl(Ctx *c, const vem_csr *M, const vem_csr *B, const vem_csr *W, do
     fprintf(stderr, "[vem setup] %-28s %9.1f ms\n", what,
             std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count());
   };
-  if (!M || !B) return fail(c, VEM_ERR_INVALID, "M and B are required");
-  c->nu = M->n_rows;
-  c->np = B->n_rows;
+  const bool dev_in = dM && dB;
+  if (!dev_in && (!M || !B)) return fail(c, VEM_ERR_INVALID, "M and B are required");
+  c->nu = dev_in ? dM->nrows : M->n_rows;
+  c->np = dev_in ? dB->nrows : B->n_rows;
   c->n = c->nu + c->np;
   if (c->nu <= 0 || c->np <= 0) return fail(c, VEM_ERR_INVALID, "empty system");
   if (c->n >= (1L << 31)) return fail(c, VEM_ERR_INVALID, "n exceeds int32 indexing");
   int r;
-  if ((r = check_csr(c, M, c->nu, c->nu, "M"))) return r;
-  if ((r = check_csr(c, B, c->np, c->nu, "B"))) return r;
+  if (dev_in) {   // assembled on the device: sorted, unique and in range by construction
+    if (dM->ncols != c->nu || dB->ncols != c->nu) return fail(c, VEM_ERR_INVALID, "assembled shapes disagree");
+  } else {
+    if ((r = check_csr(c, M, c->nu, c->nu, "M"))) return r;
+    if ((r = check_csr(c, B, c->np, c->nu, "B"))) return r;
+  }
   if (lay) {
     c->layout = *lay;
     c->nb = std::max(1, (int)lay->n_p_dof);
@@ -1714,9 +1735,9 @@ int upload_impl(Ctx *c, const vem_csr *M, const vem_csr *B, const vem_csr *W, do
     const long np = (long)lay->n_elems * lay->n_p_dof;
     if (nu != c->nu || np != c->np) return fail(c, VEM_ERR_INVALID, "layout does not match M/B sizes");
   }
-  c->nnzM = M->nnz;
-  c->nnzB = B->nnz;
-  c->nnzA = M->nnz + 2 * B->nnz;
+  c->nnzM = dev_in ? dM->nnz : M->nnz;
+  c->nnzB = dev_in ? dB->nnz : B->nnz;
+  c->nnzA = c->nnzM + 2 * c->nnzB;
   if (c->nnzA >= (1L << 31)) return fail(c, VEM_ERR_INVALID, "nnz(A) exceeds int32 indexing");
   if (W) {
     if ((r = check_csr(c, W, c->np, c->np, "W"))) return r;
@@ -1735,12 +1756,21 @@ int upload_impl(Ctx *c, const vem_csr *M, const vem_csr *B, const vem_csr *W, do
   int64_t *mrp = nullptr, *brp = nullptr;
   int *mci = nullptr, *bci = nullptr;
   double *mva = nullptr, *bva = nullptr;
-  if ((r = upload_array(c, &mrp, M->indptr, c->nu + 1))) return r;
-  if ((r = upload_array(c, &mci, M->indices, M->nnz))) return r;
-  if ((r = upload_array(c, &mva, M->values, M->nnz))) return r;
-  if ((r = upload_array(c, &brp, B->indptr, c->np + 1))) return r;
-  if ((r = upload_array(c, &bci, B->indices, B->nnz))) return r;
-  if ((r = upload_array(c, &bva, B->values, B->nnz))) return r;
+  if (dev_in) {
+    mrp = dM->rp;
+    mci = dM->ci;
+    mva = dM->va;
+    brp = dB->rp;
+    bci = dB->ci;
+    bva = dB->va;
+  } else {
+    if ((r = upload_array(c, &mrp, M->indptr, c->nu + 1))) return r;
+    if ((r = upload_array(c, &mci, M->indices, M->nnz))) return r;
+    if ((r = upload_array(c, &mva, M->values, M->nnz))) return r;
+    if ((r = upload_array(c, &brp, B->indptr, c->np + 1))) return r;
+    if ((r = upload_array(c, &bci, B->indices, B->nnz))) return r;
+    if ((r = upload_array(c, &bva, B->values, B->nnz))) return r;
+  }
   if (W) {
     std::vector<double> wd(c->np);
     for (long i = 0; i < c->np; ++i) wd[i] = W->values[W->indptr[i]];
@@ -1753,10 +1783,10 @@ int upload_impl(Ctx *c, const vem_csr *M, const vem_csr *B, const vem_csr *W, do
   double *btva = nullptr;
   DA(btrp, c->nu + 1);
   DA(fill, c->nu + 1);
-  DA(btci, B->nnz);
-  DA(btva, B->nnz);
+  DA(btci, c->nnzB);
+  DA(btva, c->nnzB);
   CK(cudaMemsetAsync(fill, 0, (c->nu + 1) * sizeof(int), c->stream));
-  k_count_cols<<<grid_stream(c, B->nnz), NT, 0, c->stream>>>(B->nnz, bci, fill);
+  k_count_cols<<<grid_stream(c, c->nnzB), NT, 0, c->stream>>>(c->nnzB, bci, fill);
   CKL();
   {
     size_t tb = 0;
@@ -1909,9 +1939,9 @@ int upload_impl(Ctx *c, const vem_csr *M, const vem_csr *B, const vem_csr *W, do
   c->a_rp = nullptr;
   c->a_ci = nullptr;
   c->a_va = nullptr;
-  for (void *p : {(void *)mrp, (void *)mci, (void *)mva, (void *)brp, (void *)bci, (void *)bva, (void *)btrp,
-                  (void *)btci, (void *)btva, (void *)fill, (void *)brp32, (void *)len})
-    dfree(c, p);
+  if (!dev_in)
+    for (void *p : {(void *)mrp, (void *)mci, (void *)mva, (void *)brp, (void *)bci, (void *)bva}) dfree(c, p);
+  for (void *p : {(void *)btrp, (void *)btci, (void *)btva, (void *)fill, (void *)brp32, (void *)len}) dfree(c, p);
   c->setup_ms = std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count();
   phase("done");
   return 0;
@@ -1945,10 +1975,108 @@ int leave(Ctx *c, int rc) {
   return rc;
 }
 
+// ----------------------------------------------------------------------------
+// element-parallel assembly (vem_mixed_assemble, assembly.cuh)
+// ----------------------------------------------------------------------------
+int assemble_impl(Ctx *c, const vem_cell_class *cls, int ncls, long nu, long np, DevCsr &M, DevCsr &B,
+                  double **f) {
+  if (!cls || ncls <= 0 || nu <= 0 || np <= 0) return fail(c, VEM_ERR_INVALID, "empty assembly input");
+  if (nu + np >= (1L << 31)) return fail(c, VEM_ERR_INVALID, "n exceeds int32 indexing");
+  long mM = 0, mB = 0;
+  for (int q = 0; q < ncls; ++q) {
+    const vem_cell_class &k = cls[q];
+    if (k.n_cells <= 0 || k.n_loc <= 0 || k.n_p <= 0 || k.n_t <= 0 || k.n_b <= 0 || !k.dof || !k.pdof || !k.ti ||
+        !k.tj || !k.tA || !k.tS || !k.coef || !k.bi || !k.bj || !k.tB || !k.Hinv || !k.F || !k.vol)
+      return fail(c, VEM_ERR_INVALID, "class %d: NULL pointer or empty size", q);
+    for (long i = 0; i < k.n_cells * (long)k.n_loc; ++i)
+      if (k.dof[i] < 0 || k.dof[i] >= nu) return fail(c, VEM_ERR_INVALID, "class %d: velocity DOF out of range", q);
+    for (long i = 0; i < k.n_cells * (long)k.n_p; ++i)
+      if (k.pdof[i] < 0 || k.pdof[i] >= np) return fail(c, VEM_ERR_INVALID, "class %d: pressure DOF out of range", q);
+    for (int t = 0; t < k.n_t; ++t)
+      if (k.ti[t] < 0 || k.ti[t] >= k.n_loc || k.tj[t] < 0 || k.tj[t] >= k.n_loc)
+        return fail(c, VEM_ERR_INVALID, "class %d: template index out of range", q);
+    for (int t = 0; t < k.n_b; ++t)
+      if (k.bi[t] < 0 || k.bi[t] >= k.n_p || k.bj[t] < 0 || k.bj[t] >= k.n_loc)
+        return fail(c, VEM_ERR_INVALID, "class %d: B template index out of range", q);
+    mM += k.n_cells * (long)k.n_t;
+    mB += k.n_cells * (long)k.n_b;
+  }
+  if (mM >= (1L << 31) || mB >= (1L << 31)) return fail(c, VEM_ERR_INVALID, "too many local entries");
+  cudaDeviceProp prop;
+  int dev = 0;
+  CK(cudaGetDevice(&dev));
+  CK(cudaGetDeviceProperties(&prop, dev));
+  c->sm_count = prop.multiProcessorCount;
+  unsigned long long *kM = nullptr, *kB = nullptr;
+  double *vM = nullptr, *vB = nullptr;
+  DA(kM, mM);
+  DA(vM, mM);
+  DA(kB, mB);
+  DA(vB, mB);
+  DA(*f, np);
+  CK(cudaMemsetAsync(*f, 0, np * sizeof(double), c->stream));
+  long oM = 0, oB = 0;
+  for (int q = 0; q < ncls; ++q) {
+    const vem_cell_class &k = cls[q];
+    const long ne = k.n_cells;
+    int *dof = nullptr, *pdof = nullptr, *ti = nullptr, *tj = nullptr, *bi = nullptr, *bj = nullptr;
+    double *tA = nullptr, *tS = nullptr, *coef = nullptr, *tB = nullptr, *Hinv = nullptr, *F = nullptr, *vol = nullptr;
+    int r;
+    if ((r = upload_array(c, &dof, k.dof, ne * k.n_loc))) return r;
+    if ((r = upload_array(c, &pdof, k.pdof, ne * k.n_p))) return r;
+    if ((r = upload_array(c, &ti, k.ti, k.n_t))) return r;
+    if ((r = upload_array(c, &tj, k.tj, k.n_t))) return r;
+    if ((r = upload_array(c, &tA, k.tA, 3L * k.n_t))) return r;
+    if ((r = upload_array(c, &tS, k.tS, k.n_t))) return r;
+    if ((r = upload_array(c, &coef, k.coef, 4 * ne))) return r;
+    if ((r = upload_array(c, &bi, k.bi, k.n_b))) return r;
+    if ((r = upload_array(c, &bj, k.bj, k.n_b))) return r;
+    if ((r = upload_array(c, &tB, k.tB, k.n_b))) return r;
+    if ((r = upload_array(c, &Hinv, k.Hinv, (long)k.n_p * k.n_p))) return r;
+    if ((r = upload_array(c, &F, k.F, ne * k.n_p))) return r;
+    if ((r = upload_array(c, &vol, k.vol, ne))) return r;
+    k_asm_m<<<grid_stream(c, ne * k.n_t), NT, 0, c->stream>>>(ne, k.n_loc, k.n_t, dof, ti, tj, tA, tS, coef, nu,
+                                                             kM + oM, vM + oM);
+    k_asm_b<<<grid_stream(c, ne * k.n_b), NT, 0, c->stream>>>(ne, k.n_loc, k.n_p, k.n_b, dof, pdof, bi, bj, tB, nu,
+                                                             kB + oB, vB + oB);
+    k_asm_f<<<grid_stream(c, ne * k.n_p), NT, 0, c->stream>>>(ne, k.n_p, pdof, Hinv, F, vol, *f);
+    CKL();
+    CK(cudaStreamSynchronize(c->stream));
+    for (void *p : {(void *)dof, (void *)pdof, (void *)ti, (void *)tj, (void *)tA, (void *)tS, (void *)coef,
+                    (void *)bi, (void *)bj, (void *)tB, (void *)Hinv, (void *)F, (void *)vol})
+      dfree(c, p);
+    oM += ne * k.n_t;
+    oB += ne * k.n_b;
+  }
+  int *rp32 = nullptr;
+  int r = sort_reduce_csr(c, kM, vM, mM, nu, nu, &rp32, &M.ci, &M.va, &M.nnz);
+  if (r) return r;
+  DA(M.rp, nu + 1);
+  k_widen64<<<grid_stream(c, nu + 1), NT, 0, c->stream>>>(nu + 1, rp32, M.rp);
+  CK(cudaStreamSynchronize(c->stream));
+  dfree(c, rp32);
+  M.nrows = nu;
+  M.ncols = nu;
+  r = sort_reduce_csr(c, kB, vB, mB, np, nu, &rp32, &B.ci, &B.va, &B.nnz);
+  if (r) return r;
+  DA(B.rp, np + 1);
+  k_widen64<<<grid_stream(c, np + 1), NT, 0, c->stream>>>(np + 1, rp32, B.rp);
+  CK(cudaStreamSynchronize(c->stream));
+  dfree(c, rp32);
+  B.nrows = np;
+  B.ncols = nu;
+  return 0;
+}
+
 }  // namespace
 
 struct vem_ctx {
   Ctx *impl;
+};
+struct vem_asm {
+  Ctx *impl;   // allocations + stream
+  DevCsr M, B;
+  double *f = nullptr;
 };
 
 static thread_local std::string g_last_err;
@@ -1980,18 +2108,15 @@ static int validate_opts(Ctx *c, const vem_opts *o) {
   return 0;
 }
 
-int vem_mixed_upload(vem_ctx **out, const vem_csr *M, const vem_csr *B, const vem_csr *W, double eps,
-                     const vem_layout *layout, const vem_opts *opts, void *stream) {
-  if (!out) return VEM_ERR_INVALID;
-  *out = nullptr;
+static Ctx *new_ctx(const vem_opts *opts, void *stream, int *rc) {
   Ctx *c = new Ctx();
   vem_mixed_default_options(&c->opts);
+  *rc = 0;
   if (opts) {
     int r = validate_opts(c, opts);
     if (r) {
-      g_last_err = c->err;
-      destroy_ctx(c);
-      return r;
+      *rc = r;
+      return c;
     }
     c->opts = *opts;
   }
@@ -1999,13 +2124,22 @@ int vem_mixed_upload(vem_ctx **out, const vem_csr *M, const vem_csr *B, const ve
   if (cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking) != cudaSuccess ||
       cudaEventCreateWithFlags(&c->ev_in, cudaEventDisableTiming) != cudaSuccess ||
       cudaEventCreateWithFlags(&c->ev_out, cudaEventDisableTiming) != cudaSuccess) {
-    g_last_err = "failed to create the library stream (no CUDA device?)";
-    destroy_ctx(c);
-    return VEM_ERR_CUDA;
+    c->err = "failed to create the library stream (no CUDA device?)";
+    *rc = VEM_ERR_CUDA;
   }
-  int r = enter(c);
-  if (!r) r = upload_impl(c, M, B, W, eps, layout);
-  leave(c, r);
+  return c;
+}
+
+static int upload_common(vem_ctx **out, const vem_csr *M, const vem_csr *B, const vem_csr *W, double eps,
+                         const vem_layout *layout, const vem_opts *opts, void *stream, const DevCsr *dM,
+                         const DevCsr *dB) {
+  if (!out) return VEM_ERR_INVALID;
+  *out = nullptr;
+  int r = 0;
+  Ctx *c = new_ctx(opts, stream, &r);
+  if (!r) r = enter(c);
+  if (!r) r = upload_impl(c, M, B, W, eps, layout, dM, dB);
+  if (c->stream) leave(c, r);
   if (r) {
     g_last_err = c->err;
     destroy_ctx(c);
@@ -2014,6 +2148,67 @@ int vem_mixed_upload(vem_ctx **out, const vem_csr *M, const vem_csr *B, const ve
   vem_ctx *h = new vem_ctx{c};
   *out = h;
   return VEM_OK;
+}
+
+int vem_mixed_upload(vem_ctx **out, const vem_csr *M, const vem_csr *B, const vem_csr *W, double eps,
+                     const vem_layout *layout, const vem_opts *opts, void *stream) {
+  return upload_common(out, M, B, W, eps, layout, opts, stream, nullptr, nullptr);
+}
+
+int vem_mixed_upload_assembled(vem_ctx **out, const vem_asm *a, const vem_csr *W, double eps,
+                               const vem_layout *layout, const vem_opts *opts, void *stream) {
+  if (!a) return VEM_ERR_INVALID;
+  CK_RET(cudaStreamSynchronize(a->impl->stream));
+  return upload_common(out, nullptr, nullptr, W, eps, layout, opts, stream, &a->M, &a->B);
+}
+
+int vem_mixed_assemble(vem_asm **out, const vem_cell_class *classes, int32_t n_classes, int64_t n_u, int64_t n_p,
+                       void *stream) {
+  if (!out) return VEM_ERR_INVALID;
+  *out = nullptr;
+  int r = 0;
+  Ctx *c = new_ctx(nullptr, stream, &r);
+  vem_asm *a = new vem_asm();
+  a->impl = c;
+  if (!r) r = enter(c);
+  if (!r) r = assemble_impl(c, classes, n_classes, n_u, n_p, a->M, a->B, &a->f);
+  if (c->stream) leave(c, r);
+  if (r) {
+    g_last_err = c->err;
+    destroy_ctx(c);
+    delete a;
+    return r;
+  }
+  *out = a;
+  return VEM_OK;
+}
+
+int vem_mixed_assembled_info(const vem_asm *a, int64_t *nnz_M, int64_t *nnz_B) {
+  if (!a || !nnz_M || !nnz_B) return VEM_ERR_INVALID;
+  *nnz_M = a->M.nnz;
+  *nnz_B = a->B.nnz;
+  return VEM_OK;
+}
+
+int vem_mixed_assembled_copy(const vem_asm *a, int64_t *mrp, int32_t *mci, double *mva, int64_t *brp, int32_t *bci,
+                             double *bva, double *f) {
+  if (!a || !mrp || !mci || !mva || !brp || !bci || !bva || !f) return VEM_ERR_INVALID;
+  cudaStream_t s = a->impl->stream;
+  CK_RET(cudaMemcpyAsync(mrp, a->M.rp, (a->M.nrows + 1) * sizeof(int64_t), cudaMemcpyDeviceToHost, s));
+  CK_RET(cudaMemcpyAsync(mci, a->M.ci, a->M.nnz * sizeof(int32_t), cudaMemcpyDeviceToHost, s));
+  CK_RET(cudaMemcpyAsync(mva, a->M.va, a->M.nnz * sizeof(double), cudaMemcpyDeviceToHost, s));
+  CK_RET(cudaMemcpyAsync(brp, a->B.rp, (a->B.nrows + 1) * sizeof(int64_t), cudaMemcpyDeviceToHost, s));
+  CK_RET(cudaMemcpyAsync(bci, a->B.ci, a->B.nnz * sizeof(int32_t), cudaMemcpyDeviceToHost, s));
+  CK_RET(cudaMemcpyAsync(bva, a->B.va, a->B.nnz * sizeof(double), cudaMemcpyDeviceToHost, s));
+  CK_RET(cudaMemcpyAsync(f, a->f, a->B.nrows * sizeof(double), cudaMemcpyDeviceToHost, s));
+  CK_RET(cudaStreamSynchronize(s));
+  return VEM_OK;
+}
+
+void vem_mixed_assembled_free(vem_asm *a) {
+  if (!a) return;
+  destroy_ctx(a->impl);
+  delete a;
 }
 
 int vem_mixed_solve(vem_ctx *h, const double *rhs, double tol, int32_t maxit, int32_t kind, double *out_u,

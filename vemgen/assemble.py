@@ -156,6 +156,51 @@ def boundary_term(mesh, k, gD):
     return dofs.reshape(-1), val.reshape(-1)
 
 
+def class_template(mesh, cls, ops, k: int, source=None) -> dict:
+    """Shape cache of one congruent cell class (the host half of the element-parallel
+    GPU assembly, vem_mixed_assemble): local DOF maps, the K-independent local
+    templates after the R11 drop, their nonzero pattern (ii, jj) / (bi, bj) and the
+    per-cell coefficients, such that cell e contributes
+        M_e[ii, jj] = ((c_e0 A0 + c_e1 A1) + c_e2 A2) + c_e3 S,   c_e = (1/K_e0, 1/K_e1, 1/K_e2, s_P)
+        B_e[bi, bj] = Bt[bi, bj]
+        f_e = -|P| Hinv F_e."""
+    nf = poly.dim_pk_2d(k)
+    nk = poly.dim_pk_3d(k)
+    n_int = (nk - 1) + poly.dim_gperp(k)
+    E = cls.cell_ids.shape[0]
+    fd = (cls.face_ids[:, :, None] * nf + np.arange(nf)[None, None, :]).reshape(E, -1)
+    idofs = mesh.n_faces * nf + cls.cell_ids[:, None] * n_int + np.arange(n_int)[None, :]
+    L = np.concatenate([fd, idofs], axis=1)
+    assert L.shape[1] == ops["nloc"]
+    P = cls.cell_ids[:, None] * nk + np.arange(nk)[None, :]
+    Kc = mesh.K[cls.cell_ids]
+    invK = 1.0 / Kc
+    sP = cls.vol * invK.mean(axis=1)
+    A = np.stack([_drop(ops["A"][:, c]) for c in range(3)], axis=1)
+    S = _drop(ops["S"])
+    Bt = _drop(-ops["vol"][:, None, None] * ops["Div"])
+    mask = (A[0] != 0).any(axis=0) | (S[0] != 0)
+    ii, jj = np.nonzero(mask)
+    bi, bj = np.nonzero(Bt[0])
+    F = source_moments(cls, k, source)
+    Hinv = np.linalg.inv(ops["Hp"])
+    return dict(L=L, P=P, ii=ii, jj=jj, A=np.stack([A[0, c][ii, jj] for c in range(3)]), S=S[0][ii, jj],
+                coef=np.concatenate([invK, sP[:, None]], axis=1), bi=bi, bj=bj, B=Bt[0][bi, bj],
+                F=F, Hinv=np.broadcast_to(Hinv, (E, nk, nk))[0], vol=cls.vol)
+
+
+def class_templates(mesh, k: int, source=None) -> list:
+    """Shape caches of every cell class (the input of vem_mixed_assemble); all
+    classes must be congruent (cube grids, cube pairs).  Kuhn tetrahedra (C2) are
+    not: every cell has its own local matrices, assembled on the host."""
+    out = []
+    for cls in mesh.classes:
+        if not cls.congruent:
+            raise ValueError("device assembly needs congruent cell classes (cubes, cube pairs)")
+        out.append(class_template(mesh, cls, local_operators(cls.rep(), k), k, source))
+    return out
+
+
 def build_system(mesh, k: int, source=None, gD=None, keep_local=False) -> System:
     """Assemble M, B, g, f for mesh at order k (RT-type, reading R1)."""
     nf = poly.dim_pk_2d(k)
@@ -169,28 +214,28 @@ def build_system(mesh, k: int, source=None, gD=None, keep_local=False) -> System
     for cls in mesh.classes:
         E = cls.cell_ids.shape[0]
         ops = local_operators(cls.rep(), k)
-        nloc = ops["nloc"]
-        fd = (cls.face_ids[:, :, None] * nf + np.arange(nf)[None, None, :]).reshape(E, -1)
-        idofs = mesh.n_faces * nf + cls.cell_ids[:, None] * n_int + np.arange(n_int)[None, :]
-        L = np.concatenate([fd, idofs], axis=1)
-        assert L.shape[1] == nloc
-        P = cls.cell_ids[:, None] * nk + np.arange(nk)[None, :]
-        Kc = mesh.K[cls.cell_ids]
-        invK = 1.0 / Kc
-        sP = cls.vol * invK.mean(axis=1)
-        A = np.stack([_drop(ops["A"][:, c]) for c in range(3)], axis=1)
-        S = _drop(ops["S"])
-        Bt = _drop(-ops["vol"][:, None, None] * ops["Div"])
         if cls.congruent:
-            mask = (A[0] != 0).any(axis=0) | (S[0] != 0)
-            ii, jj = np.nonzero(mask)
-            vals = (invK[:, 0, None] * A[0, 0][ii, jj] + invK[:, 1, None] * A[0, 1][ii, jj]
-                    + invK[:, 2, None] * A[0, 2][ii, jj] + sP[:, None] * S[0][ii, jj])
+            t = class_template(mesh, cls, ops, k, source)
+            L, P, ii, jj, bi, bj = t["L"], t["P"], t["ii"], t["jj"], t["bi"], t["bj"]
+            c = t["coef"]
+            vals = (c[:, 0, None] * t["A"][0] + c[:, 1, None] * t["A"][1] + c[:, 2, None] * t["A"][2]
+                    + c[:, 3, None] * t["S"])
             mr.append(L[:, ii].reshape(-1)); mc.append(L[:, jj].reshape(-1)); mv.append(vals.reshape(-1))
-            bi, bj = np.nonzero(Bt[0])
             br.append(P[:, bi].reshape(-1)); bc.append(L[:, bj].reshape(-1))
-            bv.append(np.broadcast_to(Bt[0][bi, bj], (E, bi.size)).reshape(-1))
+            bv.append(np.broadcast_to(t["B"], (E, bi.size)).reshape(-1))
+            fP = -cls.vol[:, None] * np.einsum("ab,eb->ea", t["Hinv"], t["F"])
         else:
+            nloc = ops["nloc"]
+            fd = (cls.face_ids[:, :, None] * nf + np.arange(nf)[None, None, :]).reshape(E, -1)
+            idofs = mesh.n_faces * nf + cls.cell_ids[:, None] * n_int + np.arange(n_int)[None, :]
+            L = np.concatenate([fd, idofs], axis=1)
+            assert L.shape[1] == nloc
+            P = cls.cell_ids[:, None] * nk + np.arange(nk)[None, :]
+            invK = 1.0 / mesh.K[cls.cell_ids]
+            sP = cls.vol * invK.mean(axis=1)
+            A = np.stack([_drop(ops["A"][:, c]) for c in range(3)], axis=1)
+            S = _drop(ops["S"])
+            Bt = _drop(-ops["vol"][:, None, None] * ops["Div"])
             Ml = np.einsum("ec,ecij->eij", invK, A) + sP[:, None, None] * S
             nz = Ml != 0
             mr.append(np.broadcast_to(L[:, :, None], Ml.shape)[nz])
@@ -200,9 +245,9 @@ def build_system(mesh, k: int, source=None, gD=None, keep_local=False) -> System
             br.append(np.broadcast_to(P[:, :, None], Bt.shape)[nzb])
             bc.append(np.broadcast_to(L[:, None, :], Bt.shape)[nzb])
             bv.append(Bt[nzb])
-        F = source_moments(cls, k, source)
-        Hinv = np.linalg.inv(ops["Hp"])
-        fP = -cls.vol[:, None] * np.einsum("eab,eb->ea", np.broadcast_to(Hinv, (E, nk, nk)), F)
+            F = source_moments(cls, k, source)
+            Hinv = np.linalg.inv(ops["Hp"])
+            fP = -cls.vol[:, None] * np.einsum("eab,eb->ea", np.broadcast_to(Hinv, (E, nk, nk)), F)
         f[P.reshape(-1)] = fP.reshape(-1)
         if keep_local:
             local_keep.append((cls, ops, L, P))
