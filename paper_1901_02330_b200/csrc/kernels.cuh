@@ -13,6 +13,7 @@
 #pragma once
 #include <cstdint>
 #include <cuda_runtime.h>
+#include <cooperative_groups.h>
 
 #define VEM_MAXM 128
 #define VEM_DOT_CHUNK 8
@@ -1207,4 +1208,132 @@ __global__ void __launch_bounds__(256) k_pcg_vec_blk(long ne, const double *__re
 __global__ void k_widen(long n, const int64_t *__restrict__ in, int *__restrict__ out) {
   for (long i = (long)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (long)gridDim.x * blockDim.x)
     out[i] = (int)in[i];
+}
+
+// ---------------------------------------------------------------------------
+// Persistent block PCG (small systems, latency-bound: C2): the whole inner solve
+// in ONE cooperative launch, grid-wide barriers between the phases of a step
+// instead of five kernel launches.  Same arithmetic as k_pcg_spmv_p /
+// k_pcg_alpha / k_pcg_vec_blk / k_pcg_beta / k_pcg_pupd (split form): block
+// partials, then EVERY block sums all partials in the same fixed order, so all
+// blocks take identical decisions (alpha, beta, convergence) without another
+// barrier.  Partial buffers of consecutive phases are disjoint (no read/write race).
+// ---------------------------------------------------------------------------
+__device__ __forceinline__ void grid_sum_parts(const double *part, int nb, int nv, double *out, double *sh) {
+  // out[0..nv) = sum over b < nb of part[b nv + i], lane-strided per warp then xor tree
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  if (warp < nv) {
+    double s = 0.0;
+    for (int b = lane; b < nb; b += 32) s += __ldcg(part + (size_t)b * nv + warp);
+    s = warp_sum(s);
+    if (lane == 0) sh[warp] = s;
+  }
+  __syncthreads();
+  for (int i = 0; i < nv; ++i) out[i] = sh[i];
+  __syncthreads();
+}
+
+// p_new = z + beta p_old formed at every gathered column (phase 3 folded into the
+// next step's phase 1: two barriers per step instead of three)
+struct GatherPz {
+  double beta;
+  const double *__restrict__ z, *__restrict__ p_old;
+  __device__ __forceinline__ double operator()(int c) const { return fma(beta, p_old[c], z[c]); }
+};
+
+template <int NB>
+__global__ void __launch_bounds__(256) k_pcg_persistent(long np, Sell S, const double *__restrict__ wdiag, double eps,
+                                                        const double *__restrict__ inv, double *__restrict__ x,
+                                                        double *__restrict__ r, double *__restrict__ z,
+                                                        double *__restrict__ p0, double *__restrict__ p1,
+                                                        double *__restrict__ q, double *part, DevState *st,
+                                                        double **p_final) {
+  namespace cg = cooperative_groups;
+  cg::grid_group grid = cg::this_grid();
+  __shared__ double sh[64];
+  __shared__ double tot[2];
+  double *part1 = part, *part2 = part + gridDim.x;
+  const long nth = (long)gridDim.x * blockDim.x, tid = (long)blockIdx.x * blockDim.x + threadIdx.x;
+  const long ne = np / NB, nw = blk_warps<NB>(ne);
+  int active = st->p.active, its = st->p.its, failed = 0;
+  const int maxit = st->p.maxit;
+  double rz = st->p.rz, rr = st->p.rr;
+  const double tol = st->p.tol_abs;
+  double beta = 0.0;            // first step: p = p0 (= z0, written by the init kernel)
+  double *pold = p0, *pnew = p1;
+  bool first = true;
+  while (active) {
+    // phase 1: p_new = z + beta p_old (own row, and on the fly at gathered columns);
+    //          q = (S + eps W) p_new; partial p_new . q
+    double v1[1] = {0.0};
+    for (long slot = tid; slot < np; slot += nth) {
+      const long row = sell_row(S, slot);
+      double acc, pi;
+      if (first) {
+        acc = sell_dot(S, slot, GatherX{pold});
+        pi = pold[row];
+      } else {
+        acc = sell_dot(S, slot, GatherPz{beta, z, pold});
+        pi = fma(beta, pold[row], z[row]);
+        pnew[row] = pi;
+      }
+      const double qi = fma(eps * (wdiag ? wdiag[row] : 1.0), pi, acc);
+      q[row] = qi;
+      v1[0] += pi * qi;
+    }
+    block_sum_n<1>(v1, sh);
+    if (threadIdx.x == 0) part1[blockIdx.x] = v1[0];
+    if (!first) {   // from here on the current direction is pnew
+      double *t = pold;
+      pold = pnew;
+      pnew = t;
+    }
+    first = false;
+    grid.sync();
+    grid_sum_parts(part1, gridDim.x, 1, tot, sh);
+    const double alpha = rz / tot[0];
+    // phase 2: x += alpha p, r -= alpha q, z = D_B^-1 r, partial r.z and r.r
+    double v[2] = {0.0, 0.0};
+    for (long gw = tid >> 5; gw < nw; gw += nth >> 5) {
+      const BlkWarp<NB> w(gw, ne);
+      double rk = 0.0;
+      if (w.valid) {
+        x[w.k] = fma(alpha, pold[w.k], x[w.k]);
+        rk = fma(-alpha, q[w.k], r[w.k]);
+        r[w.k] = rk;
+      }
+      const double tv = w.apply(inv, rk);
+      if (w.valid) {
+        z[w.k] = tv;
+        v[0] += rk * tv;
+        v[1] += rk * rk;
+      }
+    }
+    block_sum_n<2>(v, sh);
+    if (threadIdx.x == 0) {
+      part2[blockIdx.x * 2] = v[0];
+      part2[blockIdx.x * 2 + 1] = v[1];
+    }
+    grid.sync();
+    grid_sum_parts(part2, gridDim.x, 2, tot, sh);
+    ++its;
+    rr = tot[1];
+    if (sqrt(tot[1]) <= tol) {
+      active = 0;
+    } else if (its >= maxit) {
+      active = 0;
+      failed = 1;
+    } else {
+      beta = tot[0] / rz;
+      rz = tot[0];
+    }
+  }
+  if (blockIdx.x == 0 && threadIdx.x == 0) {
+    st->p.active = 0;
+    st->p.its = its;
+    st->p.failed = failed;
+    st->p.rz = rz;
+    st->p.rr = rr;
+    *p_final = pold;
+  }
 }

@@ -103,6 +103,9 @@ struct Ctx {
   // moves whole elements; the SELL slots of S_D add a row-level sort on top)
   int *s_slot = nullptr, *s_slot_old = nullptr;
   int pcg_split = 0;   // block PCG: q = S p with block partials, then a one-block alpha kernel
+  int pcg_persist = 1; // block PCG on small systems: one cooperative launch per inner solve
+  int pcg_coop_grid = 0;
+  double **pfinal = nullptr;   // persistent PCG: which p buffer holds the last direction (unused after)
   std::pair<long, long> reorder_pad{0, 0};
   double *dMinv = nullptr, *dSinv = nullptr, *dSepsinv = nullptr, *wdiag = nullptr, *sdiag = nullptr;
   // work vectors
@@ -554,9 +557,54 @@ int enqueue_pcg_steps(Ctx *c, int nsteps) {
   return 0;
 }
 
+// persistent cooperative form of the block PCG (k_pcg_persistent) for small systems
+template <int NB>
+struct PcgPersistK {
+  static void run(void **f) { *f = (void *)k_pcg_persistent<NB>; }
+};
+constexpr long PCG_PERSIST_MAX_NP = 262144;
+int ensure_part(Ctx *c, long need);
+
+int run_pcg_persistent(Ctx *c, int64_t *inner_its) {
+  void *fn = nullptr;
+  dispatch_nb<PcgPersistK>(c->nb, &fn);
+  if (!fn) return fail(c, VEM_ERR_PRECOND, "no persistent PCG for n_p_dof = %d", c->nb);
+  if (!c->pfinal) DA(c->pfinal, 1);
+  if (!c->pcg_coop_grid) {
+    int per_sm = 0;
+    CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, NT, 0));
+    if (per_sm < 1) return fail(c, VEM_ERR_CUDA, "persistent PCG does not fit on an SM");
+    c->pcg_coop_grid = (int)std::min<long>((long)per_sm * c->sm_count, (c->np + NT - 1) / NT);
+    int rr = ensure_part(c, 4L * c->pcg_coop_grid + 64);
+    if (rr) return rr;
+  }
+  long np = c->np;
+  Sell S = sellS(c);
+  const double *wd = c->wdiag;
+  double eps = c->eps;
+  const double *inv = c->dBeinv;
+  double *x = c->px, *r = c->pr, *z = c->pz, *p0 = c->pp0, *p1 = c->pp1, *q = c->pq, *part = c->part;
+  DevState *st = c->st;
+  double **pf = c->pfinal;
+  void *args[] = {&np, &S, &wd, &eps, &inv, &x, &r, &z, &p0, &p1, &q, &part, &st, &pf};
+  {
+    TimeScope ts(c, VEM_K_PCG_SPMV);
+    CK(cudaLaunchCooperativeKernel(fn, dim3(c->pcg_coop_grid), dim3(NT), args, 0, c->stream));
+  }
+  CK(cudaMemcpyAsync(&c->hst->p, &c->st->p, sizeof(PcgState), cudaMemcpyDeviceToHost, c->stream));
+  CK(cudaStreamSynchronize(c->stream));
+  flush_timing(c);
+  if (inner_its) *inner_its += c->hst->p.its;
+  if (c->hst->p.failed) return fail(c, VEM_ERR_INNER, "inner PCG did not reach %g in %d steps", c->opts.inner_rtol,
+                                    c->opts.inner_maxit);
+  return 0;
+}
+
 // Inner PCG: chunks of pcg_chunk (even) steps, graph-replayed, host polls the
 // device state between chunks.
 int run_pcg(Ctx *c, int64_t *inner_its) {
+  if (c->nb > 1 && c->pcg_persist && c->np <= PCG_PERSIST_MAX_NP && !c->capturing)
+    return run_pcg_persistent(c, inner_its);
   int chunk = std::max(2, c->opts.pcg_chunk);
   if (chunk % 2) ++chunk;
   const bool graphs = c->opts.use_graphs && c->opts.timing != 1;
@@ -1707,6 +1755,7 @@ int upload_impl(Ctx *c, const vem_csr *M, const vem_csr *B, const vem_csr *W, do
   auto t0 = std::chrono::steady_clock::now();
   const bool trace = getenv("VEM_SETUP_TRACE") != nullptr;
   c->pcg_split = getenv("VEM_PCG_SPLIT") ? atoi(getenv("VEM_PCG_SPLIT")) : 1;
+  c->pcg_persist = getenv("VEM_PCG_PERSIST") ? atoi(getenv("VEM_PCG_PERSIST")) : 1;
   auto phase = [&](const char *what) {
     if (!trace) return;
     cudaStreamSynchronize(c->stream);
