@@ -246,6 +246,17 @@ __global__ void k_sell_fill(long nrows, const int *__restrict__ rp, const int *_
     }
   }
 }
+// first element touching velocity row i of the merged A (its B^T columns >= nu): the
+// element-major key of the SELL-C-sigma velocity order
+__global__ void k_first_elem(long nu, const int *__restrict__ rp, const int *__restrict__ ci, int nb,
+                             int *__restrict__ elem) {
+  for (long i = (long)blockIdx.x * blockDim.x + threadIdx.x; i < nu; i += (long)gridDim.x * blockDim.x) {
+    int m = 0x7fffffff;
+    for (int k = rp[i]; k < rp[i + 1]; ++k)
+      if (ci[k] >= nu) m = min(m, (int)((ci[k] - nu) / nb));
+    elem[i] = m;
+  }
+}
 // out[i w + b] = in[perm[i] w + b]  (row gather of a row-major n x w array)
 __global__ void k_gather_rows(long n, int w, const int *__restrict__ perm, const double *__restrict__ in,
                               double *__restrict__ out) {

@@ -1290,13 +1290,29 @@ int build_reorder(Ctx *c) {
   std::vector<int> alen(n), slen(np);
   for (long i = 0; i < n; ++i) alen[i] = arp[i + 1] - arp[i];
   for (long i = 0; i < np; ++i) slen[i] = srp[i + 1] - srp[i];
-  // velocity rows: key = A row length
+  // velocity rows: element-major order (first element touching the row; counting sort,
+  // stable), so a row's gathers of x stay near its own index, then sorted by A row
+  // length inside the windows
   std::vector<int> pu(nu);
   std::vector<long long> ku(nu);
-  for (long i = 0; i < nu; ++i) {
-    pu[i] = (int)i;
-    ku[i] = alen[i];
+  const bool elem_major = !getenv("VEM_REORDER_ELEM") || atoi(getenv("VEM_REORDER_ELEM")) != 0;
+  if (elem_major) {
+    int *de = nullptr;
+    DA(de, nu);
+    k_first_elem<<<grid_stream(c, nu), NT, 0, c->stream>>>(nu, c->a_rp, c->a_ci, (int)nb, de);
+    CKL();
+    std::vector<int> el(nu);
+    CK(cudaMemcpyAsync(el.data(), de, nu * sizeof(int), cudaMemcpyDeviceToHost, c->stream));
+    CK(cudaStreamSynchronize(c->stream));
+    dfree(c, de);
+    std::vector<long> cnt(ne + 2, 0);
+    for (long i = 0; i < nu; ++i) cnt[std::min<long>(el[i], ne) + 1]++;
+    for (long e = 0; e <= ne; ++e) cnt[e + 1] += cnt[e];
+    for (long i = 0; i < nu; ++i) pu[cnt[std::min<long>(el[i], ne)]++] = (int)i;
+  } else {
+    for (long i = 0; i < nu; ++i) pu[i] = (int)i;
   }
+  for (long i = 0; i < nu; ++i) ku[i] = alen[i];
   window_sort(pu, ku, REORDER_WINDOW);
   // elements: key = (max B row length, max S_D row length) of the element's DOFs
   std::vector<int> pe(ne);
