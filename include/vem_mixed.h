@@ -51,7 +51,10 @@ enum {
 /* 3: Block-Schur with one aggregation V-cycle on S_D in place of the Chebyshev
  * iteration (the GPU-native stand-in for the exact MUMPS solve of S, P:978;
  * DESIGN.md reading R22; n_p_dof = 1 only in this version). */
-enum { VEM_PRECOND_NONE = 0, VEM_PRECOND_BLOCK_SCHUR = 1, VEM_PRECOND_BLOCK_REG = 2, VEM_PRECOND_BLOCK_SCHUR_AMG = 3 };
+enum { VEM_PRECOND_NONE = 0, VEM_PRECOND_BLOCK_SCHUR = 1, VEM_PRECOND_BLOCK_REG = 2, VEM_PRECOND_BLOCK_SCHUR_AMG = 3,
+       /* kind 3 with the V-cycle in FP32 (hierarchy values and vectors), GMRES and the
+        * saddle operator in FP64: the mixed-precision preconditioner of SURVEY.md §8(f) N4 */
+       VEM_PRECOND_BLOCK_SCHUR_AMG_F32 = 4 };
 
 typedef struct vem_ctx vem_ctx;    /* opaque; owns every device buffer it allocates */
 

@@ -182,6 +182,19 @@ class AMG:
         last = self.levels[-1]
         self.coarse_inv = np.linalg.inv(last.A.toarray()) if last.A.shape[0] <= coarse_size else None
 
+    def to_float32(self):
+        """The same hierarchy with every matrix, inverse and prolongator rounded to FP32
+        (precond kind 4: the V-cycle runs in FP32; the Chebyshev intervals keep the
+        FP64 Gershgorin bounds).  vcycle() then takes and returns float32 vectors."""
+        import copy
+        h = copy.copy(self)
+        h.levels = []
+        for lev in self.levels:
+            h.levels.append(Level(lev.A.astype(np.float32), lev.Dinv.astype(np.float32), lev.lmax, lev.agg, lev.nc,
+                                  None if lev.P is None else lev.P.astype(np.float32)))
+        h.coarse_inv = None if self.coarse_inv is None else self.coarse_inv.astype(np.float32)
+        return h
+
     def smooth(self, lev, b, degree=DEGREE):
         return chebyshev(lev.A, lev.Dinv, b, degree, lev.lmax, RATIO)
 
@@ -196,7 +209,7 @@ class AMG:
         if lev.P is not None:
             x = x + lev.P @ self.vcycle(lev.P.T @ r, level + 1)
         else:
-            bc = np.bincount(lev.agg, weights=r, minlength=lev.nc)
+            bc = np.bincount(lev.agg, weights=r, minlength=lev.nc).astype(r.dtype)
             xc = self.vcycle(bc, level + 1)
             x = x + xc[lev.agg]
         x = x + self.smooth(lev, b - lev.A @ x)

@@ -34,6 +34,7 @@ PRECOND_NONE = 0
 PRECOND_BLOCK_SCHUR = 1
 PRECOND_BLOCK_REG = 2
 PRECOND_BLOCK_SCHUR_AMG = 3     # Block-Schur with one aggregation V-cycle on S_D (oracle/amg.py, R22)
+PRECOND_BLOCK_SCHUR_AMG_F32 = 4  # the same V-cycle in FP32 inside the FP64 GMRES
 
 
 def spmv_saddle(M, B, x):
@@ -159,18 +160,20 @@ class Preconditioner:
     def __post_init__(self):
         self.nu = self.M.shape[0]
         self.dM = self.M.diagonal().copy()
-        if self.kind in (PRECOND_BLOCK_SCHUR, PRECOND_BLOCK_REG, PRECOND_BLOCK_SCHUR_AMG):
+        if self.kind in (PRECOND_BLOCK_SCHUR, PRECOND_BLOCK_REG, PRECOND_BLOCK_SCHUR_AMG, PRECOND_BLOCK_SCHUR_AMG_F32):
             self.SD = schur_diag(self.M, self.B)
             self.dS = self.SD.diagonal().copy()
             if np.any(self.dS <= 0):
                 raise ValueError("non-positive diag(S_D)")
             self.DBinv = block_jacobi_inv(self.SD, self.block)
             self.lmax = LAMBDA_MAX_BLOCK_JACOBI
-        if self.kind == PRECOND_BLOCK_SCHUR_AMG:
+        if self.kind in (PRECOND_BLOCK_SCHUR_AMG, PRECOND_BLOCK_SCHUR_AMG_F32):
             if self.block != 1:
                 raise NotImplementedError("Block-Schur-AMG is defined for n_p = 1 (k = 0) in this round")
             from .amg import AMG
             self.amg = AMG(self.SD)
+            if self.kind == PRECOND_BLOCK_SCHUR_AMG_F32:
+                self.amg = self.amg.to_float32()
         if self.kind == PRECOND_BLOCK_REG:
             if self.eps <= 0:
                 raise ValueError("eps must be > 0")
@@ -179,7 +182,9 @@ class Preconditioner:
 
     @property
     def flexible(self) -> bool:
-        return self.kind == PRECOND_BLOCK_REG
+        # FGMRES for the variable preconditioners: Block-Reg (inner PCG) and the FP32
+        # V-cycle (its rounding makes P^-1 (V y) differ from sum_j y_j P^-1 v_j)
+        return self.kind in (PRECOND_BLOCK_REG, PRECOND_BLOCK_SCHUR_AMG_F32)
 
     def apply(self, v):
         nu = self.nu
@@ -198,6 +203,8 @@ class Preconditioner:
             return np.concatenate([zu, zp])
         if self.kind == PRECOND_BLOCK_SCHUR_AMG:
             return np.concatenate([vu / self.dM, -self.amg.vcycle(vp)])
+        if self.kind == PRECOND_BLOCK_SCHUR_AMG_F32:
+            return np.concatenate([vu / self.dM, -self.amg.vcycle(vp.astype(np.float32)).astype(np.float64)])
         if self.kind == PRECOND_BLOCK_REG:
             # B_2^-1 = (eps W)^-1 with W = I
             zp = vp / self.eps

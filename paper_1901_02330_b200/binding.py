@@ -19,6 +19,7 @@ PRECOND_NONE = 0
 PRECOND_BLOCK_SCHUR = 1
 PRECOND_BLOCK_REG = 2
 PRECOND_BLOCK_SCHUR_AMG = 3
+PRECOND_BLOCK_SCHUR_AMG_F32 = 4
 
 STATUS = {0: "OK", 1: "NOT_CONVERGED", 2: "BREAKDOWN", -1: "ERR_INVALID", -2: "ERR_DIAG_M",
           -3: "ERR_DIAG_S", -4: "ERR_CUDA", -5: "ERR_PRECOND", -6: "ERR_INNER"}

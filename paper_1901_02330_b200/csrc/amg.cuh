@@ -197,179 +197,6 @@ __global__ void k_amg_gj_extract(long n, const double *__restrict__ D, double *_
 }
 
 // ---------------------------------------------------------------------------
-// V-cycle kernels (all gated)
-// ---------------------------------------------------------------------------
-// Chebyshev smoother init from x0 = 0: r = b, d = D^-1 b / theta, x = d
-// acc = 1: x += C(b) (post-smoothing on the residual equation accumulates into x)
-__global__ void k_amg_cheb_init(long n, const double *__restrict__ dinv, const double *__restrict__ b,
-                                double inv_theta, double *__restrict__ r, double *__restrict__ d,
-                                double *__restrict__ x, int acc, const int *gate) {
-  if (!*gate) return;
-  for (long i = (long)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (long)gridDim.x * blockDim.x) {
-    const double bi = b[i];
-    const double di = dinv[i] * bi * inv_theta;
-    r[i] = bi;
-    d[i] = di;
-    x[i] = acc ? x[i] + di : di;
-  }
-}
-// r -= A d_old; d_new = c1 d_old + c2 D^-1 r; x += d_new   (x_out may alias x)
-__global__ void __launch_bounds__(256) k_amg_cheb_step(long n, Sell A, const double *__restrict__ dinv,
-                                                       double *__restrict__ r, const double *__restrict__ d_old,
-                                                       double *__restrict__ d_new, double *__restrict__ x,
-                                                       double c1, double c2, const int *gate) {
-  if (!*gate) return;
-  const long i = (long)blockIdx.x * blockDim.x + threadIdx.x;
-  if (i >= n) return;
-  const double rn = r[i] - sell_dot(A, i, GatherX{d_old});
-  const double dn = c1 * d_old[i] + c2 * (dinv[i] * rn);
-  r[i] = rn;
-  d_new[i] = dn;
-  x[i] += dn;
-}
-// warp-per-row CSR variants for the coarse levels, whose Galerkin rows are long
-// (tens to hundreds of entries): one warp per row, lane-strided, xor-tree sum.
-__device__ __forceinline__ double warp_row_dot(const int *__restrict__ rp, const int *__restrict__ ci,
-                                               const double *__restrict__ va, const double *__restrict__ x,
-                                               long row) {
-  const int lane = threadIdx.x & 31;
-  double acc = 0.0;
-  for (int k = rp[row] + lane; k < rp[row + 1]; k += 32) acc = fma(va[k], x[ci[k]], acc);
-  return warp_sum(acc);
-}
-__global__ void __launch_bounds__(256) k_amg_cheb_step_w(long n, const int *__restrict__ rp,
-                                                         const int *__restrict__ ci, const double *__restrict__ va,
-                                                         const double *__restrict__ dinv, double *__restrict__ r,
-                                                         const double *__restrict__ d_old, double *__restrict__ d_new,
-                                                         double *__restrict__ x, double c1, double c2,
-                                                         const int *gate) {
-  if (!*gate) return;
-  const long i = ((long)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
-  if (i >= n) return;
-  const double ad = warp_row_dot(rp, ci, va, d_old, i);
-  if ((threadIdx.x & 31) == 0) {
-    const double rn = r[i] - ad;
-    const double dn = c1 * d_old[i] + c2 * (dinv[i] * rn);
-    r[i] = rn;
-    d_new[i] = dn;
-    x[i] += dn;
-  }
-}
-// t = b - A x, warp per row
-__global__ void __launch_bounds__(256) k_amg_resid_w(long n, const int *__restrict__ rp, const int *__restrict__ ci,
-                                                     const double *__restrict__ va, const double *__restrict__ x,
-                                                     const double *__restrict__ b, double *__restrict__ t,
-                                                     const int *gate) {
-  if (!*gate) return;
-  const long i = ((long)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
-  if (i >= n) return;
-  const double ax = warp_row_dot(rp, ci, va, x, i);
-  if ((threadIdx.x & 31) == 0) t[i] = b[i] - ax;
-}
-
-// bc[a] = sum over members of r (index order)
-__global__ void k_amg_restrict(long nc, const int *__restrict__ moff, const int *__restrict__ mem,
-                               const double *__restrict__ r, double *__restrict__ bc, const int *gate) {
-  if (!*gate) return;
-  for (long a = (long)blockIdx.x * blockDim.x + threadIdx.x; a < nc; a += (long)gridDim.x * blockDim.x) {
-    double s = 0.0;
-    for (int p = moff[a]; p < moff[a + 1]; ++p) s += r[mem[p]];
-    bc[a] = s;
-  }
-}
-__global__ void k_amg_prolong_add(long n, const int *__restrict__ agg, const double *__restrict__ xc,
-                                  double *__restrict__ x, const int *gate) {
-  if (!*gate) return;
-  for (long i = (long)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (long)gridDim.x * blockDim.x)
-    x[i] += xc[agg[i]];
-}
-// out = sgn * (x + y)
-__global__ void k_amg_add(long n, const double *__restrict__ x, const double *__restrict__ y, double sgn,
-                          double *__restrict__ out, const int *gate) {
-  if (!*gate) return;
-  for (long i = (long)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (long)gridDim.x * blockDim.x)
-    out[i] = sgn * (y ? x[i] + y[i] : x[i]);
-}
-// x = inv b, one warp per row (coalesced row reads)
-__global__ void __launch_bounds__(256) k_amg_dense_mv(long n, const double *__restrict__ inv,
-                                                      const double *__restrict__ b, double *__restrict__ x,
-                                                      const int *gate) {
-  if (!*gate) return;
-  const long i = ((long)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
-  if (i >= n) return;
-  const int lane = threadIdx.x & 31;
-  double s = 0.0;
-  for (long j = lane; j < n; j += 32) s = fma(inv[i * n + j], b[j], s);
-  s = warp_sum(s);
-  if (lane == 0) x[i] = s;
-}
-
-// first smoother step fused with the init (SELL levels): d0 = D^-1 b / theta gathered
-// on the fly; r = b - A d0; d1 = c1 d0 + c2 D^-1 r; x = d0 + d1
-struct GatherD0b {
-  const double *__restrict__ b, *__restrict__ dinv;
-  double it;
-  __device__ __forceinline__ double operator()(int c) const { return dinv[c] * b[c] * it; }
-};
-__global__ void __launch_bounds__(256) k_amg_cheb_first(long n, Sell A, const double *__restrict__ dinv,
-                                                        const double *__restrict__ b, double inv_theta, double c1,
-                                                        double c2, double *__restrict__ r, double *__restrict__ d_new,
-                                                        double *__restrict__ x, int acc, const int *gate) {
-  if (!*gate) return;
-  const long i = (long)blockIdx.x * blockDim.x + threadIdx.x;
-  if (i >= n) return;
-  const double ad = sell_dot(A, i, GatherD0b{b, dinv, inv_theta});
-  const double bi = b[i];
-  const double d0 = dinv[i] * bi * inv_theta;
-  const double rn = bi - ad;
-  const double dn = c1 * d0 + c2 * (dinv[i] * rn);
-  r[i] = rn;
-  d_new[i] = dn;
-  x[i] = acc ? x[i] + (d0 + dn) : d0 + dn;
-}
-
-// warp-per-row version of the fused first smoother step (small coarse levels)
-__global__ void __launch_bounds__(256) k_amg_cheb_first_w(long n, const int *__restrict__ rp,
-                                                          const int *__restrict__ ci, const double *__restrict__ va,
-                                                          const double *__restrict__ dinv, const double *__restrict__ b,
-                                                          double inv_theta, double c1, double c2,
-                                                          double *__restrict__ r, double *__restrict__ d_new,
-                                                          double *__restrict__ x, int acc, const int *gate) {
-  if (!*gate) return;
-  const long i = ((long)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
-  if (i >= n) return;
-  const int lane = threadIdx.x & 31;
-  double acc_d = 0.0;
-  for (int k = rp[i] + lane; k < rp[i + 1]; k += 32) {
-    const int c = ci[k];
-    acc_d = fma(va[k], dinv[c] * b[c] * inv_theta, acc_d);
-  }
-  acc_d = warp_sum(acc_d);
-  if (lane == 0) {
-    const double bi = b[i];
-    const double d0 = dinv[i] * bi * inv_theta;
-    const double rn = bi - acc_d;
-    const double dn = c1 * d0 + c2 * (dinv[i] * rn);
-    r[i] = rn;
-    d_new[i] = dn;
-    x[i] = acc ? x[i] + (d0 + dn) : d0 + dn;
-  }
-}
-// Block-Schur-AMG top: z_u = s v_u ./ diag(M), b0 = s v_p
-__global__ void k_amg_top(long nu, long np, const double *__restrict__ v, const double *scale,
-                          const double *__restrict__ dMinv, double *__restrict__ z, double *__restrict__ b0,
-                          const int *gate) {
-  if (!*gate) return;
-  const double s = *scale;
-  for (long i = (long)blockIdx.x * blockDim.x + threadIdx.x; i < nu + np; i += (long)gridDim.x * blockDim.x) {
-    if (i < nu)
-      z[i] = s * v[i] * dMinv[i];
-    else
-      b0[i - nu] = s * v[i];
-  }
-}
-
-// ---------------------------------------------------------------------------
 // Smoothed aggregation (level 0, oracle/amg.py smoothed_prolongator):
 //   P = (I - omega D^-1 A) T,  A_c = P^T (A P); every product is expanded into
 //   (key, value) pairs in a fixed order, stable-radix-sorted and run-reduced.
@@ -451,55 +278,4 @@ __global__ void k_sa_expand_pt(long n, const int *__restrict__ prp, const int *_
       keys[k] = (unsigned long long)((long long)pci[k] * n + i);
       vals[k] = pva[k];
     }
-}
-// restriction b_c = P^T r: 8 lanes per coarse row (rows average ~36 entries),
-// lane-strided then a 3-level xor tree inside the group (fixed order)
-__global__ void __launch_bounds__(256) k_sa_restrict(long nc, const int *__restrict__ trp, const int *__restrict__ tci,
-                                                     const double *__restrict__ tva, const double *__restrict__ r,
-                                                     double *__restrict__ bc, const int *gate) {
-  if (!*gate) return;
-  const long t = (long)blockIdx.x * blockDim.x + threadIdx.x;
-  const long a = t >> 3;
-  const int g = (int)(t & 7);
-  double acc = 0.0;
-  if (a < nc)
-    for (int k = trp[a] + g; k < trp[a + 1]; k += 8) acc = fma(tva[k], r[tci[k]], acc);
-#pragma unroll
-  for (int o = 4; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
-  if (a < nc && g == 0) bc[a] = acc;
-}
-// prolongation x += P xc (SELL-32)
-__global__ void __launch_bounds__(256) k_sa_prolong_add(long n, Sell P, const double *__restrict__ xc,
-                                                        double *__restrict__ x, const int *gate) {
-  if (!*gate) return;
-  const long i = (long)blockIdx.x * blockDim.x + threadIdx.x;
-  if (i >= n) return;
-  x[i] += sell_dot(P, i, GatherX{xc});
-}
-
-// Arnoldi-step form of the Block-Schur-AMG output (kind 3, GMRES): the preconditioned
-// vector z = [s v_u ./ diag(M); -x0] is never written; the saddle SpMV gathers it on
-// the fly (same floating-point operations as k_amg_top / k_amg_add, so w = A z is
-// bitwise the same), and the V-cycle reads b0 = s v_p from k_amg_top_p.
-struct GatherAmgZ {
-  long nu;
-  double s;
-  const double *__restrict__ v, *__restrict__ dMinv, *__restrict__ x0;
-  __device__ __forceinline__ double operator()(int c) const { return c < nu ? s * v[c] * dMinv[c] : -x0[c - nu]; }
-};
-__global__ void __launch_bounds__(256) k_spmv_amgz(long n, long nu, Sell A, const double *__restrict__ v,
-                                                   const double *scale, const double *__restrict__ dMinv,
-                                                   const double *__restrict__ x0, double *__restrict__ y,
-                                                   const int *gate) {
-  if (!*gate) return;
-  const long row = (long)blockIdx.x * blockDim.x + threadIdx.x;
-  if (row >= n) return;
-  y[row] = sell_dot(A, row, GatherAmgZ{nu, *scale, v, dMinv, x0});
-}
-__global__ void k_amg_top_p(long nu, long np, const double *__restrict__ v, const double *scale,
-                            double *__restrict__ b0, const int *gate) {
-  if (!*gate) return;
-  const double s = *scale;
-  for (long i = (long)blockIdx.x * blockDim.x + threadIdx.x; i < np; i += (long)gridDim.x * blockDim.x)
-    b0[i] = s * v[nu + i];
 }

@@ -27,6 +27,7 @@
 #include "kernels.cuh"
 #include "amg.cuh"
 #include "assembly.cuh"
+#include "amg_apply.cuh"
 
 namespace {
 
@@ -59,7 +60,44 @@ struct AmgLevel {
   int *prp = nullptr, *pci = nullptr, *ptrp = nullptr, *ptci = nullptr, *psci = nullptr;
   double *pva = nullptr, *ptva = nullptr, *psva = nullptr;
   long long *psoff = nullptr;
-  long pnnz = 0;
+  long pnnz = 0, psnnz = 0;
+  // FP32 mirror for precond kind 4 (values converted once after setup; own vectors)
+  float *sva_f = nullptr, *va_f = nullptr, *dinv_f = nullptr, *psva_f = nullptr, *ptva_f = nullptr;
+  float *b_f = nullptr, *x_f = nullptr, *t_f = nullptr, *sr_f = nullptr, *sd0_f = nullptr, *sd1_f = nullptr;
+};
+
+// level data of the V-cycle in precision T
+template <typename T>
+struct Lv;
+template <>
+struct Lv<double> {
+  AmgLevel &L;
+  const double *sva() const { return L.sva; }
+  const double *va() const { return L.va; }
+  const double *dinv() const { return L.dinv; }
+  const double *psva() const { return L.psva; }
+  const double *ptva() const { return L.ptva; }
+  double *b() const { return L.b; }
+  double *x() const { return L.x; }
+  double *t() const { return L.t; }
+  double *sr() const { return L.sr; }
+  double *sd0() const { return L.sd0; }
+  double *sd1() const { return L.sd1; }
+};
+template <>
+struct Lv<float> {
+  AmgLevel &L;
+  const float *sva() const { return L.sva_f; }
+  const float *va() const { return L.va_f; }
+  const float *dinv() const { return L.dinv_f; }
+  const float *psva() const { return L.psva_f; }
+  const float *ptva() const { return L.ptva_f; }
+  float *b() const { return L.b_f; }
+  float *x() const { return L.x_f; }
+  float *t() const { return L.t_f; }
+  float *sr() const { return L.sr_f; }
+  float *sd0() const { return L.sd0_f; }
+  float *sd1() const { return L.sd1_f; }
 };
 
 struct Ctx {
@@ -82,6 +120,11 @@ struct Ctx {
   double *h_rhs = nullptr, *h_u = nullptr, *h_p = nullptr;   // vem_mixed_solve_host staging
   std::vector<AmgLevel> amg;                     // S_D hierarchy (kind 3); empty when n_p_dof > 1
   double *amg_cinv = nullptr;                    // dense inverse of the coarsest level
+  float *amg_cinv_f = nullptr;                   // its FP32 copy (kind 4)
+  bool amg_f32 = false;                          // FP32 mirror built
+  float *f32_pool = nullptr;                     // kind 4 fine-level vectors (L2-persisting window)
+  size_t f32_pool_bytes = 0;
+  int l2_window_pool = -1;                       // pool under the window: 0 FP64 Chebyshev, 1 FP32
   bool amg_dense = false;
   size_t cheb_pool_bytes = 0;
   size_t l2_window_bytes = 0;           // bytes of the pool under a persisting L2 access window
@@ -121,7 +164,7 @@ struct Ctx {
   int *derr = nullptr;
   long part_cap = 0;
   // graphs
-  cudaGraphExec_t cycle_exec[4] = {nullptr, nullptr, nullptr, nullptr};
+  cudaGraphExec_t cycle_exec[5] = {nullptr, nullptr, nullptr, nullptr, nullptr};   // per precond kind
   cudaGraphExec_t pcg_exec = nullptr;
   int pcg_exec_chunk = 0;
   // timing
@@ -134,7 +177,7 @@ struct Ctx {
   // the host reads the pairs of the executed steps after every cycle.
   int sample_slot = -1;
   bool sample_recorded = false;        // set when an enqueue recorded a sample pair
-  bool sample_recorded_kind[4] = {false, false, false, false};
+  bool sample_recorded_kind[5] = {false, false, false, false, false};
   std::vector<cudaEvent_t> samp_a, samp_b;
   // misc
   std::string err;
@@ -664,43 +707,49 @@ void amg_cheb_coeffs(double lmax, int degree, double &inv_theta, std::vector<dou
   }
 }
 
-// out = C_degree(b) on level L (x0 = 0); `sample`: bracket the second step with the
-// sampled-timing events (fine-level pre-smoothing, timing = 2)
-void amg_smooth(Ctx *c, AmgLevel &L, const double *b, double *out, int degree, const int *gate,
-                bool sample = false, int acc = 0) {
+// out = C_degree(b) on level L (x0 = 0), in precision T; `sample`: bracket the second
+// step with the sampled-timing events (fine-level pre-smoothing, timing = 2)
+template <typename T>
+void amg_smooth(Ctx *c, AmgLevel &L, const T *b, T *out, int degree, const int *gate, bool sample = false,
+                int acc = 0) {
+  const Lv<T> D{L};
+  const double vb = sizeof(T) + 4.0;   // bytes per stored entry (value + index)
   double it;
   std::vector<double> c1, c2;
   amg_cheb_coeffs(L.lmax, degree, it, c1, c2);
-  const Sell A{L.soff, L.sci, L.sva};
-  double *dold = L.sd0, *dnew = L.sd1;
+  const SellT<T> A{L.soff, L.sci, D.sva()};
+  T *dold = D.sd0(), *dnew = D.sd1();
   int first = 1;
   if (degree > 1) {   // init fused into the first step
-    TimeScope ts(c, VEM_K_CHEB, 12.0 * L.nnz + 48.0 * L.n);
+    TimeScope ts(c, VEM_K_CHEB, vb * L.nnz + 6.0 * sizeof(T) * L.n);
     if (L.warp_rows)
-      k_amg_cheb_first_w<<<grid_for(L.n * 32), NT, 0, c->stream>>>(L.n, L.rp, L.ci, L.va, L.dinv, b, it, c1[0],
-                                                                    c2[0], L.sr, L.sd1, out, acc, gate);
+      k_vc_cheb_first_w<T><<<grid_for(L.n * 32), NT, 0, c->stream>>>(L.n, L.rp, L.ci, D.va(), D.dinv(), b, (T)it,
+                                                                       (T)c1[0], (T)c2[0], D.sr(), D.sd1(), out,
+                                                                       acc, gate);
     else
-      k_amg_cheb_first<<<grid_for(L.n), NT, 0, c->stream>>>(L.n, A, L.dinv, b, it, c1[0], c2[0], L.sr, L.sd1, out,
-                                                            acc, gate);
-    dold = L.sd1;
-    dnew = L.sd0;
+      k_vc_cheb_first<T><<<grid_for(L.n), NT, 0, c->stream>>>(L.n, A, D.dinv(), b, (T)it, (T)c1[0], (T)c2[0],
+                                                               D.sr(), D.sd1(), out, acc, gate);
+    dold = D.sd1();
+    dnew = D.sd0();
     first = 2;
   } else {
-    TimeScope ts(c, VEM_K_PRECOND_VEC, 40.0 * L.n);
-    k_amg_cheb_init<<<grid_stream(c, L.n), NT, 0, c->stream>>>(L.n, L.dinv, b, it, L.sr, L.sd0, out, acc, gate);
+    TimeScope ts(c, VEM_K_PRECOND_VEC, 5.0 * sizeof(T) * L.n);
+    k_vc_cheb_init<T><<<grid_stream(c, L.n), NT, 0, c->stream>>>(L.n, D.dinv(), b, (T)it, D.sr(), D.sd0(), out,
+                                                                  acc, gate);
   }
   for (int i = first; i < degree; ++i) {
     const bool smp = sample && i == 2 && c->opts.timing == 2 && c->sample_slot >= 0 && !L.warp_rows;
     if (smp) cudaEventRecordWithFlags(c->samp_a[c->sample_slot], c->stream, cudaEventRecordExternal);
     c->sample_recorded |= smp;
     {
-      TimeScope ts(c, VEM_K_CHEB, 12.0 * L.nnz + 56.0 * L.n);
+      TimeScope ts(c, VEM_K_CHEB, vb * L.nnz + 7.0 * sizeof(T) * L.n);
       if (L.warp_rows)
-        k_amg_cheb_step_w<<<grid_for(L.n * 32), NT, 0, c->stream>>>(L.n, L.rp, L.ci, L.va, L.dinv, L.sr, dold, dnew,
-                                                                     out, c1[i - 1], c2[i - 1], gate);
+        k_vc_cheb_step_w<T><<<grid_for(L.n * 32), NT, 0, c->stream>>>(L.n, L.rp, L.ci, D.va(), D.dinv(), D.sr(),
+                                                                       dold, dnew, out, (T)c1[i - 1], (T)c2[i - 1],
+                                                                       gate);
       else
-        k_amg_cheb_step<<<grid_for(L.n), NT, 0, c->stream>>>(L.n, A, L.dinv, L.sr, dold, dnew, out, c1[i - 1],
-                                                             c2[i - 1], gate);
+        k_vc_cheb_step<T><<<grid_for(L.n), NT, 0, c->stream>>>(L.n, A, D.dinv(), D.sr(), dold, dnew, out,
+                                                               (T)c1[i - 1], (T)c2[i - 1], gate);
     }
     if (smp) cudaEventRecordWithFlags(c->samp_b[c->sample_slot], c->stream, cudaEventRecordExternal);
     std::swap(dold, dnew);
@@ -708,77 +757,95 @@ void amg_smooth(Ctx *c, AmgLevel &L, const double *b, double *out, int degree, c
 }
 
 // t = b - A x on level L
+template <typename T>
 void amg_residual(Ctx *c, AmgLevel &L, const int *gate) {
-  TimeScope ts(c, VEM_K_SPMV, 12.0 * L.nnz + 24.0 * L.n);
-  if (L.warp_rows) {
-    k_amg_resid_w<<<grid_for(L.n * 32), NT, 0, c->stream>>>(L.n, L.rp, L.ci, L.va, L.x, L.b, L.t, gate);
-  } else {
-    const Sell A{L.soff, L.sci, L.sva};
-    k_spmv<<<grid_for(L.n), NT, 0, c->stream>>>(0, L.n, A, L.x, L.t, L.b, 1, gate);
-  }
+  const Lv<T> D{L};
+  TimeScope ts(c, VEM_K_SPMV, (sizeof(T) + 4.0) * L.nnz + 3.0 * sizeof(T) * L.n);
+  if (L.warp_rows)
+    k_vc_resid_w<T><<<grid_for(L.n * 32), NT, 0, c->stream>>>(L.n, L.rp, L.ci, D.va(), D.x(), D.b(), D.t(), gate);
+  else
+    k_vc_resid<T><<<grid_for(L.n), NT, 0, c->stream>>>(L.n, SellT<T>{L.soff, L.sci, D.sva()}, D.x(), D.b(), D.t(),
+                                                        gate);
 }
 
+template <typename T>
+const T *amg_cinv(Ctx *c);
+template <>
+const double *amg_cinv<double>(Ctx *c) { return c->amg_cinv; }
+template <>
+const float *amg_cinv<float>(Ctx *c) { return c->amg_cinv_f; }
+
+template <typename T>
 void amg_vcycle(Ctx *c, size_t l, const int *gate) {
   AmgLevel &L = c->amg[l];
+  const Lv<T> D{L};
   if (l + 1 == c->amg.size()) {   // coarsest
     if (c->amg_dense) {
-      TimeScope ts(c, VEM_K_PRECOND_VEC, 8.0 * L.n * L.n);
-      k_amg_dense_mv<<<grid_for(L.n * 32), NT, 0, c->stream>>>(L.n, c->amg_cinv, L.b, L.x, gate);
+      TimeScope ts(c, VEM_K_PRECOND_VEC, (double)sizeof(T) * L.n * L.n);
+      k_vc_dense_mv<T><<<grid_for(L.n * 32), NT, 0, c->stream>>>(L.n, amg_cinv<T>(c), D.b(), D.x(), gate);
     } else {
-      amg_smooth(c, L, L.b, L.x, AMG_COARSE_DEGREE, gate);
+      amg_smooth<T>(c, L, D.b(), D.x(), AMG_COARSE_DEGREE, gate);
     }
     return;
   }
   AmgLevel &C = c->amg[l + 1];
-  amg_smooth(c, L, L.b, L.x, AMG_DEGREE, gate, l == 0);
-  amg_residual(c, L, gate);
+  const Lv<T> DC{C};
+  amg_smooth<T>(c, L, D.b(), D.x(), AMG_DEGREE, gate, l == 0);
+  amg_residual<T>(c, L, gate);
   if (L.sa) {
-    TimeScope ts(c, VEM_K_PRECOND_VEC, 12.0 * L.pnnz + 8.0 * L.n + 8.0 * C.n);
-    k_sa_restrict<<<grid_for(C.n * 8), NT, 0, c->stream>>>(C.n, L.ptrp, L.ptci, L.ptva, L.t, C.b, gate);
+    TimeScope ts(c, VEM_K_PRECOND_VEC, (sizeof(T) + 4.0) * L.pnnz + sizeof(T) * (1.0 * L.n + C.n));
+    k_vc_sa_restrict<T><<<grid_for(C.n * 8), NT, 0, c->stream>>>(C.n, L.ptrp, L.ptci, D.ptva(), D.t(), DC.b(), gate);
   } else {
-    TimeScope ts(c, VEM_K_PRECOND_VEC, 8.0 * L.n * 2 + 8.0 * C.n);
-    k_amg_restrict<<<grid_stream(c, C.n), NT, 0, c->stream>>>(C.n, L.moff, L.mem, L.t, C.b, gate);
+    TimeScope ts(c, VEM_K_PRECOND_VEC, sizeof(T) * (2.0 * L.n + C.n));
+    k_vc_restrict<T><<<grid_stream(c, C.n), NT, 0, c->stream>>>(C.n, L.moff, L.mem, D.t(), DC.b(), gate);
   }
-  amg_vcycle(c, l + 1, gate);
+  amg_vcycle<T>(c, l + 1, gate);
   if (L.sa) {
-    TimeScope ts(c, VEM_K_PRECOND_VEC, 12.0 * L.pnnz + 16.0 * L.n + 8.0 * C.n);
-    k_sa_prolong_add<<<grid_for(L.n), NT, 0, c->stream>>>(L.n, Sell{L.psoff, L.psci, L.psva}, C.x, L.x, gate);
+    TimeScope ts(c, VEM_K_PRECOND_VEC, (sizeof(T) + 4.0) * L.pnnz + sizeof(T) * (2.0 * L.n + C.n));
+    k_vc_sa_prolong_add<T><<<grid_for(L.n), NT, 0, c->stream>>>(L.n, SellT<T>{L.psoff, L.psci, D.psva()}, DC.x(),
+                                                                 D.x(), gate);
   } else {
-    TimeScope ts(c, VEM_K_PRECOND_VEC, 8.0 * L.n * 3);
-    k_amg_prolong_add<<<grid_stream(c, L.n), NT, 0, c->stream>>>(L.n, L.agg, C.x, L.x, gate);
+    TimeScope ts(c, VEM_K_PRECOND_VEC, sizeof(T) * 3.0 * L.n);
+    k_vc_prolong_add<T><<<grid_stream(c, L.n), NT, 0, c->stream>>>(L.n, L.agg, DC.x(), D.x(), gate);
   }
-  amg_residual(c, L, gate);
-  amg_smooth(c, L, L.t, L.x, AMG_DEGREE, gate, false, 1);   // x += C(b - A x)
+  amg_residual<T>(c, L, gate);
+  amg_smooth<T>(c, L, D.t(), D.x(), AMG_DEGREE, gate, false, 1);   // x += C(b - A x)
 }
 
-// z_out = false: only the V-cycle runs (x0 = V(s v_p)); k_spmv_amgz forms z on the fly
+// Block-Schur-AMG apply in precision T (kind 3: double, kind 4: float V-cycle).
+// z_out = false: only the V-cycle runs (x0 = V(s v_p)); k_vc_spmv_z forms z on the fly
+template <typename T>
 int enqueue_block_schur_amg(Ctx *c, const double *v, const double *scale, double *z, const int *gate,
                             bool z_out = true) {
   if (c->amg.empty()) return fail(c, VEM_ERR_PRECOND, "Block-Schur-AMG needs n_p_dof = 1 (k = 0)");
+  if (sizeof(T) == 4 && !c->amg_f32) return fail(c, VEM_ERR_PRECOND, "FP32 hierarchy not built");
   AmgLevel &L0 = c->amg[0];
-  if (z_out) {
-    TimeScope ts(c, VEM_K_PRECOND_VEC, 8.0 * (3 * c->nu + 2 * c->np));
-    k_amg_top<<<grid_stream(c, c->n), NT, 0, c->stream>>>(c->nu, c->np, v, scale, c->dMinv, z, L0.b, gate);
-  } else {
-    TimeScope ts(c, VEM_K_PRECOND_VEC, 16.0 * c->np);
-    k_amg_top_p<<<grid_stream(c, c->np), NT, 0, c->stream>>>(c->nu, c->np, v, scale, L0.b, gate);
-  }
-  amg_vcycle(c, 0, gate);
-  if (!z_out) {
-    CKL();
-    return 0;
-  }
+  const Lv<T> D0{L0};
   {
-    TimeScope ts(c, VEM_K_PRECOND_VEC, 24.0 * c->np);
-    k_amg_add<<<grid_stream(c, c->np), NT, 0, c->stream>>>(c->np, L0.x, nullptr, -1.0, z + c->nu, gate);
+    TimeScope ts(c, VEM_K_PRECOND_VEC, z_out ? 24.0 * c->nu + (8.0 + sizeof(T)) * c->np : (8.0 + sizeof(T)) * c->np);
+    if (z_out)
+      k_vc_top<T><<<grid_stream(c, c->n), NT, 0, c->stream>>>(c->nu, c->np, v, scale, c->dMinv, z, D0.b(), gate);
+    else   // pressure part only
+      k_vc_top<T><<<grid_stream(c, c->np), NT, 0, c->stream>>>(0, c->np, v + c->nu, scale, nullptr, nullptr, D0.b(),
+                                                                gate);
+  }
+  amg_vcycle<T>(c, 0, gate);
+  if (z_out) {
+    TimeScope ts(c, VEM_K_PRECOND_VEC, (8.0 + sizeof(T)) * c->np);
+    k_vc_out<T><<<grid_stream(c, c->np), NT, 0, c->stream>>>(c->np, D0.x(), z + c->nu, gate);
   }
   CKL();
   return 0;
 }
 
+// FGMRES (Z stored) for the variable preconditioners: Block-Reg (inner PCG) and the
+// FP32 V-cycle (its rounding makes P^-1 (V y) differ from sum y_j P^-1 v_j)
+inline bool is_flexible(int kind) { return kind == VEM_PRECOND_BLOCK_REG || kind == VEM_PRECOND_BLOCK_SCHUR_AMG_F32; }
+
 int enqueue_precond(Ctx *c, int kind, const double *v, const double *scale, double *z, const int *gate,
                     int64_t *inner_its) {
-  if (kind == VEM_PRECOND_BLOCK_SCHUR_AMG) return enqueue_block_schur_amg(c, v, scale, z, gate);
+  if (kind == VEM_PRECOND_BLOCK_SCHUR_AMG) return enqueue_block_schur_amg<double>(c, v, scale, z, gate);
+  if (kind == VEM_PRECOND_BLOCK_SCHUR_AMG_F32) return enqueue_block_schur_amg<float>(c, v, scale, z, gate);
   if (kind == VEM_PRECOND_BLOCK_SCHUR) return enqueue_block_schur(c, v, scale, z, gate);
   if (kind == VEM_PRECOND_BLOCK_REG) return enqueue_block_reg(c, v, scale, z, gate, inner_its);
   // NONE: z = scale * v
@@ -802,18 +869,25 @@ int ensure_part(Ctx *c, long need) {
 }
 
 int enqueue_arnoldi_step(Ctx *c, int kind, int j, int64_t *inner_its) {
-  const bool flex = kind == VEM_PRECOND_BLOCK_REG;
+  const bool flex = is_flexible(kind);
   double *Vj = c->V + (size_t)j * c->ldv;
   double *w = c->V + (size_t)(j + 1) * c->ldv;
   double *zj = flex ? c->Z + (size_t)j * c->ldv : c->z;
   c->sample_slot = j;
-  if (kind == VEM_PRECOND_BLOCK_SCHUR_AMG) {   // z = P^-1 v_j formed inside the SpMV gather
-    int rc = enqueue_block_schur_amg(c, Vj, &c->st->vscale[j], nullptr, gate_active(c), false);
+  if (kind == VEM_PRECOND_BLOCK_SCHUR_AMG || kind == VEM_PRECOND_BLOCK_SCHUR_AMG_F32) {
+    // z = P^-1 v_j formed inside the SpMV gather
+    const bool f32 = kind == VEM_PRECOND_BLOCK_SCHUR_AMG_F32;
+    int rc = f32 ? enqueue_block_schur_amg<float>(c, Vj, &c->st->vscale[j], nullptr, gate_active(c), false)
+                 : enqueue_block_schur_amg<double>(c, Vj, &c->st->vscale[j], nullptr, gate_active(c), false);
     c->sample_slot = -1;
     if (rc) return rc;
     TimeScope ts(c, VEM_K_SPMV, bytes_spmv(c) + 8.0 * c->nu);
-    k_spmv_amgz<<<grid_for(c->n), NT, 0, c->stream>>>(c->n, c->nu, sellA(c), Vj, &c->st->vscale[j], c->dMinv,
-                                                      c->amg[0].x, w, gate_active(c));
+    if (f32)   // FGMRES: z_j is also stored (row by row, by the thread that owns the row)
+      k_vc_spmv_z<float><<<grid_for(c->n), NT, 0, c->stream>>>(c->n, c->nu, sellA(c), Vj, &c->st->vscale[j],
+                                                                c->dMinv, c->amg[0].x_f, w, zj, gate_active(c));
+    else
+      k_vc_spmv_z<double><<<grid_for(c->n), NT, 0, c->stream>>>(c->n, c->nu, sellA(c), Vj, &c->st->vscale[j],
+                                                                 c->dMinv, c->amg[0].x, w, nullptr, gate_active(c));
   } else {
     int rc = enqueue_precond(c, kind, Vj, &c->st->vscale[j], zj, gate_active(c), inner_its);
     c->sample_slot = -1;
@@ -824,7 +898,7 @@ int enqueue_arnoldi_step(Ctx *c, int kind, int j, int64_t *inner_its) {
   const int nv = j + 1;
   const int gx = c->sm_count * 2;
   // reorth: 1 CGS2, 0 CGS1, -1 auto = CGS1 for GMRES, CGS2 for FGMRES/Block-Reg (reading R17)
-  const int npass = (c->opts.reorth == 1 || (c->opts.reorth < 0 && flex)) ? 2 : 1;
+  const int npass = (c->opts.reorth == 1 || (c->opts.reorth < 0 && kind == VEM_PRECOND_BLOCK_REG)) ? 2 : 1;
   for (int pass = 1; pass <= npass; ++pass) {
     const int nout = nv + (pass == 1 ? 1 : 0);
     dim3 grid(gx, (nout + VEM_DOT_CHUNK - 1) / VEM_DOT_CHUNK);
@@ -844,7 +918,7 @@ int enqueue_arnoldi_step(Ctx *c, int kind, int j, int64_t *inner_its) {
 }
 
 int enqueue_cycle_end(Ctx *c, int kind, int64_t *inner_its) {
-  const bool flex = kind == VEM_PRECOND_BLOCK_REG;
+  const bool flex = is_flexible(kind);
   {
     TimeScope ts(c, VEM_K_CYCLE);
     k_backsolve<<<1, 32, 0, c->stream>>>(c->st, flex ? 0 : 1);
@@ -894,7 +968,7 @@ int ensure_work(Ctx *c, int kind) {
     DA(c->V, (size_t)(m + 1) * c->ldv);
     CK(cudaMemsetAsync(c->V, 0, (size_t)(m + 1) * c->ldv * sizeof(double), c->stream));
   }
-  if (kind == VEM_PRECOND_BLOCK_REG && c->zcap < m) {
+  if (is_flexible(kind) && c->zcap < m) {
     if (c->Z) dfree(c, c->Z);
     c->Z = nullptr;
     DA(c->Z, (size_t)m * c->ldv);
@@ -903,6 +977,8 @@ int ensure_work(Ctx *c, int kind) {
   return ensure_part(c, (long)c->sm_count * 2 * ((m + 2 + VEM_DOT_CHUNK - 1) / VEM_DOT_CHUNK + 1) * VEM_DOT_CHUNK +
                             (long)c->sm_count * 64 * 2 + grid_for(c->n * 32) + 1024);
 }
+
+int apply_l2_window(Ctx *c, int which = 0);
 
 // caller numbering <-> internal (SELL-C-sigma reordered) numbering of [u; p]
 void to_internal(Ctx *c, const double *in, double *out) {
@@ -923,12 +999,19 @@ void from_internal(Ctx *c, const double *in, double *out_u, double *out_p) {
 int solve_impl(Ctx *c, const double *rhs, double tol, int maxit, int kind, double *out_u, double *out_p,
                vem_solve_report *rep) {
   vem_solve_report R{};
-  if (kind < 0 || kind > 3) return fail(c, VEM_ERR_PRECOND, "unsupported precond_kind %d", kind);
+  if (kind < 0 || kind > 4) return fail(c, VEM_ERR_PRECOND, "unsupported precond_kind %d", kind);
   if (kind == VEM_PRECOND_BLOCK_REG && !c->has_reg)
     return fail(c, VEM_ERR_PRECOND, "Block-Reg needs eps > 0 at upload");
   if (!rhs || !out_u || !out_p || maxit < 0 || !(tol > 0)) return fail(c, VEM_ERR_INVALID, "invalid solve arguments");
   int rc = ensure_work(c, kind);
   if (rc) return rc;
+  {  // the L2-persisting window covers the fine-level pool of the precision this kind runs in
+    const int pool = kind == VEM_PRECOND_BLOCK_SCHUR_AMG_F32 ? 1 : 0;
+    if (c->opts.l2_persist && c->l2_window_pool != pool) {
+      rc = apply_l2_window(c, pool);
+      if (rc) return rc;
+    }
+  }
   cudaEvent_t e0, e1;
   CK(cudaEventCreate(&e0));
   CK(cudaEventCreate(&e1));
@@ -940,7 +1023,7 @@ int solve_impl(Ctx *c, const double *rhs, double tol, int maxit, int kind, doubl
   g0.m = c->opts.restart;
   g0.maxit = maxit;
   g0.tol_abs = 0.0;
-  g0.flexible = kind == VEM_PRECOND_BLOCK_REG;
+  g0.flexible = is_flexible(kind);
   CK(cudaMemcpyAsync(&c->hst->g, &g0, sizeof(g0), cudaMemcpyHostToDevice, c->stream));
   CK(cudaMemcpyAsync(&c->st->g, &c->hst->g, sizeof(g0), cudaMemcpyHostToDevice, c->stream));
   CK(cudaStreamSynchronize(c->stream));
@@ -1194,9 +1277,14 @@ int build_schur(Ctx *c, const int64_t *brp, const int *bci, const double *bva, c
 // 126 MB L2 across the d-1 steps of an apply, so each step streams only S_D
 // from HBM: a persisting access-policy window on the library stream (captured
 // into the graph kernel nodes).  opts.l2_persist = 0 disables it.
-int apply_l2_window(Ctx *c) {
+// which = 0: the FP64 Chebyshev / AMG fine-level pool; 1: the FP32 pool of kind 4
+int apply_l2_window(Ctx *c, int which) {
   cudaStreamAttrValue attr{};
-  if (!c->opts.l2_persist || !c->cheb_pool) {
+  void *pool = which ? (void *)c->f32_pool : (void *)c->cheb_pool;
+  const size_t pool_bytes = which ? c->f32_pool_bytes : c->cheb_pool_bytes;
+  if (c->l2_window_pool >= 0 && c->l2_window_pool != which) cudaCtxResetPersistingL2Cache();
+  c->l2_window_pool = which;
+  if (!c->opts.l2_persist || !pool) {
     attr.accessPolicyWindow.num_bytes = 0;
     cudaStreamSetAttribute(c->stream, cudaStreamAttributeAccessPolicyWindow, &attr);
     c->l2_window_bytes = 0;
@@ -1207,10 +1295,10 @@ int apply_l2_window(Ctx *c) {
   CK(cudaDeviceGetAttribute(&maxp, cudaDevAttrMaxPersistingL2CacheSize, dev));
   CK(cudaDeviceGetAttribute(&maxw, cudaDevAttrMaxAccessPolicyWindowSize, dev));
   if (maxp <= 0 || maxw <= 0) return 0;
-  const size_t win = std::min(c->cheb_pool_bytes, (size_t)maxw);
+  const size_t win = std::min(pool_bytes, (size_t)maxw);
   const size_t setaside = std::min(win, (size_t)maxp);
   CK(cudaDeviceSetLimit(cudaLimitPersistingL2CacheSize, setaside));
-  attr.accessPolicyWindow.base_ptr = c->cheb_pool;
+  attr.accessPolicyWindow.base_ptr = pool;
   attr.accessPolicyWindow.num_bytes = win;
   attr.accessPolicyWindow.hitRatio = (float)std::min(1.0, (double)setaside / (double)win);
   attr.accessPolicyWindow.hitProp = cudaAccessPropertyPersisting;
@@ -1614,8 +1702,7 @@ int amg_sa_level(Ctx *c, AmgLevel &L, long nc, AmgLevel &C) {
     long tn = 0;
     int r = sort_reduce_csr(c, k0, v0, L.pnnz, nc, n, &L.ptrp, &L.ptci, &L.ptva, &tn);
     if (r) return r;
-    long ps = 0;
-    r = build_sell(c, n, L.prp, L.pci, L.pva, &L.psoff, &L.psci, &L.psva, &ps);
+    r = build_sell(c, n, L.prp, L.pci, L.pva, &L.psoff, &L.psci, &L.psva, &L.psnnz);
     if (r) return r;
   }
   L.sa = true;
@@ -1754,6 +1841,59 @@ int build_amg(Ctx *c) {
     if (read_back(c, c->derr)) return fail(c, VEM_ERR_DIAG_S, "coarsest S_D level not positive definite");
   }
   CK(cudaStreamSynchronize(c->stream));
+  return 0;
+}
+
+// FP32 mirror of the hierarchy for precond kind 4 (values rounded once; own vectors)
+int build_amg_f32(Ctx *c) {
+  auto cvt = [&](const double *in, long n, float **out) -> int {
+    if (!in || n <= 0) return 0;
+    DA(*out, n);
+    k_d2f<<<grid_stream(c, n), NT, 0, c->stream>>>(n, in, *out);
+    return 0;
+  };
+  for (size_t l = 0; l < c->amg.size(); ++l) {
+    AmgLevel &L = c->amg[l];
+    int r;
+    if ((r = cvt(L.sva, l == 0 ? c->nnzS_sell : L.nnz_sell, &L.sva_f))) return r;
+    if ((r = cvt(L.va, L.nnz, &L.va_f))) return r;
+    if ((r = cvt(L.dinv, L.n, &L.dinv_f))) return r;
+    if (L.sa) {
+      if ((r = cvt(L.psva, L.psnnz, &L.psva_f))) return r;
+      if ((r = cvt(L.ptva, L.pnnz, &L.ptva_f))) return r;
+    }
+    if (l == 0) {   // fine level: one contiguous pool (D^-1, r, d0, d1, x, b, t) for the L2 window
+      const long npad = (L.n + 63) / 64 * 64;
+      DA(c->f32_pool, 7 * npad);
+      c->f32_pool_bytes = (size_t)7 * npad * sizeof(float);
+      float *q = c->f32_pool;
+      CK(cudaMemcpyAsync(q, L.dinv_f, L.n * sizeof(float), cudaMemcpyDeviceToDevice, c->stream));
+      CK(cudaStreamSynchronize(c->stream));
+      dfree(c, L.dinv_f);
+      L.dinv_f = q;
+      L.sr_f = q + npad;
+      L.sd0_f = q + 2 * npad;
+      L.sd1_f = q + 3 * npad;
+      L.x_f = q + 4 * npad;
+      L.b_f = q + 5 * npad;
+      L.t_f = q + 6 * npad;
+      continue;
+    }
+    DA(L.b_f, L.n);
+    DA(L.x_f, L.n);
+    DA(L.t_f, L.n);
+    DA(L.sr_f, L.n);
+    DA(L.sd0_f, L.n);
+    DA(L.sd1_f, L.n);
+  }
+  if (c->amg_dense) {
+    const long nc = c->amg.back().n;
+    int r = cvt(c->amg_cinv, nc * nc, &c->amg_cinv_f);
+    if (r) return r;
+  }
+  CKL();
+  CK(cudaStreamSynchronize(c->stream));
+  c->amg_f32 = true;
   return 0;
 }
 
@@ -1989,8 +2129,10 @@ int upload_impl(Ctx *c, const vem_csr *M, const vem_csr *B, const vem_csr *W, do
   }
   CK(cudaStreamSynchronize(c->stream));
   phase("block inverses, SELL");
-  if (c->nb == 1) {   // S_D hierarchy for precond kind 3 (k = 0)
+  if (c->nb == 1) {   // S_D hierarchy for precond kinds 3 and 4 (k = 0)
     int rr = build_amg(c);
+    if (rr) return rr;
+    rr = build_amg_f32(c);
     if (rr) return rr;
   }
   phase("AMG hierarchy");
@@ -2346,7 +2488,7 @@ int vem_mixed_schur_spmv(vem_ctx *h, const double *x, double *y) {
 int vem_mixed_precond_apply(vem_ctx *h, int32_t kind, const double *v, double *z, int64_t *inner_its) {
   if (!h || !v || !z) return VEM_ERR_INVALID;
   Ctx *c = h->impl;
-  if (kind < 0 || kind > 3) return fail(c, VEM_ERR_PRECOND, "unsupported precond_kind %d", kind);
+  if (kind < 0 || kind > 4) return fail(c, VEM_ERR_PRECOND, "unsupported precond_kind %d", kind);
   if (kind == VEM_PRECOND_BLOCK_REG && !c->has_reg) return fail(c, VEM_ERR_PRECOND, "Block-Reg needs eps > 0");
   int64_t its = 0;
   int r = enter(c);

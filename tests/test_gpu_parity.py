@@ -241,6 +241,29 @@ def test_amg_hierarchy_matches_oracle(name):
     sv.close()
 
 
+@pytest.mark.parametrize("name", ["C1", "C3s"])
+def test_amg_fp32_vcycle_parity(name):
+    """Precond kind 4: the same hierarchy with the V-cycle in
+    FP32 inside FP64 FGMRES.  The apply agrees with the oracle's float32 V-cycle to
+    FP32 accuracy, and the solve reaches the FP64 tolerance with the oracle's count."""
+    s = system(name)
+    cfg = configs.CONFIGS[name]
+    sv = solver_for(s, restart=cfg.restart)
+    P = O.Preconditioner(O.PRECOND_BLOCK_SCHUR_AMG_F32, s.M, s.B)
+    v = RNG.normal(size=s.n)
+    z, _ = sv.precond_apply(pkg.PRECOND_BLOCK_SCHUR_AMG_F32, torch.from_numpy(v).cuda())
+    zo = P.apply(v)
+    nu = s.layout.n_u
+    assert rel_inf(z.cpu().numpy()[:nu], zo[:nu]) <= 1e-12
+    assert rel_inf(z.cpu().numpy()[nu:], zo[nu:]) <= 2e-5
+    ref, lo, hi = oracle_iteration_band(s, 4, cfg.restart, 0.0)
+    res = sv.solve(torch.from_numpy(s.rhs).cuda(), 1e-10, 10000, 4)
+    assert res.report["converged"] == 1
+    assert lo - 2 <= res.report["iterations"] <= hi + 2, (res.report["iterations"], lo, hi)
+    assert rel_inf(res.u.cpu().numpy(), ref.x[:nu]) <= 1e-8 and rel_inf(res.p.cpu().numpy(), ref.x[nu:]) <= 1e-8
+    sv.close()
+
+
 def test_solve_host_matches_device_and_is_deterministic():
     s = system("C3s")
     sv = solver_for(s, restart=50)

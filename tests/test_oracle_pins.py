@@ -261,6 +261,25 @@ def test_amg_smoothed_prolongator():
     assert np.abs(SE - SE.T).max() <= 1e-8 * np.abs(SD.toarray()).max()
 
 
+def test_amg_fp32_vcycle_is_the_fp64_one_to_fp32_accuracy():
+    """Kind 4 rounds the hierarchy to FP32 and runs the V-cycle in FP32: its output
+    equals the FP64 V-cycle's to a few FP32 units (a dropped cast or a wrong operand
+    would show at O(1)), and FGMRES (the FP32 apply is not exactly linear) with it
+    reaches the FP64 tolerance in the FP64 preconditioner's iteration count."""
+    from oracle import amg
+    s, SD = _c3s_sd()
+    h = amg.AMG(SD)
+    h32 = h.to_float32()
+    b = RNG.normal(size=SD.shape[0])
+    x64 = h.vcycle(b)
+    x32 = h32.vcycle(b.astype(np.float32))
+    assert x32.dtype == np.float32
+    assert np.abs(x32 - x64).max() <= 1e-5 * np.abs(x64).max()
+    r3 = O.solve(s.M, s.B, s.rhs, O.PRECOND_BLOCK_SCHUR_AMG, 1e-10, 50)
+    r4 = O.solve(s.M, s.B, s.rhs, O.PRECOND_BLOCK_SCHUR_AMG_F32, 1e-10, 50)
+    assert r4.converged and r4.rel_residual_true <= 1e-10 and abs(r4.iterations - r3.iterations) <= 2
+
+
 def test_block_schur_amg_gmres_vs_lu():
     for name in ("C1", "C3s"):
         s = configs.CONFIGS[name].build()
