@@ -281,3 +281,36 @@ def test_patch_test_linear_pressure(k):
     xP, h = cls.centroid, cls.h
     assert np.abs(pc[:, 0] - pfun(xP)).max() < 1e-8
     assert np.abs(pc[:, 1:4] - h[:, None] * grad[None, :]).max() < 1e-8
+
+
+def test_class_templates_recombine_to_the_assembled_system():
+    """The shape cache handed to the device assembly (class_template) recombines on the
+    host into exactly the M, B, f that build_system assembles (C5s: cube and pair
+    classes; C4s: k = 2), and Kuhn tetrahedra are refused (not congruent)."""
+    import numpy as np
+    import scipy.sparse as sp
+    from vemgen import configs
+    from vemgen.assemble import class_templates
+    for name in ("C5s", "C4s"):
+        cfg = configs.CONFIGS[name]
+        s = cfg.build()
+        rows, cols, vals, brows, bcols, bvals = [], [], [], [], [], []
+        f = np.zeros(s.layout.n_p)
+        for t in class_templates(cfg.make_mesh(), cfg.k):
+            c = t["coef"]
+            v = (c[:, 0, None] * t["A"][0] + c[:, 1, None] * t["A"][1] + c[:, 2, None] * t["A"][2]
+                 + c[:, 3, None] * t["S"])
+            rows.append(t["L"][:, t["ii"]].ravel()); cols.append(t["L"][:, t["jj"]].ravel()); vals.append(v.ravel())
+            brows.append(t["P"][:, t["bi"]].ravel()); bcols.append(t["L"][:, t["bj"]].ravel())
+            bvals.append(np.broadcast_to(t["B"], (t["L"].shape[0], len(t["bi"]))).ravel())
+            f[t["P"].ravel()] = (-t["vol"][:, None] * (t["F"] @ t["Hinv"].T)).ravel()
+        M = sp.coo_matrix((np.concatenate(vals), (np.concatenate(rows), np.concatenate(cols))),
+                          shape=s.M.shape).tocsr()
+        B = sp.coo_matrix((np.concatenate(bvals), (np.concatenate(brows), np.concatenate(bcols))),
+                          shape=s.B.shape).tocsr()
+        assert abs(M - s.M).max() <= 1e-15 * abs(s.M).max()
+        assert abs(B - s.B).max() == 0.0
+        assert np.abs(f - s.f).max() <= 1e-14 * np.abs(s.f).max()
+    import pytest
+    with pytest.raises(ValueError):
+        class_templates(configs.CONFIGS["C2s"].make_mesh(), 1)
