@@ -242,6 +242,35 @@ typedef struct vem_asm vem_asm;  /* opaque: device CSR of M (n_u x n_u), B (n_p 
  * VEM_ERR_CUDA.  On success *out owns the device arrays. */
 int vem_mixed_assemble(vem_asm **out, const vem_cell_class *classes, int32_t n_classes, int64_t n_u,
                        int64_t n_p, void *cuda_stream);
+/* Non-congruent single-tetrahedron classes (Kuhn meshes, C2), k = 0 or 1: the local
+ * operators themselves (face polynomials, divergence, Pi^0_k via
+ * Props. 1-3 and P:478-490, consistency + dofi-dofi stabilisation; the batched small
+ * dense solves) are computed on the device, one thread per cell, then assembled as
+ * above (same drop, reading R11; same (cell, row, col) emission order).  Host arrays
+ * (vemgen.assemble.tet_class_input), row-major, copied during the call. */
+typedef struct {
+  int32_t k;
+  int64_t n_cells;
+  const double *cell;     /* n_cells x 17: centroid (3), h_P, |P|, the 4 vertices (12)            */
+  const double *faces;    /* n_cells x 4 x 23: v0, v1, v2, normal, e1, e2, centroid, area, h_f     */
+  const double *signs;    /* n_cells x 4 face orientation signs                                   */
+  const double *coef;     /* n_cells x 4: 1/K_x, 1/K_y, 1/K_z, s_P                                */
+  const int32_t *dof;     /* n_cells x n_loc                                                       */
+  const int32_t *pdof;    /* n_cells x n_p                                                         */
+  const double *F;        /* n_cells x n_p source moments                                          */
+  int32_t n_qv;           /* reference tetrahedron rule: n_qv x 4 (s, t, r, weight)               */
+  const double *vref;
+  int32_t n_qf;           /* reference triangle rule: n_qf x 3 (s, t, weight)                     */
+  const double *fref;
+  const double *alphas1;  /* dim P_{k+1} x 3 graded-lex exponents                                 */
+  const double *betas;    /* dim P_k(f) x 2                                                        */
+  const double *rgrad;    /* 3 dim P_k x 2: (grad coefficient, index of beta in M_{k+1})          */
+  const double *rcross;   /* 3 dim P_k x 4 x 2: (generator, coefficient), generator -1 = unused  */
+  const double *dgrad;    /* max(dim P_k - 1, 1) x 3 x 2: (alpha_c, index of alpha - e_c), -1    */
+  const double *gens;     /* dim G_k^perp x 2: (component, index of the exponent in M_{k-1})      */
+} vem_tet_class;
+int vem_mixed_assemble_tets(vem_asm **out, const vem_tet_class *classes, int32_t n_classes, int64_t n_u,
+                            int64_t n_p, void *cuda_stream);
 /* nnz of the assembled M and B. */
 int vem_mixed_assembled_info(const vem_asm *a, int64_t *nnz_M, int64_t *nnz_B);
 /* Copy the assembled CSR (int64 indptr, int32 indices, fp64 values; sorted, unique

@@ -78,6 +78,13 @@ class vem_cell_class(C.Structure):
                 ("vol", _PD)]
 
 
+class vem_tet_class(C.Structure):
+    _fields_ = [("k", C.c_int32), ("n_cells", C.c_int64), ("cell", _PD), ("faces", _PD), ("signs", _PD),
+                ("coef", _PD), ("dof", _PI), ("pdof", _PI), ("F", _PD), ("n_qv", C.c_int32), ("vref", _PD),
+                ("n_qf", C.c_int32), ("fref", _PD), ("alphas1", _PD), ("betas", _PD), ("rgrad", _PD),
+                ("rcross", _PD), ("dgrad", _PD), ("gens", _PD)]
+
+
 class vem_kernel_stats(C.Structure):
     _fields_ = [("launches", C.c_int64 * 8), ("ms", C.c_double * 8), ("bytes", C.c_double * 8)]
 
@@ -87,7 +94,7 @@ class vem_kernel_stats(C.Structure):
 
 
 EXPORTS = ["vem_mixed_default_options", "vem_mixed_upload", "vem_mixed_solve", "vem_mixed_solve_host",
-           "vem_mixed_assemble", "vem_mixed_assembled_info", "vem_mixed_assembled_copy",
+           "vem_mixed_assemble", "vem_mixed_assemble_tets", "vem_mixed_assembled_info", "vem_mixed_assembled_copy",
            "vem_mixed_upload_assembled", "vem_mixed_assembled_free",
            "vem_mixed_spmv", "vem_mixed_schur_spmv", "vem_mixed_precond_apply", "vem_mixed_set_options",
            "vem_mixed_get_options", "vem_mixed_get_info", "vem_mixed_get_schur", "vem_mixed_kernel_stats",
@@ -123,6 +130,8 @@ def load_library(path: str = LIB_PATH):
     lib.vem_mixed_kernel_stats.argtypes = [P, C.POINTER(vem_kernel_stats), C.c_int32]
     lib.vem_mixed_amg_level.argtypes = [P, C.c_int32, C.POINTER(C.c_int64), C.POINTER(C.c_int64)]
     lib.vem_mixed_assemble.argtypes = [C.POINTER(P), C.POINTER(vem_cell_class), C.c_int32, C.c_int64, C.c_int64, P]
+    lib.vem_mixed_assemble_tets.argtypes = [C.POINTER(P), C.POINTER(vem_tet_class), C.c_int32, C.c_int64,
+                                            C.c_int64, P]
     lib.vem_mixed_assembled_info.argtypes = [P, C.POINTER(C.c_int64), C.POINTER(C.c_int64)]
     lib.vem_mixed_assembled_copy.argtypes = [P, C.POINTER(C.c_int64), C.POINTER(C.c_int32), D,
                                              C.POINTER(C.c_int64), C.POINTER(C.c_int32), D, D]
@@ -361,13 +370,19 @@ class Assembled:
     """vem_mixed_assemble: element-parallel device assembly of M, B and f from the
     per-class shape caches (vemgen.assemble.class_templates); marshalling only."""
 
-    def __init__(self, templates, n_u: int, n_p: int, stream=None):
+    def __init__(self, templates, n_u: int, n_p: int, stream=None, tets=None):
+        """templates: congruent-class shape caches (vemgen.assemble.class_templates);
+        tets: inputs of single-tetrahedron classes (vemgen.assemble.tet_class_input),
+        whose local operators are computed on the device."""
         import torch
         self._lib = load_library()
         if not torch.cuda.is_available():
             raise VemError("no CUDA device: the VEM assembly has no CPU path")
         stream = stream if stream is not None else torch.cuda.current_stream()
         self._keep = []
+        if tets is not None:
+            self._init_tets(tets, n_u, n_p, stream)
+            return
         arr = (vem_cell_class * len(templates))()
 
         def i32(a):
@@ -394,6 +409,34 @@ class Assembled:
         if rc != 0:
             self._h = None
             raise VemError(f"vem_mixed_assemble: {STATUS.get(rc, rc)}: {self._lib.vem_last_error(None).decode()}")
+        self.n_u, self.n_p = int(n_u), int(n_p)
+
+    def _init_tets(self, tets, n_u, n_p, stream):
+        def i32(a):
+            a = np.ascontiguousarray(a, dtype=np.int32)
+            self._keep.append(a)
+            return a.ctypes.data_as(_PI)
+
+        def f64(a):
+            a = np.ascontiguousarray(a, dtype=np.float64)
+            self._keep.append(a)
+            return a.ctypes.data_as(_PD)
+
+        arr = (vem_tet_class * len(tets))()
+        for q, t in enumerate(tets):
+            arr[q] = vem_tet_class(t["k"], t["L"].shape[0], f64(t["cell"]), f64(t["faces"]), f64(t["signs"]),
+                                   f64(t["coef"]), i32(t["L"]), i32(t["P"]), f64(t["F"]), t["vref"].shape[0],
+                                   f64(t["vref"]), t["fref"].shape[0], f64(t["fref"]), f64(t["alphas1"]),
+                                   f64(t["betas"]), f64(t["rgrad"]), f64(t["rcross"]), f64(t["dgrad"]),
+                                   f64(t["gens"]) if t["gens"].size else None)
+        self._h = C.c_void_p()
+        rc = self._lib.vem_mixed_assemble_tets(C.byref(self._h), arr, len(tets), int(n_u), int(n_p),
+                                               C.c_void_p(stream.cuda_stream))
+        self._keep = []
+        if rc != 0:
+            self._h = None
+            raise VemError(f"vem_mixed_assemble_tets: {STATUS.get(rc, rc)}: "
+                           f"{self._lib.vem_last_error(None).decode()}")
         self.n_u, self.n_p = int(n_u), int(n_p)
 
     def nnz(self):

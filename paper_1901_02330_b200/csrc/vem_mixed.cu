@@ -399,9 +399,6 @@ int grid_blk(Ctx *c, long ne) {
   const long blocks = (blk_warps<NB>(ne) * 32 + 255) / 256;
   return (int)std::max<long>(1, std::min<long>(blocks, (long)c->sm_count * 8));
 }
-inline int grid_resident(Ctx *c, long n) {
-  return (int)std::max<long>(1, std::min<long>((n + NT - 1) / NT, (long)c->sm_count * 8));
-}
 
 template <int NB>
 void BlkInvL<NB>::run(Ctx *c, double shift, double *out) {
@@ -1560,8 +1557,9 @@ int amg_aggregate(Ctx *c, AmgLevel &L, double *diag, double theta, long &nc_out)
 // (key, value) pairs with key = row * ncols + col -> CSR (nrows x ncols): stable radix
 // sort, flags at run starts, in-order run sums (deterministic).  k0 / v0 are consumed
 // (freed).  *row_out (optional) receives the row of every stored entry.
+// m_valid >= 0: the keys hold m - m_valid dropped entries (ASM_DROPPED, sorted last)
 int sort_reduce_csr(Ctx *c, unsigned long long *k0, double *v0, long m, long nrows, long ncols, int **rp_out,
-                    int **ci_out, double **va_out, long *nnz_out, int **row_out = nullptr) {
+                    int **ci_out, double **va_out, long *nnz_out, int **row_out = nullptr, long m_valid = -1) {
   unsigned long long *k1 = nullptr;
   double *v1 = nullptr;
   int *flag = nullptr, *pos = nullptr, *crow = nullptr, *cnt = nullptr;
@@ -1571,6 +1569,7 @@ int sort_reduce_csr(Ctx *c, unsigned long long *k0, double *v0, long m, long nro
   DA(pos, m + 1);
   int bits = 1;
   while ((1ULL << bits) < (unsigned long long)nrows * (unsigned long long)ncols) ++bits;
+  if (m_valid >= 0) bits = 64;   // the drop marker is the largest key
   {
     size_t tb = 0;
     CK(cub::DeviceRadixSort::SortPairs(nullptr, tb, k0, k1, v0, v1, (int)m, 0, bits, c->stream));
@@ -1582,6 +1581,7 @@ int sort_reduce_csr(Ctx *c, unsigned long long *k0, double *v0, long m, long nro
   }
   dfree(c, k0);
   dfree(c, v0);
+  if (m_valid >= 0) m = m_valid;
   k_amg_run_flags<<<grid_stream(c, m), NT, 0, c->stream>>>(m, k1, flag);
   CK(cudaMemsetAsync(flag + m, 0, sizeof(int), c->stream));
   {
@@ -2315,6 +2315,119 @@ static int validate_opts(Ctx *c, const vem_opts *o) {
   return 0;
 }
 
+__global__ void k_count_valid(long m, const unsigned long long *__restrict__ keys, unsigned long long *cnt) {
+  unsigned long long local = 0;
+  for (long i = (long)blockIdx.x * blockDim.x + threadIdx.x; i < m; i += (long)gridDim.x * blockDim.x)
+    local += keys[i] != ASM_DROPPED ? 1ULL : 0ULL;
+  if (local) atomicAdd(cnt, local);
+}
+
+int assemble_tets_impl(Ctx *c, const vem_tet_class *cls, int ncls, long nu, long np, DevCsr &M, DevCsr &B,
+                       double **f) {
+  if (!cls || ncls <= 0 || nu <= 0 || np <= 0) return fail(c, VEM_ERR_INVALID, "empty assembly input");
+  cudaDeviceProp prop;
+  int dev = 0;
+  CK(cudaGetDevice(&dev));
+  CK(cudaGetDeviceProperties(&prop, dev));
+  c->sm_count = prop.multiProcessorCount;
+  long mM = 0, mB = 0;
+  for (int q = 0; q < ncls; ++q) {
+    const vem_tet_class &t = cls[q];
+    if (t.k < 0 || t.k > 1) return fail(c, VEM_ERR_INVALID, "device tetrahedral local operators: k = 0, 1 only");
+    if (t.n_cells <= 0 || !t.cell || !t.faces || !t.signs || !t.coef || !t.dof || !t.pdof || !t.F || !t.vref ||
+        !t.fref || t.n_qv <= 0 || t.n_qf <= 0 || !t.alphas1 || !t.betas || !t.rgrad || !t.rcross || !t.dgrad ||
+        (t.k > 0 && !t.gens))
+      return fail(c, VEM_ERR_INVALID, "tet class %d: NULL pointer or empty size", q);
+    const int nk = dim_pk3(t.k), nloc = 4 * dim_pk2(t.k) + nk - 1 + dim_gp(t.k);
+    for (long i = 0; i < t.n_cells * (long)nloc; ++i)
+      if (t.dof[i] < 0 || t.dof[i] >= nu) return fail(c, VEM_ERR_INVALID, "tet class %d: velocity DOF out of range", q);
+    for (long i = 0; i < t.n_cells * (long)nk; ++i)
+      if (t.pdof[i] < 0 || t.pdof[i] >= np) return fail(c, VEM_ERR_INVALID, "tet class %d: pressure DOF out of range", q);
+    mM += t.n_cells * (long)nloc * nloc;
+    mB += t.n_cells * (long)nk * nloc;
+  }
+  if (mM >= (1L << 31) || mB >= (1L << 31)) return fail(c, VEM_ERR_INVALID, "too many local entries");
+  unsigned long long *kM = nullptr, *kB = nullptr, *cnt = nullptr;
+  double *vM = nullptr, *vB = nullptr;
+  DA(kM, mM);
+  DA(vM, mM);
+  DA(kB, mB);
+  DA(vB, mB);
+  DA(cnt, 2);
+  DA(*f, np);
+  CK(cudaMemsetAsync(*f, 0, np * sizeof(double), c->stream));
+  CK(cudaMemsetAsync(cnt, 0, 2 * sizeof(unsigned long long), c->stream));
+  long oM = 0, oB = 0;
+  for (int q = 0; q < ncls; ++q) {
+    const vem_tet_class &t = cls[q];
+    const long ne = t.n_cells;
+    const int nk = dim_pk3(t.k), nk1 = dim_pk3(t.k + 1), nf = dim_pk2(t.k), ng = dim_gp(t.k);
+    const int nloc = 4 * nf + nk - 1 + ng;
+    double *cell = nullptr, *faces = nullptr, *signs = nullptr, *coef = nullptr, *F = nullptr, *vref = nullptr,
+           *fref = nullptr, *al1 = nullptr, *bet = nullptr, *rg = nullptr, *rc = nullptr, *dg = nullptr,
+           *gens = nullptr;
+    int *dof = nullptr, *pdof = nullptr;
+    int r;
+    if ((r = upload_array(c, &cell, t.cell, ne * 17))) return r;
+    if ((r = upload_array(c, &faces, t.faces, ne * 4 * 23))) return r;
+    if ((r = upload_array(c, &signs, t.signs, ne * 4))) return r;
+    if ((r = upload_array(c, &coef, t.coef, ne * 4))) return r;
+    if ((r = upload_array(c, &F, t.F, ne * nk))) return r;
+    if ((r = upload_array(c, &dof, t.dof, ne * nloc))) return r;
+    if ((r = upload_array(c, &pdof, t.pdof, ne * nk))) return r;
+    if ((r = upload_array(c, &vref, t.vref, 4L * t.n_qv))) return r;
+    if ((r = upload_array(c, &fref, t.fref, 3L * t.n_qf))) return r;
+    if ((r = upload_array(c, &al1, t.alphas1, 3L * nk1))) return r;
+    if ((r = upload_array(c, &bet, t.betas, 2L * nf))) return r;
+    if ((r = upload_array(c, &rg, t.rgrad, 6L * nk))) return r;
+    if ((r = upload_array(c, &rc, t.rcross, 24L * nk))) return r;
+    if ((r = upload_array(c, &dg, t.dgrad, 6L * std::max(nk - 1, 1)))) return r;
+    if (ng > 0 && (r = upload_array(c, &gens, t.gens, 2L * ng))) return r;
+    const int blocks = (int)((ne + 63) / 64);
+    if (t.k == 0)
+      k_local_tet<0><<<blocks, 64, 0, c->stream>>>(ne, cell, faces, signs, coef, dof, pdof, F, vref, t.n_qv, fref,
+                                                    t.n_qf, al1, bet, rg, rc, dg, gens, nu, kM + oM, vM + oM,
+                                                    kB + oB, vB + oB, *f);
+    else
+      k_local_tet<1><<<blocks, 64, 0, c->stream>>>(ne, cell, faces, signs, coef, dof, pdof, F, vref, t.n_qv, fref,
+                                                    t.n_qf, al1, bet, rg, rc, dg, gens, nu, kM + oM, vM + oM,
+                                                    kB + oB, vB + oB, *f);
+    CKL();
+    CK(cudaStreamSynchronize(c->stream));
+    for (void *p : {(void *)cell, (void *)faces, (void *)signs, (void *)coef, (void *)F, (void *)dof, (void *)pdof,
+                    (void *)vref, (void *)fref, (void *)al1, (void *)bet, (void *)rg, (void *)rc, (void *)dg,
+                    (void *)gens})
+      dfree(c, p);
+    oM += ne * (long)nloc * nloc;
+    oB += ne * (long)nk * nloc;
+  }
+  k_count_valid<<<grid_stream(c, mM), NT, 0, c->stream>>>(mM, kM, cnt);
+  k_count_valid<<<grid_stream(c, mB), NT, 0, c->stream>>>(mB, kB, cnt + 1);
+  CKL();
+  unsigned long long nv[2];
+  CK(cudaMemcpyAsync(nv, cnt, sizeof(nv), cudaMemcpyDeviceToHost, c->stream));
+  CK(cudaStreamSynchronize(c->stream));
+  dfree(c, cnt);
+  int *rp32 = nullptr;
+  int r = sort_reduce_csr(c, kM, vM, mM, nu, nu, &rp32, &M.ci, &M.va, &M.nnz, nullptr, (long)nv[0]);
+  if (r) return r;
+  DA(M.rp, nu + 1);
+  k_widen64<<<grid_stream(c, nu + 1), NT, 0, c->stream>>>(nu + 1, rp32, M.rp);
+  CK(cudaStreamSynchronize(c->stream));
+  dfree(c, rp32);
+  M.nrows = nu;
+  M.ncols = nu;
+  r = sort_reduce_csr(c, kB, vB, mB, np, nu, &rp32, &B.ci, &B.va, &B.nnz, nullptr, (long)nv[1]);
+  if (r) return r;
+  DA(B.rp, np + 1);
+  k_widen64<<<grid_stream(c, np + 1), NT, 0, c->stream>>>(np + 1, rp32, B.rp);
+  CK(cudaStreamSynchronize(c->stream));
+  dfree(c, rp32);
+  B.nrows = np;
+  B.ncols = nu;
+  return 0;
+}
+
 static Ctx *new_ctx(const vem_opts *opts, void *stream, int *rc) {
   Ctx *c = new Ctx();
   vem_mixed_default_options(&c->opts);
@@ -2379,6 +2492,27 @@ int vem_mixed_assemble(vem_asm **out, const vem_cell_class *classes, int32_t n_c
   a->impl = c;
   if (!r) r = enter(c);
   if (!r) r = assemble_impl(c, classes, n_classes, n_u, n_p, a->M, a->B, &a->f);
+  if (c->stream) leave(c, r);
+  if (r) {
+    g_last_err = c->err;
+    destroy_ctx(c);
+    delete a;
+    return r;
+  }
+  *out = a;
+  return VEM_OK;
+}
+
+int vem_mixed_assemble_tets(vem_asm **out, const vem_tet_class *classes, int32_t n_classes, int64_t n_u,
+                            int64_t n_p, void *stream) {
+  if (!out) return VEM_ERR_INVALID;
+  *out = nullptr;
+  int r = 0;
+  Ctx *c = new_ctx(nullptr, stream, &r);
+  vem_asm *a = new vem_asm();
+  a->impl = c;
+  if (!r) r = enter(c);
+  if (!r) r = assemble_tets_impl(c, classes, n_classes, n_u, n_p, a->M, a->B, &a->f);
   if (c->stream) leave(c, r);
   if (r) {
     g_last_err = c->err;

@@ -189,6 +189,79 @@ def class_template(mesh, cls, ops, k: int, source=None) -> dict:
                 F=F, Hinv=np.broadcast_to(Hinv, (E, nk, nk))[0], vol=cls.vol)
 
 
+def tet_class_input(mesh, cls, k: int, source=None) -> dict:
+    """Per-cell input of the device computation of the local operators for a class of
+    single tetrahedra (Kuhn meshes, C2; vem_mixed_assemble_tets): geometry, the
+    reference quadrature rules, the symbolic tables of Props. 1-3 / P:478-490 and the
+    generator basis, DOF maps, per-cell coefficients and source moments.  The local
+    matrices themselves (the batched small dense Pi / Div solves of local_operators)
+    are then computed on the device, one thread per cell."""
+    assert cls.vol_kind == "tet" and not cls.congruent and cls.n_faces == 4
+    nf = poly.dim_pk_2d(k)
+    nk = poly.dim_pk_3d(k)
+    n_int = (nk - 1) + poly.dim_gperp(k)
+    E = cls.cell_ids.shape[0]
+    fd = (cls.face_ids[:, :, None] * nf + np.arange(nf)[None, None, :]).reshape(E, -1)
+    idofs = mesh.n_faces * nf + cls.cell_ids[:, None] * n_int + np.arange(n_int)[None, :]
+    L = np.concatenate([fd, idofs], axis=1)
+    P = cls.cell_ids[:, None] * nk + np.arange(nk)[None, :]
+    invK = 1.0 / mesh.K[cls.cell_ids]
+    sP = cls.vol * invK.mean(axis=1)
+    # faces: v0, v1, v2, normal, e1, e2, centroid (3 each), area, h
+    fg = np.zeros((E, 4, 23))
+    for lf, f in enumerate(cls.faces):
+        fg[:, lf, :] = np.concatenate([f.v0, f.v1, f.v2, f.normal, f.e1, f.e2, f.centroid,
+                                       f.area[:, None], f.h[:, None]], axis=1)
+    cell = np.concatenate([cls.centroid, cls.h[:, None], cls.vol[:, None], cls.tet_verts.reshape(E, 12)], axis=1)
+    # reference rules (the same collapsed Gauss-Legendre rules as quad.tet_rule / triangle_rule)
+    from .quad import gauss_legendre_01, npts_for_degree
+    q = 2 * k + 2
+    n3 = npts_for_degree(q, 2)
+    x, w = gauss_legendre_01(n3)
+    U, V, Wc = (a.reshape(-1) for a in np.meshgrid(x, x, x, indexing="ij"))
+    Wt = (w[:, None, None] * w[None, :, None] * w[None, None, :]).reshape(-1) * (1.0 - U) ** 2 * (1.0 - V)
+    vref = np.stack([U, (1.0 - U) * V, (1.0 - U) * (1.0 - V) * Wc, Wt], axis=1)
+    n2 = npts_for_degree(q, 1)
+    x2, w2 = gauss_legendre_01(n2)
+    U2, V2 = (a.reshape(-1) for a in np.meshgrid(x2, x2, indexing="ij"))
+    W2 = (w2[:, None] * w2[None, :]).reshape(-1) * (1.0 - U2)
+    fref = np.stack([U2, (1.0 - U2) * V2, W2], axis=1)
+    # symbolic tables
+    alphas = poly.multi_indices_3d(k)
+    alphas1 = poly.multi_indices_3d(k + 1)
+    idx1 = poly.index_map_3d(k + 1)
+    imap = poly.index_map_3d(k)
+    gens = poly.generators(k)
+    gen_idx = {gg: i for i, gg in enumerate(gens)}
+    rgrad = np.zeros((3 * nk, 2))                   # (gc, index of beta in M_{k+1}) per R row
+    rcross = np.zeros((3 * nk, 4, 2))               # up to 4 (generator, coef) per R row; generator -1 = none
+    rcross[..., 0] = -1
+    for c in range(3):
+        for a, alpha in enumerate(alphas):
+            gc, beta, cross = poly.decompose_vector_monomial(c, alpha)
+            rgrad[c * nk + a] = (gc, idx1[beta])
+            terms = {}
+            for coef, cc, al in cross:
+                for coef2, c2, al2 in poly.cross_term_as_generators(cc, al):
+                    g = gen_idx[(c2, al2)]
+                    terms[g] = terms.get(g, 0.0) + coef * coef2
+            assert len(terms) <= 4
+            for t, (g, v) in enumerate(sorted(terms.items())):
+                rcross[c * nk + a, t] = (g, v)
+    dgrad = np.full((max(nk - 1, 1), 3, 2), -1.0)   # per gradient DOF a >= 1, component c: (alpha_c, imap[a - e_c])
+    for a in range(1, nk):
+        for c in range(3):
+            if alphas[a][c] > 0:
+                am = list(alphas[a])
+                am[c] -= 1
+                dgrad[a - 1, c] = (alphas[a][c], imap[tuple(am)])
+    gtab = np.array([(c2, imap[al]) for c2, al in gens], dtype=np.float64).reshape(-1, 2)
+    return dict(k=k, L=L, P=P, coef=np.concatenate([invK, sP[:, None]], axis=1), cell=cell, faces=fg,
+                signs=cls.face_signs.astype(np.float64), F=source_moments(cls, k, source), vref=vref, fref=fref,
+                alphas1=np.array(alphas1, dtype=np.float64), betas=np.array(poly.multi_indices_2d(k), dtype=np.float64),
+                rgrad=rgrad, rcross=rcross, dgrad=dgrad, gens=gtab)
+
+
 def class_templates(mesh, k: int, source=None) -> list:
     """Shape caches of every cell class (the input of vem_mixed_assemble); all
     classes must be congruent (cube grids, cube pairs).  Kuhn tetrahedra (C2) are
