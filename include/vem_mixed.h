@@ -168,7 +168,14 @@ int vem_mixed_upload(vem_ctx **ctx, const vem_csr *M, const vem_csr *B, const ve
  * checked every step, confirmed by the true residual at each cycle end).
  * rhs (n_u + n_p), out_u (n_u), out_p (n_p): caller-owned DEVICE pointers
  * (never freed by the library).  maxit caps the total Arnoldi steps.  The
- * stream is synchronised before return.  report (host) may be NULL. */
+ * stream is synchronised before return.  report (host) may be NULL.
+ * precond_kind (readings R15-R17, R22):
+ *   0 none; 1 Block-Schur, B_2^-1 by degree-d Chebyshev on S_D (GMRES);
+ *   2 Block-Reg, Woodbury with an inner PCG (FGMRES, CGS2);
+ *   3 Block-Schur, B_2^-1 by one smoothed-aggregation V-cycle on S_D (GMRES; n_p_dof = 1);
+ *   4 kind 3 with the V-cycle in FP32 (FGMRES; n_p_dof = 1).
+ * Errors: VEM_ERR_PRECOND for an unknown kind, kind 2 without eps > 0, kinds 3/4
+ * without the hierarchy (n_p_dof > 1); VEM_ERR_INNER if the inner PCG fails. */
 int vem_mixed_solve(vem_ctx *ctx, const double *rhs, double tol, int32_t maxit,
                     int32_t precond_kind, double *out_u, double *out_p,
                     vem_solve_report *report);
