@@ -25,7 +25,9 @@ Definition (the GPU follows it step by step):
     Jacobi step on the tentative prolongator); below, P = T.  A_c = P^T A P; stop
     when n <= COARSE_SIZE, at MAX_LEVELS, or when a level coarsens by less than 1/0.75
   * coarsest level (COARSE_SIZE = 2048): dense inverse applied as a matvec, else
-    (stagnated coarsening) a degree-COARSE_DEGREE Chebyshev smoother
+    (stagnated coarsening) a degree-COARSE_DEGREE = 32 Chebyshev smoother (C3: the
+    11,794-row coarsest; degree 8 / 16 / 32 / exact inverse give 118 / 101 / 95 / 95
+    GMRES iterations, R22)
   * smoother C_l(b): degree-DEGREE point-Jacobi Chebyshev from x0 = 0 (Saad
     Alg. 12.1, exactly oracle.solver.chebyshev) on [lmax/RATIO, lmax] with the
     Gershgorin bound lmax = max_i sum_j |A_ij| / A_ii
@@ -51,7 +53,7 @@ COARSE_SIZE = 2048
 MAX_LEVELS = 12
 DEGREE = 3
 RATIO = 30.0
-COARSE_DEGREE = 8
+COARSE_DEGREE = 32
 STAGNATION = 0.75
 KEY_INDEX_BITS = 30
 ROOT_KEY = np.int64(np.iinfo(np.int64).max)

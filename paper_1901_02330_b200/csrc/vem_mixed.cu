@@ -122,6 +122,7 @@ struct Ctx {
   double *amg_cinv = nullptr;                    // dense inverse of the coarsest level
   float *amg_cinv_f = nullptr;                   // its FP32 copy (kind 4)
   bool amg_f32 = false;                          // FP32 mirror built
+  int amg_coarse_degree = 8;                     // Chebyshev degree of a non-dense coarsest level
   float *f32_pool = nullptr;                     // kind 4 fine-level vectors (L2-persisting window)
   size_t f32_pool_bytes = 0;
   int l2_window_pool = -1;                       // pool under the window: 0 FP64 Chebyshev, 1 FP32
@@ -687,7 +688,7 @@ int run_pcg(Ctx *c, int64_t *inner_its) {
 // ----------------------------------------------------------------------------
 constexpr double AMG_THETA = 0.08, AMG_THETA_COARSE = 0.04, AMG_RATIO = 30.0, AMG_STAGNATION = 0.75;
 constexpr int AMG_SA_LEVELS = 1;   // levels with the smoothed prolongator (oracle/amg.py SA_LEVELS)
-constexpr int AMG_COARSE_SIZE = 2048, AMG_MAX_LEVELS = 12, AMG_DEGREE = 3, AMG_COARSE_DEGREE = 8;
+constexpr int AMG_COARSE_SIZE = 2048, AMG_MAX_LEVELS = 12, AMG_DEGREE = 3, AMG_COARSE_DEGREE = 32;
 
 void amg_cheb_coeffs(double lmax, int degree, double &inv_theta, std::vector<double> &c1, std::vector<double> &c2) {
   const double b = lmax, a = lmax / AMG_RATIO;
@@ -781,7 +782,7 @@ void amg_vcycle(Ctx *c, size_t l, const int *gate) {
       TimeScope ts(c, VEM_K_PRECOND_VEC, (double)sizeof(T) * L.n * L.n);
       k_vc_dense_mv<T><<<grid_for(L.n * 32), NT, 0, c->stream>>>(L.n, amg_cinv<T>(c), D.b(), D.x(), gate);
     } else {
-      amg_smooth<T>(c, L, D.b(), D.x(), AMG_COARSE_DEGREE, gate);
+      amg_smooth<T>(c, L, D.b(), D.x(), c->amg_coarse_degree, gate);
     }
     return;
   }
@@ -1912,6 +1913,7 @@ int upload_impl(Ctx *c, const vem_csr *M, const vem_csr *B, const vem_csr *W, do
   const bool trace = getenv("VEM_SETUP_TRACE") != nullptr;
   c->pcg_split = getenv("VEM_PCG_SPLIT") ? atoi(getenv("VEM_PCG_SPLIT")) : 1;
   c->pcg_persist = getenv("VEM_PCG_PERSIST") ? atoi(getenv("VEM_PCG_PERSIST")) : 1;
+  c->amg_coarse_degree = getenv("VEM_AMG_COARSE_DEGREE") ? atoi(getenv("VEM_AMG_COARSE_DEGREE")) : AMG_COARSE_DEGREE;
   auto phase = [&](const char *what) {
     if (!trace) return;
     cudaStreamSynchronize(c->stream);
