@@ -121,7 +121,8 @@ typedef struct {
   int32_t amg_levels;             /* levels of the S_D hierarchy (0: kind 3 unavailable)   */
   int64_t amg_coarsest;           /* rows of its coarsest level                            */
   int32_t reordered;              /* 1 if the SELL-C-sigma reordering is active            */
-  int32_t pad3;
+  int32_t amg_coarse_cluster;     /* 1 if the non-dense coarsest level is smoothed by one
+                                     16-CTA thread-block-cluster launch (k_vc_coarse_cluster) */
   int64_t nnz_A_stored, nnz_S_stored; /* stored SELL-32 slots (nonzeros + slice padding)   */
 } vem_info;
 

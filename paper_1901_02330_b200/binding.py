@@ -61,7 +61,7 @@ class vem_info(C.Structure):
                 ("eps", C.c_double), ("spmv_group", C.c_int32), ("schur_group", C.c_int32),
                 ("sm_count", C.c_int32), ("device_bytes", C.c_int64), ("l2_window_bytes", C.c_int64),
                 ("amg_levels", C.c_int32), ("amg_coarsest", C.c_int64), ("reordered", C.c_int32),
-                ("pad3", C.c_int32), ("nnz_A_stored", C.c_int64), ("nnz_S_stored", C.c_int64)]
+                ("amg_coarse_cluster", C.c_int32), ("nnz_A_stored", C.c_int64), ("nnz_S_stored", C.c_int64)]
 
     def as_dict(self):
         return {f: getattr(self, f) for f, _ in self._fields_}

@@ -266,3 +266,127 @@ __global__ void k_d2f(long n, const double *__restrict__ in, float *__restrict__
   for (long i = (long)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (long)gridDim.x * blockDim.x)
     out[i] = (float)in[i];
 }
+
+// ---------------------------------------------------------------------------
+// Coarsest level without a dense inverse (stagnated coarsening; C3: 11,794 rows):
+// the degree-d Chebyshev smoother (oracle/amg.py AMG.vcycle -> smooth(lev, b,
+// COARSE_DEGREE)) as ONE launch of a 16-CTA thread-block cluster instead of d
+// launches.  Each CTA owns a contiguous nnz-balanced row range (at most two rows
+// per thread, r, x, d, D^-1 of its rows in registers) and keeps its CSR slice in
+// shared memory (16-bit columns) for all d-1 steps, together with a full copy of
+// the current direction: the gathers of A d are shared-memory loads.  The new
+// directions are exchanged through two global (L2-resident) buffers: each CTA
+// writes its slice, one cluster barrier (release/acquire at cluster scope), then
+// every CTA copies the whole vector into its shared memory with 16-byte loads.
+// Gathering the directions from L2 or through distributed shared memory instead
+// was bound by the per-SM rate of scattered 8-byte requests (~11k per SM per
+// step on 16 SMs): 3x slower than the per-step launches.
+// ---------------------------------------------------------------------------
+constexpr int VC_CLUSTER = 16;          // CTAs per cluster (non-portable size, B200 allows 16)
+constexpr int VC_CLUSTER_THREADS = 1024;
+constexpr int VC_ROWS_PER_THREAD = 2;
+constexpr int VC_MAX_DEGREE = 64;
+
+struct VcCheb {
+  double inv_theta;
+  int degree;
+  double c1[VC_MAX_DEGREE - 1], c2[VC_MAX_DEGREE - 1];
+};
+
+template <typename T>
+struct VcCluster {
+  const int *rs;              // [VC_CLUSTER + 1] first row of each rank
+  const int *rp;              // level CSR row pointers
+  const unsigned short *c16;  // level CSR columns as 16-bit (n <= 65535)
+  const T *va;
+  const T *dinv, *b;
+  T *x;
+  T *dg0, *dg1;               // direction exchange buffers (n each, global, 16-byte aligned)
+  int n;
+};
+
+// shared-memory bytes of one CTA of the cluster kernel
+template <typename T>
+inline size_t vc_cluster_smem(long n, int rows, long nnz) {
+  const size_t dv = ((size_t)n * sizeof(T) + 15) / 16 * 16;
+  const size_t va = ((size_t)nnz * sizeof(T) + 15) / 16 * 16;
+  const size_t rp = ((size_t)(rows + 1) * 4 + 15) / 16 * 16;
+  return dv + va + rp + 2 * (size_t)nnz + 16;
+}
+
+template <typename T>
+__global__ void __launch_bounds__(VC_CLUSTER_THREADS) k_vc_coarse_cluster(VcCluster<T> P, VcCheb cf,
+                                                                          const int *gate) {
+  if (!*gate) return;   // the gate is uniform: every CTA of the cluster leaves together
+  namespace cg = cooperative_groups;
+  cg::cluster_group cl = cg::this_cluster();
+  const int g = (int)cl.block_rank();
+  const int r0 = P.rs[g], nr = P.rs[g + 1] - r0;
+  const int z0 = P.rp[r0], nz = P.rp[r0 + nr] - z0;
+  extern __shared__ __align__(16) unsigned char vc_smem[];
+  T *sdv = reinterpret_cast<T *>(vc_smem);                                   // full direction
+  T *sva = reinterpret_cast<T *>(vc_smem + ((size_t)P.n * sizeof(T) + 15) / 16 * 16);
+  int *srp = reinterpret_cast<int *>(reinterpret_cast<unsigned char *>(sva) + ((size_t)nz * sizeof(T) + 15) / 16 * 16);
+  unsigned short *scc = reinterpret_cast<unsigned short *>(srp + ((nr + 1 + 3) / 4) * 4);
+  for (int k = threadIdx.x; k < nz; k += blockDim.x) {
+    sva[k] = P.va[z0 + k];
+    scc[k] = P.c16[z0 + k];
+  }
+  for (int i = threadIdx.x; i <= nr; i += blockDim.x) srp[i] = P.rp[r0 + i] - z0;
+  const T it = (T)cf.inv_theta;
+  // x0 = 0: r = b, d_0 = D^-1 b / theta, x = d_0 (Saad Alg. 12.1 as oracle.solver.chebyshev)
+  T rr[VC_ROWS_PER_THREAD], xx[VC_ROWS_PER_THREAD], dd[VC_ROWS_PER_THREAD], di[VC_ROWS_PER_THREAD];
+#pragma unroll
+  for (int q = 0; q < VC_ROWS_PER_THREAD; ++q) {
+    const int i = threadIdx.x + q * VC_CLUSTER_THREADS;
+    rr[q] = xx[q] = dd[q] = di[q] = T(0);
+    if (i < nr) {
+      di[q] = P.dinv[r0 + i];
+      rr[q] = P.b[r0 + i];
+      dd[q] = di[q] * rr[q] * it;
+      xx[q] = dd[q];
+      P.dg0[r0 + i] = dd[q];
+    }
+  }
+  cl.sync();
+  using V4 = uint4;   // 16-byte copy of the exchanged direction into shared memory
+  const int nv = (int)(((size_t)P.n * sizeof(T)) / 16), tail = (int)((size_t)P.n * sizeof(T) - 16 * (size_t)nv);
+  for (int s = 0; s + 1 < cf.degree; ++s) {
+    const T c1 = (T)cf.c1[s], c2 = (T)cf.c2[s];
+    const T *dold = (s & 1) ? P.dg1 : P.dg0;
+    T *dnew = (s & 1) ? P.dg0 : P.dg1;
+    const V4 *src = reinterpret_cast<const V4 *>(dold);
+    V4 *dst = reinterpret_cast<V4 *>(sdv);
+    for (int k = threadIdx.x; k < nv; k += blockDim.x) dst[k] = __ldcg(src + k);
+    if (tail && threadIdx.x < tail / (int)sizeof(T))
+      sdv[16 * nv / sizeof(T) + threadIdx.x] = __ldcg(dold + 16 * nv / sizeof(T) + threadIdx.x);
+    __syncthreads();
+#pragma unroll
+    for (int q = 0; q < VC_ROWS_PER_THREAD; ++q) {
+      const int i = threadIdx.x + q * VC_CLUSTER_THREADS;
+      if (i < nr) {
+        T acc = T(0);
+        const int ke = srp[i + 1];
+#pragma unroll 4
+        for (int k = srp[i]; k < ke; ++k) acc = fma(sva[k], sdv[scc[k]], acc);
+        const T rn = rr[q] - acc;          // r_i = r_{i-1} - A d_{i-1}
+        const T dn = c1 * dd[q] + c2 * (di[q] * rn);
+        rr[q] = rn;
+        dd[q] = dn;
+        xx[q] += dn;
+        dnew[r0 + i] = dn;
+      }
+    }
+    cl.sync();   // every slice of d_new written; every CTA done reading d_old and its shared copy
+  }
+#pragma unroll
+  for (int q = 0; q < VC_ROWS_PER_THREAD; ++q) {
+    const int i = threadIdx.x + q * VC_CLUSTER_THREADS;
+    if (i < nr) P.x[r0 + i] = xx[q];
+  }
+}
+
+__global__ void k_vc_cols16(long nnz, const int *__restrict__ ci, unsigned short *__restrict__ c16) {
+  for (long k = (long)blockIdx.x * blockDim.x + threadIdx.x; k < nnz; k += (long)gridDim.x * blockDim.x)
+    c16[k] = (unsigned short)ci[k];
+}

@@ -64,6 +64,12 @@ struct AmgLevel {
   // FP32 mirror for precond kind 4 (values converted once after setup; own vectors)
   float *sva_f = nullptr, *va_f = nullptr, *dinv_f = nullptr, *psva_f = nullptr, *ptva_f = nullptr;
   float *b_f = nullptr, *x_f = nullptr, *t_f = nullptr, *sr_f = nullptr, *sd0_f = nullptr, *sd1_f = nullptr;
+  // coarsest level without a dense inverse: one thread-block-cluster launch per smoother
+  // (k_vc_coarse_cluster): rank row ranges, packed columns, shared bytes per precision
+  int *vc_rs = nullptr;
+  unsigned short *vc_c16 = nullptr;
+  size_t vc_smem_d = 0, vc_smem_f = 0;
+  bool vc_ok = false;
 };
 
 // level data of the V-cycle in precision T
@@ -123,6 +129,9 @@ struct Ctx {
   float *amg_cinv_f = nullptr;                   // its FP32 copy (kind 4)
   bool amg_f32 = false;                          // FP32 mirror built
   int amg_coarse_degree = 8;                     // Chebyshev degree of a non-dense coarsest level
+  int amg_max_levels = 12;                       // AMG_MAX_LEVELS (VEM_AMG_MAX_LEVELS: tests only)
+  int amg_cluster = 0;                           // coarsest smoother as one cluster launch (VEM_AMG_CLUSTER=1;
+                                                 // off by default: slower than the per-step launches)
   float *f32_pool = nullptr;                     // kind 4 fine-level vectors (L2-persisting window)
   size_t f32_pool_bytes = 0;
   int l2_window_pool = -1;                       // pool under the window: 0 FP64 Chebyshev, 1 FP32
@@ -773,6 +782,38 @@ const double *amg_cinv<double>(Ctx *c) { return c->amg_cinv; }
 template <>
 const float *amg_cinv<float>(Ctx *c) { return c->amg_cinv_f; }
 
+// coarsest-level Chebyshev(d) from x0 = 0 as one 16-CTA cluster launch (k_vc_coarse_cluster)
+template <typename T>
+void amg_coarse_cluster(Ctx *c, AmgLevel &L, const int *gate) {
+  const Lv<T> D{L};
+  double it;
+  std::vector<double> c1, c2;
+  amg_cheb_coeffs(L.lmax, c->amg_coarse_degree, it, c1, c2);
+  VcCheb cf{};
+  cf.inv_theta = it;
+  cf.degree = c->amg_coarse_degree;
+  for (size_t i = 0; i < c1.size(); ++i) {
+    cf.c1[i] = c1[i];
+    cf.c2[i] = c2[i];
+  }
+  const VcCluster<T> P{L.vc_rs, L.rp, L.vc_c16, D.va(), D.dinv(), D.b(), D.x(), D.sd0(), D.sd1(), (int)L.n};
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = dim3(VC_CLUSTER);
+  cfg.blockDim = dim3(VC_CLUSTER_THREADS);
+  cfg.dynamicSmemBytes = sizeof(T) == 8 ? L.vc_smem_d : L.vc_smem_f;
+  cfg.stream = c->stream;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeClusterDimension;
+  at[0].val.clusterDim.x = VC_CLUSTER;
+  at[0].val.clusterDim.y = 1;
+  at[0].val.clusterDim.z = 1;
+  cfg.attrs = at;
+  cfg.numAttrs = 1;
+  // bytes that move from memory: the level's CSR (16-bit columns) and the b, D^-1, x vectors once
+  TimeScope ts(c, VEM_K_CHEB, (sizeof(T) + 2.0) * L.nnz + 4.0 * L.n + 3.0 * sizeof(T) * L.n);
+  cudaLaunchKernelEx(&cfg, k_vc_coarse_cluster<T>, P, cf, gate);
+}
+
 template <typename T>
 void amg_vcycle(Ctx *c, size_t l, const int *gate) {
   AmgLevel &L = c->amg[l];
@@ -781,6 +822,8 @@ void amg_vcycle(Ctx *c, size_t l, const int *gate) {
     if (c->amg_dense) {
       TimeScope ts(c, VEM_K_PRECOND_VEC, (double)sizeof(T) * L.n * L.n);
       k_vc_dense_mv<T><<<grid_for(L.n * 32), NT, 0, c->stream>>>(L.n, amg_cinv<T>(c), D.b(), D.x(), gate);
+    } else if (L.vc_ok) {
+      amg_coarse_cluster<T>(c, L, gate);
     } else {
       amg_smooth<T>(c, L, D.b(), D.x(), c->amg_coarse_degree, gate);
     }
@@ -1775,7 +1818,7 @@ int build_amg(Ctx *c) {
   double *diag = c->sdiag;
   while (true) {
     AmgLevel &L = c->amg.back();
-    if (L.n <= AMG_COARSE_SIZE || (int)c->amg.size() >= AMG_MAX_LEVELS) break;
+    if (L.n <= AMG_COARSE_SIZE || (int)c->amg.size() >= c->amg_max_levels) break;
     long nc = 0;
     const size_t lev = c->amg.size() - 1;
     r = amg_aggregate(c, L, diag, lev == 0 ? AMG_THETA : AMG_THETA_COARSE, nc);
@@ -1842,6 +1885,76 @@ int build_amg(Ctx *c) {
     if (read_back(c, c->derr)) return fail(c, VEM_ERR_DIAG_S, "coarsest S_D level not positive definite");
   }
   CK(cudaStreamSynchronize(c->stream));
+  return 0;
+}
+
+// Coarsest level without a dense inverse: nnz-balanced row ranges of the 16 CTAs of
+// k_vc_coarse_cluster.  Left off (the per-step
+// warp kernels run instead) when the cluster cannot be launched or a rank's slice
+// does not fit in shared memory.
+int build_amg_cluster(Ctx *c) {
+  if (c->amg.empty() || c->amg_dense || !c->amg_cluster) return 0;
+  AmgLevel &L = c->amg.back();
+  if (!L.rp || !L.ci || L.n < VC_CLUSTER || L.n > 65535 || L.nnz >= (1L << 31)) return 0;
+  if (c->amg_coarse_degree < 1 || c->amg_coarse_degree > VC_MAX_DEGREE) return 0;
+  std::vector<int> rp(L.n + 1);
+  CK(cudaMemcpyAsync(rp.data(), L.rp, (L.n + 1) * sizeof(int), cudaMemcpyDeviceToHost, c->stream));
+  CK(cudaStreamSynchronize(c->stream));
+  std::vector<int> rs(VC_CLUSTER + 1);
+  rs[0] = 0;
+  rs[VC_CLUSTER] = (int)L.n;
+  for (int g = 1; g < VC_CLUSTER; ++g) {
+    const long target = (long)rp[L.n] * g / VC_CLUSTER;
+    rs[g] = std::max(rs[g - 1], (int)(std::lower_bound(rp.begin(), rp.end(), (int)target) - rp.begin()));
+    rs[g] = std::min(rs[g], (int)L.n);
+  }
+  size_t sd = 0, sf = 0;
+  for (int g = 0; g < VC_CLUSTER; ++g) {
+    const int nr = rs[g + 1] - rs[g];
+    const long nz = rp[rs[g + 1]] - rp[rs[g]];
+    if (nr > VC_CLUSTER_THREADS * VC_ROWS_PER_THREAD) return 0;
+    sd = std::max(sd, vc_cluster_smem<double>(L.n, nr, nz));
+    sf = std::max(sf, vc_cluster_smem<float>(L.n, nr, nz));
+  }
+  int dev = 0, optin = 0;
+  CK(cudaGetDevice(&dev));
+  CK(cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev));
+  if (sd > (size_t)optin) return 0;
+  auto prep = [&](const void *fn, size_t smem) -> bool {
+    if (cudaFuncSetAttribute(fn, cudaFuncAttributeNonPortableClusterSizeAllowed, 1) != cudaSuccess ||
+        cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) != cudaSuccess) {
+      cudaGetLastError();
+      return false;
+    }
+    cudaLaunchConfig_t cfg{};
+    cfg.gridDim = dim3(VC_CLUSTER);
+    cfg.blockDim = dim3(VC_CLUSTER_THREADS);
+    cfg.dynamicSmemBytes = smem;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeClusterDimension;
+    at[0].val.clusterDim.x = VC_CLUSTER;
+    at[0].val.clusterDim.y = 1;
+    at[0].val.clusterDim.z = 1;
+    cfg.attrs = at;
+    cfg.numAttrs = 1;
+    int nclusters = 0;
+    if (cudaOccupancyMaxActiveClusters(&nclusters, fn, &cfg) != cudaSuccess) {
+      cudaGetLastError();
+      return false;
+    }
+    return nclusters >= 1;
+  };
+  if (!prep((const void *)k_vc_coarse_cluster<double>, sd)) return 0;
+  if (c->amg_f32 && !prep((const void *)k_vc_coarse_cluster<float>, sf)) return 0;
+  DA(L.vc_rs, VC_CLUSTER + 1);
+  DA(L.vc_c16, L.nnz);
+  CK(cudaMemcpyAsync(L.vc_rs, rs.data(), (VC_CLUSTER + 1) * sizeof(int), cudaMemcpyHostToDevice, c->stream));
+  k_vc_cols16<<<grid_stream(c, L.nnz), NT, 0, c->stream>>>(L.nnz, L.ci, L.vc_c16);
+  CKL();
+  CK(cudaStreamSynchronize(c->stream));
+  L.vc_smem_d = sd;
+  L.vc_smem_f = sf;
+  L.vc_ok = true;
   return 0;
 }
 
@@ -1914,6 +2027,8 @@ int upload_impl(Ctx *c, const vem_csr *M, const vem_csr *B, const vem_csr *W, do
   c->pcg_split = getenv("VEM_PCG_SPLIT") ? atoi(getenv("VEM_PCG_SPLIT")) : 1;
   c->pcg_persist = getenv("VEM_PCG_PERSIST") ? atoi(getenv("VEM_PCG_PERSIST")) : 1;
   c->amg_coarse_degree = getenv("VEM_AMG_COARSE_DEGREE") ? atoi(getenv("VEM_AMG_COARSE_DEGREE")) : AMG_COARSE_DEGREE;
+  c->amg_max_levels = getenv("VEM_AMG_MAX_LEVELS") ? atoi(getenv("VEM_AMG_MAX_LEVELS")) : AMG_MAX_LEVELS;
+  c->amg_cluster = getenv("VEM_AMG_CLUSTER") ? atoi(getenv("VEM_AMG_CLUSTER")) : 0;
   auto phase = [&](const char *what) {
     if (!trace) return;
     cudaStreamSynchronize(c->stream);
@@ -2135,6 +2250,8 @@ int upload_impl(Ctx *c, const vem_csr *M, const vem_csr *B, const vem_csr *W, do
     int rr = build_amg(c);
     if (rr) return rr;
     rr = build_amg_f32(c);
+    if (rr) return rr;
+    rr = build_amg_cluster(c);
     if (rr) return rr;
   }
   phase("AMG hierarchy");
@@ -2690,6 +2807,7 @@ int vem_mixed_get_info(vem_ctx *h, vem_info *info) {
   info->l2_window_bytes = (int64_t)c->l2_window_bytes;
   info->amg_levels = (int32_t)c->amg.size();
   info->amg_coarsest = c->amg.empty() ? 0 : c->amg.back().n;
+  info->amg_coarse_cluster = c->amg.empty() ? 0 : (int32_t)c->amg.back().vc_ok;
   info->reordered = c->perm ? 1 : 0;
   info->nnz_A_stored = c->nnzA_sell;
   info->nnz_S_stored = c->nnzS_sell;

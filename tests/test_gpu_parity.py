@@ -264,6 +264,43 @@ def test_amg_fp32_vcycle_parity(name):
     sv.close()
 
 
+# 32^3 C3-type cube system: with VEM_AMG_MAX_LEVELS=2 its coarsest level (the SA
+# Galerkin level, 3,643 rows, 33 nnz/row) is above the dense-inverse size, so the
+# V-cycle ends in the degree-32 Chebyshev coarse smoother (oracle/amg.py AMG.vcycle)
+C3M = configs.Config("C3m", "cube", 32, 0, (3,), 50, block=4, seed=3)
+
+
+@pytest.mark.parametrize("cluster", [1, 0])
+def test_amg_cluster_coarsest(monkeypatch, cluster):
+    """The non-dense coarsest level smoothed by ONE 16-CTA thread-block-cluster launch
+    (k_vc_coarse_cluster: CSR slices in shared memory, directions read through
+    distributed shared memory) against the oracle's Chebyshev(32) coarse solve, FP64
+    and FP32, and against the per-step warp kernels (cluster = 0)."""
+    from oracle.amg import AMG
+    monkeypatch.setenv("VEM_AMG_MAX_LEVELS", "2")
+    monkeypatch.setenv("VEM_AMG_CLUSTER", str(cluster))
+    if "C3m" not in _CACHE:
+        _CACHE["C3m"] = C3M.build()
+    s = _CACHE["C3m"]
+    SD = O.schur_diag(s.M, s.B)
+    h = AMG(SD, max_levels=2)
+    assert h.coarse_inv is None
+    sv = solver_for(s, restart=50)
+    assert sv.amg_levels() == [(lev.A.shape[0], lev.A.nnz) for lev in h.levels]
+    assert sv.info()["amg_coarse_cluster"] == cluster
+    nu = s.layout.n_u
+    v = RNG.normal(size=s.n)
+    z, _ = sv.precond_apply(pkg.PRECOND_BLOCK_SCHUR_AMG, torch.from_numpy(v).cuda())
+    zo = -h.vcycle(v[nu:])
+    assert rel_inf(z.cpu().numpy()[nu:], zo) <= 1e-10
+    z32, _ = sv.precond_apply(pkg.PRECOND_BLOCK_SCHUR_AMG_F32, torch.from_numpy(v).cuda())
+    zo32 = -h.to_float32().vcycle(v[nu:].astype(np.float32)).astype(np.float64)
+    assert rel_inf(z32.cpu().numpy()[nu:], zo32) <= 2e-5
+    res = sv.solve(torch.from_numpy(s.rhs).cuda(), 1e-10, 10000, 3)
+    assert res.report["converged"] == 1 and res.report["rel_residual_true"] <= 1e-10
+    sv.close()
+
+
 def test_solve_host_matches_device_and_is_deterministic():
     s = system("C3s")
     sv = solver_for(s, restart=50)
