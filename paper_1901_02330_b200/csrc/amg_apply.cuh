@@ -34,13 +34,16 @@ __device__ __forceinline__ T warp_sum_t(T v) {
   return v;
 }
 
-template <typename T, typename Gather>
+// one row per group of G lanes (G = 4 .. 32, a power of two): lane-strided CSR entries, xor-shuffle sum
+template <typename T, int G, typename Gather>
 __device__ __forceinline__ T warp_row_dot_t(const int *__restrict__ rp, const int *__restrict__ ci,
                                             const T *__restrict__ va, long row, Gather g) {
-  const int lane = threadIdx.x & 31;
+  const int lane = threadIdx.x & (G - 1);
   T acc = T(0);
-  for (int k = rp[row] + lane; k < rp[row + 1]; k += 32) acc = fma(va[k], g(ci[k]), acc);
-  return warp_sum_t(acc);
+  for (int k = rp[row] + lane; k < rp[row + 1]; k += G) acc = fma(va[k], g(ci[k]), acc);
+#pragma unroll
+  for (int o = G / 2; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+  return acc;
 }
 
 template <typename T>
@@ -84,17 +87,17 @@ __global__ void __launch_bounds__(256) k_vc_cheb_step(long n, SellT<T> A, const 
   d_new[i] = dn;
   x[i] += dn;
 }
-template <typename T>
+template <typename T, int G>
 __global__ void __launch_bounds__(256) k_vc_cheb_step_w(long n, const int *__restrict__ rp, const int *__restrict__ ci,
                                                         const T *__restrict__ va, const T *__restrict__ dinv,
                                                         T *__restrict__ r, const T *__restrict__ d_old,
                                                         T *__restrict__ d_new, T *__restrict__ x, T c1, T c2,
                                                         const int *gate) {
   if (!*gate) return;
-  const long i = ((long)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
-  if (i >= n) return;
-  const T ad = warp_row_dot_t(rp, ci, va, i, GatherT<T>{d_old});
-  if ((threadIdx.x & 31) == 0) {
+  const long i = ((long)blockIdx.x * blockDim.x + threadIdx.x) / G;
+  if ((i & ~(long)(32 / G - 1)) >= n) return;   // whole warps only: the groups of a warp shuffle together
+  const T ad = warp_row_dot_t<T, G>(rp, ci, va, i < n ? i : n - 1, GatherT<T>{d_old});
+  if ((threadIdx.x & (G - 1)) == 0 && i < n) {
     const T rn = r[i] - ad;
     const T dn = c1 * d_old[i] + c2 * (dinv[i] * rn);
     r[i] = rn;
@@ -121,7 +124,7 @@ __global__ void __launch_bounds__(256) k_vc_cheb_first(long n, SellT<T> A, const
   d_new[i] = dn;
   x[i] = acc ? x[i] + (d0 + dn) : d0 + dn;
 }
-template <typename T>
+template <typename T, int G>
 __global__ void __launch_bounds__(256) k_vc_cheb_first_w(long n, const int *__restrict__ rp,
                                                          const int *__restrict__ ci, const T *__restrict__ va,
                                                          const T *__restrict__ dinv, const T *__restrict__ b,
@@ -129,10 +132,10 @@ __global__ void __launch_bounds__(256) k_vc_cheb_first_w(long n, const int *__re
                                                          T *__restrict__ d_new, T *__restrict__ x, int acc,
                                                          const int *gate) {
   if (!*gate) return;
-  const long i = ((long)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
-  if (i >= n) return;
-  const T ad = warp_row_dot_t(rp, ci, va, i, GatherD0T<T>{b, dinv, inv_theta});
-  if ((threadIdx.x & 31) == 0) {
+  const long i = ((long)blockIdx.x * blockDim.x + threadIdx.x) / G;
+  if ((i & ~(long)(32 / G - 1)) >= n) return;   // whole warps only: the groups of a warp shuffle together
+  const T ad = warp_row_dot_t<T, G>(rp, ci, va, i < n ? i : n - 1, GatherD0T<T>{b, dinv, inv_theta});
+  if ((threadIdx.x & (G - 1)) == 0 && i < n) {
     const T bi = b[i];
     const T d0 = dinv[i] * bi * inv_theta;
     const T rn = bi - ad;
@@ -152,15 +155,15 @@ __global__ void __launch_bounds__(256) k_vc_resid(long n, SellT<T> A, const T *_
   const T acc = sellt_dot(A, i, GatherT<T>{x});
   t[i] = b[i] - acc;
 }
-template <typename T>
+template <typename T, int G>
 __global__ void __launch_bounds__(256) k_vc_resid_w(long n, const int *__restrict__ rp, const int *__restrict__ ci,
                                                     const T *__restrict__ va, const T *__restrict__ x,
                                                     const T *__restrict__ b, T *__restrict__ t, const int *gate) {
   if (!*gate) return;
-  const long i = ((long)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
-  if (i >= n) return;
-  const T ax = warp_row_dot_t(rp, ci, va, i, GatherT<T>{x});
-  if ((threadIdx.x & 31) == 0) t[i] = b[i] - ax;
+  const long i = ((long)blockIdx.x * blockDim.x + threadIdx.x) / G;
+  if ((i & ~(long)(32 / G - 1)) >= n) return;   // whole warps only: the groups of a warp shuffle together
+  const T ax = warp_row_dot_t<T, G>(rp, ci, va, i < n ? i : n - 1, GatherT<T>{x});
+  if ((threadIdx.x & (G - 1)) == 0 && i < n) t[i] = b[i] - ax;
 }
 // plain aggregation transfers: bc[a] = sum over members (index order); x += xc[agg]
 template <typename T>

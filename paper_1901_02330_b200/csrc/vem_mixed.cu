@@ -54,7 +54,8 @@ struct AmgLevel {
   long nc = 0;
   double *b = nullptr, *x = nullptr, *t = nullptr, *y = nullptr, *sr = nullptr, *sd0 = nullptr, *sd1 = nullptr;
   bool owns_matrix = true;
-  bool warp_rows = false;                      // coarse levels: long Galerkin rows -> warp per row
+  bool warp_rows = false;                      // coarse levels: long Galerkin rows -> G lanes per row (CSR)
+  int group = 32;                              // lanes per row of the CSR level kernels (4 .. 32)
   // smoothed aggregation (level 0): P CSR (setup), P SELL (prolongation), P^T CSR (restriction)
   bool sa = false;
   int *prp = nullptr, *pci = nullptr, *ptrp = nullptr, *ptci = nullptr, *psci = nullptr;
@@ -130,6 +131,11 @@ struct Ctx {
   bool amg_f32 = false;                          // FP32 mirror built
   int amg_coarse_degree = 8;                     // Chebyshev degree of a non-dense coarsest level
   int amg_max_levels = 12;                       // AMG_MAX_LEVELS (VEM_AMG_MAX_LEVELS: tests only)
+  long amg_warp_rows = 100000;                   // coarse levels below this many rows: CSR group kernels
+  double amg_warp_nnz = 1e30;                    // ... or with at least this many nnz per row (off: r8 A/B,
+                                                 // SELL-32 beats group CSR on C3's 35-nnz/row level 1)
+  int amg_group = 8;                             // lanes per CSR row (0: by the mean row length; r8 A/B)
+  double amg_group_div = 2.0;                    // ... G = power of two >= mean row length / this
   int amg_cluster = 0;                           // coarsest smoother as one cluster launch (VEM_AMG_CLUSTER=1;
                                                  // off by default: slower than the per-step launches)
   float *f32_pool = nullptr;                     // kind 4 fine-level vectors (L2-persisting window)
@@ -714,6 +720,15 @@ void amg_cheb_coeffs(double lmax, int degree, double &inv_theta, std::vector<dou
   }
 }
 
+// CSR level kernels with L.group lanes per row
+#define VC_GROUP_LAUNCH(KERNEL, L_, ...)                                                              \
+  switch ((L_).group) {                                                                               \
+    case 4: KERNEL<T, 4><<<grid_for((L_).n * 4), NT, 0, c->stream>>>(__VA_ARGS__); break;            \
+    case 8: KERNEL<T, 8><<<grid_for((L_).n * 8), NT, 0, c->stream>>>(__VA_ARGS__); break;            \
+    case 16: KERNEL<T, 16><<<grid_for((L_).n * 16), NT, 0, c->stream>>>(__VA_ARGS__); break;         \
+    default: KERNEL<T, 32><<<grid_for((L_).n * 32), NT, 0, c->stream>>>(__VA_ARGS__); break;         \
+  }
+
 // out = C_degree(b) on level L (x0 = 0), in precision T; `sample`: bracket the second
 // step with the sampled-timing events (fine-level pre-smoothing, timing = 2)
 template <typename T>
@@ -730,9 +745,8 @@ void amg_smooth(Ctx *c, AmgLevel &L, const T *b, T *out, int degree, const int *
   if (degree > 1) {   // init fused into the first step
     TimeScope ts(c, VEM_K_CHEB, vb * L.nnz + 6.0 * sizeof(T) * L.n);
     if (L.warp_rows)
-      k_vc_cheb_first_w<T><<<grid_for(L.n * 32), NT, 0, c->stream>>>(L.n, L.rp, L.ci, D.va(), D.dinv(), b, (T)it,
-                                                                       (T)c1[0], (T)c2[0], D.sr(), D.sd1(), out,
-                                                                       acc, gate);
+      VC_GROUP_LAUNCH(k_vc_cheb_first_w, L, L.n, L.rp, L.ci, D.va(), D.dinv(), b, (T)it, (T)c1[0], (T)c2[0],
+                      D.sr(), D.sd1(), out, acc, gate)
     else
       k_vc_cheb_first<T><<<grid_for(L.n), NT, 0, c->stream>>>(L.n, A, D.dinv(), b, (T)it, (T)c1[0], (T)c2[0],
                                                                D.sr(), D.sd1(), out, acc, gate);
@@ -751,9 +765,8 @@ void amg_smooth(Ctx *c, AmgLevel &L, const T *b, T *out, int degree, const int *
     {
       TimeScope ts(c, VEM_K_CHEB, vb * L.nnz + 7.0 * sizeof(T) * L.n);
       if (L.warp_rows)
-        k_vc_cheb_step_w<T><<<grid_for(L.n * 32), NT, 0, c->stream>>>(L.n, L.rp, L.ci, D.va(), D.dinv(), D.sr(),
-                                                                       dold, dnew, out, (T)c1[i - 1], (T)c2[i - 1],
-                                                                       gate);
+        VC_GROUP_LAUNCH(k_vc_cheb_step_w, L, L.n, L.rp, L.ci, D.va(), D.dinv(), D.sr(), dold, dnew, out,
+                        (T)c1[i - 1], (T)c2[i - 1], gate)
       else
         k_vc_cheb_step<T><<<grid_for(L.n), NT, 0, c->stream>>>(L.n, A, D.dinv(), D.sr(), dold, dnew, out,
                                                                (T)c1[i - 1], (T)c2[i - 1], gate);
@@ -769,7 +782,7 @@ void amg_residual(Ctx *c, AmgLevel &L, const int *gate) {
   const Lv<T> D{L};
   TimeScope ts(c, VEM_K_SPMV, (sizeof(T) + 4.0) * L.nnz + 3.0 * sizeof(T) * L.n);
   if (L.warp_rows)
-    k_vc_resid_w<T><<<grid_for(L.n * 32), NT, 0, c->stream>>>(L.n, L.rp, L.ci, D.va(), D.x(), D.b(), D.t(), gate);
+    VC_GROUP_LAUNCH(k_vc_resid_w, L, L.n, L.rp, L.ci, D.va(), D.x(), D.b(), D.t(), gate)
   else
     k_vc_resid<T><<<grid_for(L.n), NT, 0, c->stream>>>(L.n, SellT<T>{L.soff, L.sci, D.sva()}, D.x(), D.b(), D.t(),
                                                         gate);
@@ -1850,7 +1863,15 @@ int build_amg(Ctx *c) {
     if (read_back(c, c->derr)) return fail(c, VEM_ERR_DIAG_S, "non-positive diagonal in a coarse S_D level");
     r = build_sell(c, C.n, C.rp, C.ci, C.va, &C.soff, &C.sci, &C.sva, &C.nnz_sell);
     if (r) return r;
-    C.warp_rows = C.n < 100000;   // small coarse levels: warp per row (latency), else SELL-32
+    // small coarse levels (latency-bound): G lanes per CSR row, G = 8 (C3 levels 2 and 3, 24.5 and 15.5
+    // nnz per row: 151.8 ms vs 158.0 ms with a warp per row, r8 A/B in DESIGN §5; VEM_AMG_GROUP=0 picks
+    // the power of two >= mean row length / VEM_AMG_GROUP_DIV in [4, 32]); else SELL-32, one thread per row
+    C.warp_rows = C.n < c->amg_warp_rows || (double)C.nnz / C.n >= c->amg_warp_nnz;
+    {
+      int g = 4;
+      while (g < 32 && c->amg_group_div * g < (double)C.nnz / C.n) g *= 2;
+      C.group = c->amg_group ? c->amg_group : g;
+    }
     r = amg_level_vectors(c, C);
     if (r) return r;
     c->amg.push_back(C);
@@ -2029,6 +2050,10 @@ int upload_impl(Ctx *c, const vem_csr *M, const vem_csr *B, const vem_csr *W, do
   c->amg_coarse_degree = getenv("VEM_AMG_COARSE_DEGREE") ? atoi(getenv("VEM_AMG_COARSE_DEGREE")) : AMG_COARSE_DEGREE;
   c->amg_max_levels = getenv("VEM_AMG_MAX_LEVELS") ? atoi(getenv("VEM_AMG_MAX_LEVELS")) : AMG_MAX_LEVELS;
   c->amg_cluster = getenv("VEM_AMG_CLUSTER") ? atoi(getenv("VEM_AMG_CLUSTER")) : 0;
+  c->amg_warp_rows = getenv("VEM_AMG_WARP_ROWS") ? atol(getenv("VEM_AMG_WARP_ROWS")) : 100000;
+  c->amg_warp_nnz = getenv("VEM_AMG_WARP_NNZ") ? atof(getenv("VEM_AMG_WARP_NNZ")) : 1e30;
+  c->amg_group = getenv("VEM_AMG_GROUP") ? atoi(getenv("VEM_AMG_GROUP")) : 8;
+  c->amg_group_div = getenv("VEM_AMG_GROUP_DIV") ? atof(getenv("VEM_AMG_GROUP_DIV")) : 2.0;
   auto phase = [&](const char *what) {
     if (!trace) return;
     cudaStreamSynchronize(c->stream);
