@@ -301,6 +301,39 @@ def test_amg_cluster_coarsest(monkeypatch, cluster):
     sv.close()
 
 
+@pytest.mark.parametrize("group", [4, 8, 16, 32])
+def test_amg_three_level_group_csr(monkeypatch, group):
+    """Default hierarchy of the 32^3 C3-type system: 32768 -> 3643 -> 867 (dense)
+    rows, so the middle level runs the coarse CSR kernels (pre/post Chebyshev(3)
+    smoothing, residuals) with G lanes per row (VEM_AMG_GROUP; default 8).  The
+    V-cycle matches the oracle in FP64 and FP32 and the solve lands in the
+    oracle's iteration band for every G."""
+    from oracle.amg import AMG
+    monkeypatch.setenv("VEM_AMG_GROUP", str(group))
+    if "C3m" not in _CACHE:
+        _CACHE["C3m"] = C3M.build()
+    s = _CACHE["C3m"]
+    SD = O.schur_diag(s.M, s.B)
+    h = AMG(SD)
+    assert len(h.levels) == 3 and h.coarse_inv is not None
+    sv = solver_for(s, restart=50)
+    assert sv.amg_levels() == [(lev.A.shape[0], lev.A.nnz) for lev in h.levels]
+    nu = s.layout.n_u
+    v = RNG.normal(size=s.n)
+    z, _ = sv.precond_apply(pkg.PRECOND_BLOCK_SCHUR_AMG, torch.from_numpy(v).cuda())
+    assert rel_inf(z.cpu().numpy()[nu:], -h.vcycle(v[nu:])) <= 1e-10
+    z32, _ = sv.precond_apply(pkg.PRECOND_BLOCK_SCHUR_AMG_F32, torch.from_numpy(v).cuda())
+    zo32 = -h.to_float32().vcycle(v[nu:].astype(np.float32)).astype(np.float64)
+    assert rel_inf(z32.cpu().numpy()[nu:], zo32) <= 2e-5
+    if group == 8:
+        ref, lo, hi = oracle_iteration_band(s, 3, 50, 0.0, trials=2)
+        res = sv.solve(torch.from_numpy(s.rhs).cuda(), 1e-10, 10000, 3)
+        assert res.report["converged"] == 1
+        assert lo - 2 <= res.report["iterations"] <= hi + 2, (res.report["iterations"], lo, hi)
+        assert rel_inf(res.u.cpu().numpy(), ref.x[:nu]) <= 1e-8 and rel_inf(res.p.cpu().numpy(), ref.x[nu:]) <= 1e-8
+    sv.close()
+
+
 def test_solve_host_matches_device_and_is_deterministic():
     s = system("C3s")
     sv = solver_for(s, restart=50)
