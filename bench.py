@@ -353,6 +353,28 @@ def main():
                          "rel_residual_true": vrep[-1]["rel_residual_true"]})
     variant = variants or None
 
+    # SURVEY.md §8(d) Q21 benchmark extra: the same matrices with a seeded N(0, 1) RHS (seed 7)
+    random_rhs = None
+    if not args.no_variant:
+        from vemgen.configs import random_rhs as _rr
+        rr_dev = torch.from_numpy(_rr(s.n)).cuda()
+        sv.set_options(timing=0, use_graphs=1)
+        sv.solve(rr_dev, cfg.rtol, 20000, kind)
+        torch.cuda.synchronize()
+        q0, q1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        qrep = []
+        q0.record(stream)
+        for _ in range(args.steps):
+            qrep.append(sv.solve(rr_dev, cfg.rtol, 20000, kind).report)
+        q1.record(stream)
+        torch.cuda.synchronize()
+        qms = q0.elapsed_time(q1) / args.steps
+        random_rhs = {"rhs": "N(0,1), seed 7 (vemgen.configs.random_rhs)", "precond": kind,
+                      "time_to_solution_ms": round(qms, 2),
+                      "iterations_per_solve": [r["iterations"] for r in qrep],
+                      "GMRES_it_per_s": round(sum(r["iterations"] for r in qrep) / (args.steps * qms / 1e3), 2),
+                      "rel_residual_true": qrep[-1]["rel_residual_true"]}
+
     hbm, peak_kind = peaks()
     per = {k: v for k, v in breakdown.items() if v["launches"]}
     dom = max(per, key=lambda k: per[k]["ms"]) if per else None
@@ -403,6 +425,7 @@ def main():
                                   else "per-launch CUDA events, no graphs"),
                        "kernels_source": "per-launch CUDA events over one extra solve after the timed region"},
             "roofline": roof, "kernels": kern, "gpu_launches": launches, "variant": variant,
+            "random_rhs": random_rhs,
             "e2e": {"value": round(args.steps / e2e_s, 3), "unit": UNIT, "time_to_solution_ms": round(1e3 * e2e_s / args.steps, 2),
                     "gmres_it_per_s": round(e2e_graph_its / e2e_s, 1),
                     "h2d_bytes_per_step": 8 * s.n, "d2h_bytes_per_step": 8 * s.n,

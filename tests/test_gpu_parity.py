@@ -334,6 +334,29 @@ def test_amg_three_level_group_csr(monkeypatch, group):
     sv.close()
 
 
+@pytest.mark.parametrize("name,kind", [("C1", 1), ("C3s", 1), ("C3s", 3), ("C2s", 2)])
+def test_random_rhs_parity(name, kind):
+    """the same matrices with the seeded N(0, 1) right-hand side
+    (vemgen.configs.random_rhs, seed 7) -- representative iteration counts; GPU within
+    the oracle's band, u and p within 1e-8."""
+    s = system(name)
+    cfg = configs.CONFIGS[name]
+    eps = configs.eps_for(s)
+    rhs = configs.random_rhs(s.n)
+
+    class _S:   # the system with the random RHS (same matrices)
+        M, B, layout = s.M, s.B, s.layout
+    _S.rhs = rhs
+    ref, lo, hi = oracle_iteration_band(_S, kind, cfg.restart, eps, trials=2)
+    sv = solver_for(s, restart=cfg.restart)
+    res = sv.solve(torch.from_numpy(rhs).cuda(), 1e-10, 10000, kind)
+    assert res.report["converged"] == 1
+    assert lo - 2 <= res.report["iterations"] <= hi + 2, (res.report["iterations"], lo, hi)
+    nu = s.layout.n_u
+    assert rel_inf(res.u.cpu().numpy(), ref.x[:nu]) <= 1e-8 and rel_inf(res.p.cpu().numpy(), ref.x[nu:]) <= 1e-8
+    sv.close()
+
+
 def test_solve_host_matches_device_and_is_deterministic():
     s = system("C3s")
     sv = solver_for(s, restart=50)

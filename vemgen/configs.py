@@ -91,3 +91,12 @@ CONFIGS = {
 def eps_for(system) -> float:
     """Block-Reg regularisation eps = 1e-6 * mean diag(M) (BASELINE.json C2)."""
     return 1e-6 * float(system.M.diagonal().mean())
+
+
+def random_rhs(n: int, seed: int = 7) -> np.ndarray:
+    """the benchmark extra -- the same matrices with a
+    seeded N(0, 1) right-hand side (seed 7).  With K = I on uniform cubes the sin
+    source is nearly an eigenvector (R21) and iteration counts are not
+    representative; this RHS is."""
+    return np.random.default_rng(seed).standard_normal(n)
+
