@@ -6,6 +6,15 @@
 #pragma once
 #include "kernels.cuh"
 
+// programmatic dependent launch (coarse-level chains of small kernels): wait for the
+// previous kernel of the stream (all its writes visible), then let the next one be
+// scheduled.  No-ops when the kernel was launched without the PDL attribute.
+__device__ __forceinline__ void pdl_enter() {
+  asm volatile("griddepcontrol.wait;" ::: "memory");
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+}
+
+
 template <typename T>
 struct SellT {
   const long long *__restrict__ soff;
@@ -93,6 +102,7 @@ __global__ void __launch_bounds__(256) k_vc_cheb_step_w(long n, const int *__res
                                                         T *__restrict__ r, const T *__restrict__ d_old,
                                                         T *__restrict__ d_new, T *__restrict__ x, T c1, T c2,
                                                         const int *gate) {
+  pdl_enter();
   if (!*gate) return;
   const long i = ((long)blockIdx.x * blockDim.x + threadIdx.x) / G;
   if ((i & ~(long)(32 / G - 1)) >= n) return;   // whole warps only: the groups of a warp shuffle together
@@ -131,6 +141,7 @@ __global__ void __launch_bounds__(256) k_vc_cheb_first_w(long n, const int *__re
                                                          T inv_theta, T c1, T c2, T *__restrict__ r,
                                                          T *__restrict__ d_new, T *__restrict__ x, int acc,
                                                          const int *gate) {
+  pdl_enter();
   if (!*gate) return;
   const long i = ((long)blockIdx.x * blockDim.x + threadIdx.x) / G;
   if ((i & ~(long)(32 / G - 1)) >= n) return;   // whole warps only: the groups of a warp shuffle together
@@ -159,6 +170,7 @@ template <typename T, int G>
 __global__ void __launch_bounds__(256) k_vc_resid_w(long n, const int *__restrict__ rp, const int *__restrict__ ci,
                                                     const T *__restrict__ va, const T *__restrict__ x,
                                                     const T *__restrict__ b, T *__restrict__ t, const int *gate) {
+  pdl_enter();
   if (!*gate) return;
   const long i = ((long)blockIdx.x * blockDim.x + threadIdx.x) / G;
   if ((i & ~(long)(32 / G - 1)) >= n) return;   // whole warps only: the groups of a warp shuffle together

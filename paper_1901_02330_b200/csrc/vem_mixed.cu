@@ -135,7 +135,9 @@ struct Ctx {
   double amg_warp_nnz = 1e30;                    // ... or with at least this many nnz per row (off: r8 A/B,
                                                  // SELL-32 beats group CSR on C3's 35-nnz/row level 1)
   int amg_group = 8;                             // lanes per CSR row (0: by the mean row length; r8 A/B)
-  double amg_group_div = 2.0;                    // ... G = power of two >= mean row length / this
+  double amg_group_div = 2.0;
+  int pdl = 1;                                   // programmatic dependent launch of the V-cycle kernels
+  bool pdl_skip = false;                         // next launch follows an event record: plain edge                    // ... G = power of two >= mean row length / this
   int amg_cluster = 0;                           // coarsest smoother as one cluster launch (VEM_AMG_CLUSTER=1;
                                                  // off by default: slower than the per-step launches)
   float *f32_pool = nullptr;                     // kind 4 fine-level vectors (L2-persisting window)
@@ -495,13 +497,19 @@ int enqueue_block_schur(Ctx *c, const double *v, const double *scale, double *z,
     for (int i = 2; i < deg; ++i) {
       const int last = i == deg - 1 ? 1 : 0;
       const bool smp = c->opts.timing == 2 && c->sample_slot >= 0 && i == deg / 2;
-      if (smp) cudaEventRecordWithFlags(c->samp_a[c->sample_slot], c->stream, cudaEventRecordExternal);
+      if (smp) {
+      cudaEventRecordWithFlags(c->samp_a[c->sample_slot], c->stream, cudaEventRecordExternal);
+      c->pdl_skip = true;
+    }
       c->sample_recorded |= smp;
       {
         TimeScope ts(c, VEM_K_CHEB, bytes_cheb(c));
         launch_cheb(c, dold, dnew, c1[i - 1], c2[i - 1], last, z + c->nu, gate);
       }
-      if (smp) cudaEventRecordWithFlags(c->samp_b[c->sample_slot], c->stream, cudaEventRecordExternal);
+      if (smp) {
+      cudaEventRecordWithFlags(c->samp_b[c->sample_slot], c->stream, cudaEventRecordExternal);
+      c->pdl_skip = true;
+    }
       std::swap(dold, dnew);
     }
     CKL();
@@ -720,13 +728,39 @@ void amg_cheb_coeffs(double lmax, int degree, double &inv_theta, std::vector<dou
   }
 }
 
+// launch on the library stream, with programmatic dependent launch when c->pdl (the kernel
+// must start with pdl_enter())
+template <typename... KArgs, typename... Args>
+void launch_pdl(Ctx *c, void (*k)(KArgs...), unsigned grid, unsigned block, Args... args) {
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = dim3(grid);
+  cfg.blockDim = dim3(block);
+  cfg.dynamicSmemBytes = 0;
+  cfg.stream = c->stream;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  at[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = at;
+  // no programmatic edge right after an event node, nor under per-launch event timing
+  cfg.numAttrs = c->pdl && !c->pdl_skip && c->opts.timing != 1 ? 1 : 0;
+  c->pdl_skip = false;
+  cudaLaunchKernelEx(&cfg, k, ((KArgs)args)...);
+}
+
+// the same launch without the PDL attribute: every V-cycle kernel but the coarse CSR ones (r13 A/B:
+// PDL on every V-cycle kernel 151.2 / 151.2 ms vs 149.7 / 149.7 ms without)
+template <typename... KArgs, typename... Args>
+void launch_plain(Ctx *c, void (*k)(KArgs...), unsigned grid, unsigned block, Args... args) {
+  k<<<grid, block, 0, c->stream>>>(((KArgs)args)...);
+}
+
 // CSR level kernels with L.group lanes per row
 #define VC_GROUP_LAUNCH(KERNEL, L_, ...)                                                              \
   switch ((L_).group) {                                                                               \
-    case 4: KERNEL<T, 4><<<grid_for((L_).n * 4), NT, 0, c->stream>>>(__VA_ARGS__); break;            \
-    case 8: KERNEL<T, 8><<<grid_for((L_).n * 8), NT, 0, c->stream>>>(__VA_ARGS__); break;            \
-    case 16: KERNEL<T, 16><<<grid_for((L_).n * 16), NT, 0, c->stream>>>(__VA_ARGS__); break;         \
-    default: KERNEL<T, 32><<<grid_for((L_).n * 32), NT, 0, c->stream>>>(__VA_ARGS__); break;         \
+    case 4: launch_pdl(c, KERNEL<T, 4>, grid_for((L_).n * 4), NT, __VA_ARGS__); break;                \
+    case 8: launch_pdl(c, KERNEL<T, 8>, grid_for((L_).n * 8), NT, __VA_ARGS__); break;                \
+    case 16: launch_pdl(c, KERNEL<T, 16>, grid_for((L_).n * 16), NT, __VA_ARGS__); break;             \
+    default: launch_pdl(c, KERNEL<T, 32>, grid_for((L_).n * 32), NT, __VA_ARGS__); break;             \
   }
 
 // out = C_degree(b) on level L (x0 = 0), in precision T; `sample`: bracket the second
@@ -748,14 +782,14 @@ void amg_smooth(Ctx *c, AmgLevel &L, const T *b, T *out, int degree, const int *
       VC_GROUP_LAUNCH(k_vc_cheb_first_w, L, L.n, L.rp, L.ci, D.va(), D.dinv(), b, (T)it, (T)c1[0], (T)c2[0],
                       D.sr(), D.sd1(), out, acc, gate)
     else
-      k_vc_cheb_first<T><<<grid_for(L.n), NT, 0, c->stream>>>(L.n, A, D.dinv(), b, (T)it, (T)c1[0], (T)c2[0],
+      launch_plain(c, k_vc_cheb_first<T>, grid_for(L.n), NT, L.n, A, D.dinv(), b, (T)it, (T)c1[0], (T)c2[0],
                                                                D.sr(), D.sd1(), out, acc, gate);
     dold = D.sd1();
     dnew = D.sd0();
     first = 2;
   } else {
     TimeScope ts(c, VEM_K_PRECOND_VEC, 5.0 * sizeof(T) * L.n);
-    k_vc_cheb_init<T><<<grid_stream(c, L.n), NT, 0, c->stream>>>(L.n, D.dinv(), b, (T)it, D.sr(), D.sd0(), out,
+    launch_plain(c, k_vc_cheb_init<T>, grid_stream(c, L.n), NT, L.n, D.dinv(), b, (T)it, D.sr(), D.sd0(), out,
                                                                   acc, gate);
   }
   for (int i = first; i < degree; ++i) {
@@ -768,7 +802,7 @@ void amg_smooth(Ctx *c, AmgLevel &L, const T *b, T *out, int degree, const int *
         VC_GROUP_LAUNCH(k_vc_cheb_step_w, L, L.n, L.rp, L.ci, D.va(), D.dinv(), D.sr(), dold, dnew, out,
                         (T)c1[i - 1], (T)c2[i - 1], gate)
       else
-        k_vc_cheb_step<T><<<grid_for(L.n), NT, 0, c->stream>>>(L.n, A, D.dinv(), D.sr(), dold, dnew, out,
+        launch_plain(c, k_vc_cheb_step<T>, grid_for(L.n), NT, L.n, A, D.dinv(), D.sr(), dold, dnew, out,
                                                                (T)c1[i - 1], (T)c2[i - 1], gate);
     }
     if (smp) cudaEventRecordWithFlags(c->samp_b[c->sample_slot], c->stream, cudaEventRecordExternal);
@@ -784,7 +818,7 @@ void amg_residual(Ctx *c, AmgLevel &L, const int *gate) {
   if (L.warp_rows)
     VC_GROUP_LAUNCH(k_vc_resid_w, L, L.n, L.rp, L.ci, D.va(), D.x(), D.b(), D.t(), gate)
   else
-    k_vc_resid<T><<<grid_for(L.n), NT, 0, c->stream>>>(L.n, SellT<T>{L.soff, L.sci, D.sva()}, D.x(), D.b(), D.t(),
+    launch_plain(c, k_vc_resid<T>, grid_for(L.n), NT, L.n, SellT<T>{L.soff, L.sci, D.sva()}, D.x(), D.b(), D.t(),
                                                         gate);
 }
 
@@ -834,7 +868,7 @@ void amg_vcycle(Ctx *c, size_t l, const int *gate) {
   if (l + 1 == c->amg.size()) {   // coarsest
     if (c->amg_dense) {
       TimeScope ts(c, VEM_K_PRECOND_VEC, (double)sizeof(T) * L.n * L.n);
-      k_vc_dense_mv<T><<<grid_for(L.n * 32), NT, 0, c->stream>>>(L.n, amg_cinv<T>(c), D.b(), D.x(), gate);
+      launch_plain(c, k_vc_dense_mv<T>, grid_for(L.n * 32), NT, L.n, amg_cinv<T>(c), D.b(), D.x(), gate);
     } else if (L.vc_ok) {
       amg_coarse_cluster<T>(c, L, gate);
     } else {
@@ -848,19 +882,19 @@ void amg_vcycle(Ctx *c, size_t l, const int *gate) {
   amg_residual<T>(c, L, gate);
   if (L.sa) {
     TimeScope ts(c, VEM_K_PRECOND_VEC, (sizeof(T) + 4.0) * L.pnnz + sizeof(T) * (1.0 * L.n + C.n));
-    k_vc_sa_restrict<T><<<grid_for(C.n * 8), NT, 0, c->stream>>>(C.n, L.ptrp, L.ptci, D.ptva(), D.t(), DC.b(), gate);
+    launch_plain(c, k_vc_sa_restrict<T>, grid_for(C.n * 8), NT, C.n, L.ptrp, L.ptci, D.ptva(), D.t(), DC.b(), gate);
   } else {
     TimeScope ts(c, VEM_K_PRECOND_VEC, sizeof(T) * (2.0 * L.n + C.n));
-    k_vc_restrict<T><<<grid_stream(c, C.n), NT, 0, c->stream>>>(C.n, L.moff, L.mem, D.t(), DC.b(), gate);
+    launch_plain(c, k_vc_restrict<T>, grid_stream(c, C.n), NT, C.n, L.moff, L.mem, D.t(), DC.b(), gate);
   }
   amg_vcycle<T>(c, l + 1, gate);
   if (L.sa) {
     TimeScope ts(c, VEM_K_PRECOND_VEC, (sizeof(T) + 4.0) * L.pnnz + sizeof(T) * (2.0 * L.n + C.n));
-    k_vc_sa_prolong_add<T><<<grid_for(L.n), NT, 0, c->stream>>>(L.n, SellT<T>{L.psoff, L.psci, D.psva()}, DC.x(),
+    launch_plain(c, k_vc_sa_prolong_add<T>, grid_for(L.n), NT, L.n, SellT<T>{L.psoff, L.psci, D.psva()}, DC.x(),
                                                                  D.x(), gate);
   } else {
     TimeScope ts(c, VEM_K_PRECOND_VEC, sizeof(T) * 3.0 * L.n);
-    k_vc_prolong_add<T><<<grid_stream(c, L.n), NT, 0, c->stream>>>(L.n, L.agg, DC.x(), D.x(), gate);
+    launch_plain(c, k_vc_prolong_add<T>, grid_stream(c, L.n), NT, L.n, L.agg, DC.x(), D.x(), gate);
   }
   amg_residual<T>(c, L, gate);
   amg_smooth<T>(c, L, D.t(), D.x(), AMG_DEGREE, gate, false, 1);   // x += C(b - A x)
@@ -878,15 +912,15 @@ int enqueue_block_schur_amg(Ctx *c, const double *v, const double *scale, double
   {
     TimeScope ts(c, VEM_K_PRECOND_VEC, z_out ? 24.0 * c->nu + (8.0 + sizeof(T)) * c->np : (8.0 + sizeof(T)) * c->np);
     if (z_out)
-      k_vc_top<T><<<grid_stream(c, c->n), NT, 0, c->stream>>>(c->nu, c->np, v, scale, c->dMinv, z, D0.b(), gate);
+      launch_plain(c, k_vc_top<T>, grid_stream(c, c->n), NT, c->nu, c->np, v, scale, c->dMinv, z, D0.b(), gate);
     else   // pressure part only
-      k_vc_top<T><<<grid_stream(c, c->np), NT, 0, c->stream>>>(0, c->np, v + c->nu, scale, nullptr, nullptr, D0.b(),
+      launch_plain(c, k_vc_top<T>, grid_stream(c, c->np), NT, 0, c->np, v + c->nu, scale, nullptr, nullptr, D0.b(),
                                                                 gate);
   }
   amg_vcycle<T>(c, 0, gate);
   if (z_out) {
     TimeScope ts(c, VEM_K_PRECOND_VEC, (8.0 + sizeof(T)) * c->np);
-    k_vc_out<T><<<grid_stream(c, c->np), NT, 0, c->stream>>>(c->np, D0.x(), z + c->nu, gate);
+    launch_plain(c, k_vc_out<T>, grid_stream(c, c->np), NT, c->np, D0.x(), z + c->nu, gate);
   }
   CKL();
   return 0;
@@ -937,10 +971,10 @@ int enqueue_arnoldi_step(Ctx *c, int kind, int j, int64_t *inner_its) {
     if (rc) return rc;
     TimeScope ts(c, VEM_K_SPMV, bytes_spmv(c) + 8.0 * c->nu);
     if (f32)   // FGMRES: z_j is also stored (row by row, by the thread that owns the row)
-      k_vc_spmv_z<float><<<grid_for(c->n), NT, 0, c->stream>>>(c->n, c->nu, sellA(c), Vj, &c->st->vscale[j],
+      launch_plain(c, k_vc_spmv_z<float>, grid_for(c->n), NT, c->n, c->nu, sellA(c), Vj, &c->st->vscale[j],
                                                                 c->dMinv, c->amg[0].x_f, w, zj, gate_active(c));
     else
-      k_vc_spmv_z<double><<<grid_for(c->n), NT, 0, c->stream>>>(c->n, c->nu, sellA(c), Vj, &c->st->vscale[j],
+      launch_plain(c, k_vc_spmv_z<double>, grid_for(c->n), NT, c->n, c->nu, sellA(c), Vj, &c->st->vscale[j],
                                                                  c->dMinv, c->amg[0].x, w, nullptr, gate_active(c));
   } else {
     int rc = enqueue_precond(c, kind, Vj, &c->st->vscale[j], zj, gate_active(c), inner_its);
@@ -2054,6 +2088,7 @@ int upload_impl(Ctx *c, const vem_csr *M, const vem_csr *B, const vem_csr *W, do
   c->amg_warp_nnz = getenv("VEM_AMG_WARP_NNZ") ? atof(getenv("VEM_AMG_WARP_NNZ")) : 1e30;
   c->amg_group = getenv("VEM_AMG_GROUP") ? atoi(getenv("VEM_AMG_GROUP")) : 8;
   c->amg_group_div = getenv("VEM_AMG_GROUP_DIV") ? atof(getenv("VEM_AMG_GROUP_DIV")) : 2.0;
+  c->pdl = getenv("VEM_PDL") ? atoi(getenv("VEM_PDL")) : 1;
   auto phase = [&](const char *what) {
     if (!trace) return;
     cudaStreamSynchronize(c->stream);
