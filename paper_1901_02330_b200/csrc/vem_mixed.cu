@@ -137,6 +137,7 @@ struct Ctx {
   int amg_group = 8;                             // lanes per CSR row (0: by the mean row length; r8 A/B)
   double amg_group_div = 2.0;
   int pdl = 1;                                   // programmatic dependent launch of the V-cycle kernels
+  int mdot_slots = 0;                            // >0: k_mdot grid = one full wave of this many resident CTAs
   bool pdl_skip = false;                         // next launch follows an event record: plain edge                    // ... G = power of two >= mean row length / this
   int amg_cluster = 0;                           // coarsest smoother as one cluster launch (VEM_AMG_CLUSTER=1;
                                                  // off by default: slower than the per-step launches)
@@ -989,7 +990,10 @@ int enqueue_arnoldi_step(Ctx *c, int kind, int j, int64_t *inner_its) {
   const int npass = (c->opts.reorth == 1 || (c->opts.reorth < 0 && kind == VEM_PRECOND_BLOCK_REG)) ? 2 : 1;
   for (int pass = 1; pass <= npass; ++pass) {
     const int nout = nv + (pass == 1 ? 1 : 0);
-    dim3 grid(gx, (nout + VEM_DOT_CHUNK - 1) / VEM_DOT_CHUNK);
+    const int nchunk = (nout + VEM_DOT_CHUNK - 1) / VEM_DOT_CHUNK;
+    // one full wave of resident CTAs over all chunks (a fixed 2 CTAs/SM per chunk leaves the
+    // short-basis steps at a quarter of the SM slots and the long ones at 1.75 waves)
+    dim3 grid(c->mdot_slots > 0 ? std::max(c->mdot_slots / nchunk, 1) : gx, nchunk);
     {
       TimeScope ts(c, VEM_K_DOT, bytes_vecs(c, nv + 1));
       k_mdot<<<grid, NT, 0, c->stream>>>(c->n, c->V, c->ldv, nv, pass == 1 ? 1 : 0, w, c->part, c->counter, c->st,
@@ -1063,6 +1067,8 @@ int ensure_work(Ctx *c, int kind) {
     c->zcap = m;
   }
   return ensure_part(c, (long)c->sm_count * 2 * ((m + 2 + VEM_DOT_CHUNK - 1) / VEM_DOT_CHUNK + 1) * VEM_DOT_CHUNK +
+                            (long)(c->mdot_slots + c->sm_count * ((m + 2 + VEM_DOT_CHUNK - 1) / VEM_DOT_CHUNK)) *
+                                VEM_DOT_CHUNK +
                             (long)c->sm_count * 64 * 2 + grid_for(c->n * 32) + 1024);
 }
 
@@ -2133,6 +2139,11 @@ int upload_impl(Ctx *c, const vem_csr *M, const vem_csr *B, const vem_csr *W, do
   CK(cudaGetDevice(&dev));
   CK(cudaGetDeviceProperties(&prop, dev));
   c->sm_count = prop.multiProcessorCount;
+  if (!getenv("VEM_MDOT_WAVE") || atoi(getenv("VEM_MDOT_WAVE")) != 0) {
+    int occ = 0;
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_mdot, NT, 0) == cudaSuccess && occ > 0)
+      c->mdot_slots = occ * c->sm_count;
+  }
 
   // raw uploads (freed after the merged formats are built)
   int64_t *mrp = nullptr, *brp = nullptr;
