@@ -138,6 +138,7 @@ struct Ctx {
   double amg_group_div = 2.0;
   int pdl = 1;                                   // programmatic dependent launch of the V-cycle kernels
   int mdot_slots = 0;                            // >0: k_mdot grid = one full wave of this many resident CTAs
+  int update_slots = 0;                          // >0: k_update grid = one full wave (VEM_UPDATE_WAVE)
   bool pdl_skip = false;                         // next launch follows an event record: plain edge                    // ... G = power of two >= mean row length / this
   int amg_cluster = 0;                           // coarsest smoother as one cluster launch (VEM_AMG_CLUSTER=1;
                                                  // off by default: slower than the per-step launches)
@@ -1001,7 +1002,7 @@ int enqueue_arnoldi_step(Ctx *c, int kind, int j, int64_t *inner_its) {
     }
     {
       TimeScope ts(c, VEM_K_UPDATE, bytes_vecs(c, nv + 2));
-      k_update<<<gx * 2, NT, 0, c->stream>>>(c->n, c->V, c->ldv, nv, w, pass == npass ? 1 : 0, c->part,
+      k_update<<<c->update_slots > 0 ? c->update_slots : gx * 2, NT, 0, c->stream>>>(c->n, c->V, c->ldv, nv, w, pass == npass ? 1 : 0, c->part,
                                              c->counter, c->st, j);
     }
   }
@@ -2143,6 +2144,11 @@ int upload_impl(Ctx *c, const vem_csr *M, const vem_csr *B, const vem_csr *W, do
     int occ = 0;
     if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_mdot, NT, 0) == cudaSuccess && occ > 0)
       c->mdot_slots = occ * c->sm_count;
+  }
+  if (!getenv("VEM_UPDATE_WAVE") || atoi(getenv("VEM_UPDATE_WAVE")) != 0) {
+    int occ = 0;
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_update, NT, 0) == cudaSuccess && occ > 0)
+      c->update_slots = occ * c->sm_count;
   }
 
   // raw uploads (freed after the merged formats are built)
