@@ -216,3 +216,49 @@ class AMG:
             x = x + xc[lev.agg]
         x = x + self.smooth(lev, b - lev.A @ x)
         return x
+
+
+class SchurMG:
+    """V-cycle of S_D used as the preconditioner of Block-Reg's inner PCG on
+    S_D + eps W ("use it ... as the PCG preconditioner inside
+    Block-Reg"; reading R23).  A fixed symmetric positive definite
+    operator, so plain PCG applies.
+
+      * n_p = 1 (k = 0): one V-cycle of AMG(S_D), exactly the kind-3 V-cycle above.
+      * n_p > 1 (k >= 1), two-grid p-multigrid onto the element-mean moment:
+          C(b)  = degree-DEGREE Chebyshev with the element-block Jacobi D_B of S_D
+                  on [2/RATIO, 2] (oracle.solver.chebyshev; lambda_max(D_B^-1 S_D) <= 2,
+                  reading R15), x0 = 0
+          R r   = r[0::n_p]   (pressure moments are element-major with the mean
+                  moment (1/|P|) int q first: a constant pressure has zero
+                  higher moments, so injection of the mean is the P_0 coarse space)
+          S_c   = R S_D R^T = S_D[0::n_p, 0::n_p], solved by one V-cycle of AMG(S_c)
+          V(b)  : x = C(b); r = b - S_D x; x[0::n_p] += AMG(S_c).vcycle(r[0::n_p]);
+                  x += C(b - S_D x)
+    """
+
+    def __init__(self, S, nb, DBinv=None):
+        self.S = S.tocsr()
+        self.nb = nb
+        if nb == 1:
+            self.amg = AMG(self.S)
+        else:
+            from .solver import block_jacobi_inv
+            self.DBinv = block_jacobi_inv(self.S, nb) if DBinv is None else DBinv
+            self.Sc = self.S[0::nb, 0::nb].tocsr()
+            self.Sc.sort_indices()
+            self.amg = AMG(self.Sc)
+
+    def smooth(self, b):
+        return chebyshev(self.S, self.DBinv, b, DEGREE, 2.0, RATIO)
+
+    def __call__(self, b):
+        if self.nb == 1:
+            return self.amg.vcycle(b)
+        nb = self.nb
+        x = self.smooth(b)
+        r = b - self.S @ x
+        x = x.copy()
+        x[0::nb] += self.amg.vcycle(r[0::nb])
+        x = x + self.smooth(b - self.S @ x)
+        return x

@@ -12,6 +12,13 @@ Plain fp64 numpy/scipy, written in the order of the paper / SURVEY.md §8(c):
   * pcg              block-Jacobi PCG from x0 = 0                (reading R16)
   * block_reg        B_2^-1 = (eps W)^-1, B_1^-1 by Woodbury with diag(M)
                      and an inner PCG on S_D + eps W             (reading R16)
+                     whose preconditioner is the element-block Jacobi of
+                     S_D + eps W (inner_precond = 0) or one V-cycle of S_D
+                     (inner_precond = 1, oracle/amg.py SchurMG; N1, reading R23)
+  * block_reg_m      kind 5: B_2^-1 = (eps W)^-1, B_1^-1 y = PCG on
+                     K = M + B^T (eps W)^-1 B (the paper's regularised velocity
+                     block itself) preconditioned by the kind-2 B_1,
+                     to a relative tolerance k_rtol (reading R24)
   * gmres            right-preconditioned GMRES(m) / FGMRES(m), CGS2 Arnoldi,
                      Givens rotations                            (O8)
   * dense_solve      LAPACK LU of the assembled saddle matrix    (O9)
@@ -35,6 +42,9 @@ PRECOND_BLOCK_SCHUR = 1
 PRECOND_BLOCK_REG = 2
 PRECOND_BLOCK_SCHUR_AMG = 3     # Block-Schur with one aggregation V-cycle on S_D (oracle/amg.py, R22)
 PRECOND_BLOCK_SCHUR_AMG_F32 = 4  # the same V-cycle in FP32 inside the FP64 GMRES
+PRECOND_BLOCK_REG_M = 5          # Block-Reg with an M-aware velocity block: PCG on M + B^T (eps W)^-1 B (R24)
+INNER_JACOBI = 0                 # Block-Reg inner PCG preconditioner: element-block Jacobi of S_D + eps W
+INNER_MG = 1                     # ... one V-cycle of S_D (oracle/amg.py SchurMG)
 
 
 def spmv_saddle(M, B, x):
@@ -116,14 +126,20 @@ def chebyshev(S, Dinv, v, degree, lmax, ratio):
 
 
 def pcg(A, Dinv, b, rtol, maxit):
-    """Preconditioned CG (preconditioner matrix Dinv) from x0 = 0; stops when
-    ||r||_2 <= rtol ||b||_2 (Hestenes-Stiefel recurrences).  Returns (x, iterations, converged)."""
+    """Preconditioned CG (preconditioner Dinv: a matrix, or a callable z = Dinv(r))
+    from x0 = 0; stops when ||r||_2 <= rtol ||b||_2 (Hestenes-Stiefel recurrences).
+    Returns (x, iterations, converged)."""
+    if callable(Dinv):
+        prec = Dinv
+    else:
+        def prec(r):
+            return Dinv @ r
     x = np.zeros_like(b)
     bn = np.linalg.norm(b)
     if bn == 0.0:
         return x, 0, True
     r = b.copy()
-    z = Dinv @ r
+    z = prec(r)
     p = z.copy()
     rz = r @ z
     for it in range(1, maxit + 1):
@@ -133,12 +149,40 @@ def pcg(A, Dinv, b, rtol, maxit):
         r = r - alpha * q
         if np.linalg.norm(r) <= rtol * bn:
             return x, it, True
-        z = Dinv @ r
+        z = prec(r)
         rz_new = r @ z
         beta = rz_new / rz
         rz = rz_new
         p = z + beta * p
     return x, maxit, False
+
+
+def pcg_k(Kmul, prec, b, rtol, maxit):
+    """PCG for the regularised velocity block K y = b (kind 5, reading R24) from
+    y0 = 0 with the SPD preconditioner `prec`; stops when the preconditioned
+    residual norm sqrt(r.z) <= rtol sqrt(r_0.z_0) (K = M + B^T (eps W)^-1 B has
+    eigenvalues of order 1/eps on range(B^T), so the 2-norm of r would only
+    measure that part).  Returns (y, iterations, converged)."""
+    y = np.zeros_like(b)
+    if not np.any(b):
+        return y, 0, True
+    r = b.copy()
+    z = prec(r)
+    rz = r @ z
+    rz0 = rz
+    p = z.copy()
+    for it in range(1, maxit + 1):
+        q = Kmul(p)
+        alpha = rz / (p @ q)
+        y = y + alpha * p
+        r = r - alpha * q
+        z = prec(r)
+        rz_new = r @ z
+        if np.sqrt(abs(rz_new)) <= rtol * np.sqrt(rz0):
+            return y, it, True
+        p = z + (rz_new / rz) * p
+        rz = rz_new
+    return y, maxit, False
 
 
 @dataclass
@@ -153,14 +197,20 @@ class Preconditioner:
     inner_maxit: int = 10000
     exact_schur: bool = False          # pins only: B_2^-1 = -S_D^-1 exactly
     block: int = 1                     # n_p: pressure DOFs per element (element-block Jacobi)
+    inner_precond: int = INNER_MG      # Block-Reg inner PCG preconditioner (R23)
+    k_rtol: float = 0.1                # kind 5: relative tolerance of the PCG on K (R24)
+    k_maxit: int = 500
+    k_inner_rtol: float = 1e-6         # kind 5: inner PCG tolerance of the Woodbury preconditioner (R24)
     inner_iterations: int = 0
+    k_iterations: int = 0
     inner_failed: bool = False
     _cache: dict = field(default_factory=dict)
 
     def __post_init__(self):
         self.nu = self.M.shape[0]
         self.dM = self.M.diagonal().copy()
-        if self.kind in (PRECOND_BLOCK_SCHUR, PRECOND_BLOCK_REG, PRECOND_BLOCK_SCHUR_AMG, PRECOND_BLOCK_SCHUR_AMG_F32):
+        if self.kind in (PRECOND_BLOCK_SCHUR, PRECOND_BLOCK_REG, PRECOND_BLOCK_SCHUR_AMG, PRECOND_BLOCK_SCHUR_AMG_F32,
+                         PRECOND_BLOCK_REG_M):
             self.SD = schur_diag(self.M, self.B)
             self.dS = self.SD.diagonal().copy()
             if np.any(self.dS <= 0):
@@ -174,17 +224,35 @@ class Preconditioner:
             self.amg = AMG(self.SD)
             if self.kind == PRECOND_BLOCK_SCHUR_AMG_F32:
                 self.amg = self.amg.to_float32()
-        if self.kind == PRECOND_BLOCK_REG:
+        if self.kind in (PRECOND_BLOCK_REG, PRECOND_BLOCK_REG_M):
             if self.eps <= 0:
                 raise ValueError("eps must be > 0")
             self.Seps = (self.SD + self.eps * sp.identity(self.SD.shape[0], format="csr")).tocsr()
-            self.DBeps_inv = block_jacobi_inv(self.Seps, self.block)
+            if self.inner_precond == INNER_MG:
+                from .amg import SchurMG
+                self.inner_prec = SchurMG(self.SD, self.block, self.DBinv if self.block > 1 else None)
+            else:
+                self.inner_prec = block_jacobi_inv(self.Seps, self.block)
 
     @property
     def flexible(self) -> bool:
         # FGMRES for the variable preconditioners: Block-Reg (inner PCG) and the FP32
         # V-cycle (its rounding makes P^-1 (V y) differ from sum_j y_j P^-1 v_j)
-        return self.kind in (PRECOND_BLOCK_REG, PRECOND_BLOCK_SCHUR_AMG_F32)
+        return self.kind in (PRECOND_BLOCK_REG, PRECOND_BLOCK_SCHUR_AMG_F32, PRECOND_BLOCK_REG_M)
+
+    def woodbury_d(self, vu, rtol=None):
+        """(diag(M) + B^T (eps W)^-1 B)^-1 vu = D^-1 vu - D^-1 B^T (eps W + S_D)^-1 B D^-1 vu
+        (Woodbury; the inner solve is the PCG of reading R16/R23 to rtol, default inner_rtol)."""
+        t0 = vu / self.dM
+        s = self.B @ t0
+        t, its, ok = pcg(self.Seps, self.inner_prec, s, self.inner_rtol if rtol is None else rtol, self.inner_maxit)
+        self.inner_iterations += its
+        self.inner_failed |= not ok
+        return t0 - (self.B.T @ t) / self.dM
+
+    def kmul(self, y):
+        """K y = M y + B^T (eps W)^-1 B y, W = I."""
+        return self.M @ y + (self.B.T @ (self.B @ y)) / self.eps
 
     def apply(self, v):
         nu = self.nu
@@ -209,12 +277,15 @@ class Preconditioner:
             # B_2^-1 = (eps W)^-1 with W = I
             zp = vp / self.eps
             # B_1^-1 = (D + B^T (eps W)^-1 B)^-1 = D^-1 - D^-1 B^T (eps W + B D^-1 B^T)^-1 B D^-1
-            t0 = vu / self.dM
-            s = self.B @ t0
-            t, its, ok = pcg(self.Seps, self.DBeps_inv, s, self.inner_rtol, self.inner_maxit)
-            self.inner_iterations += its
+            zu = self.woodbury_d(vu)
+            return np.concatenate([zu, zp])
+        if self.kind == PRECOND_BLOCK_REG_M:
+            zp = vp / self.eps
+            # B_1^-1 ~ K^-1 = (M + B^T (eps W)^-1 B)^-1 by PCG, preconditioned by the kind-2 B_1
+            zu, its, ok = pcg_k(self.kmul, lambda r: self.woodbury_d(r, self.k_inner_rtol), vu, self.k_rtol,
+                                self.k_maxit)
+            self.k_iterations += its
             self.inner_failed |= not ok
-            zu = t0 - (self.B.T @ t) / self.dM
             return np.concatenate([zu, zp])
         raise ValueError(f"unsupported precond kind {self.kind}")
 
@@ -328,16 +399,20 @@ def gmres(matvec, precond, b, rtol=1e-10, restart=30, maxit=10000, flexible=Fals
 
 def solve(M, B, rhs, precond_kind=PRECOND_BLOCK_SCHUR, rtol=1e-10, restart=30, maxit=10000,
           eps=0.0, cheb_degree=16, cheb_ratio=30.0, inner_rtol=1e-14, inner_maxit=10000,
-          exact_schur=False, block=1, reorth=-1):
+          exact_schur=False, block=1, reorth=-1, inner_precond=INNER_MG, k_rtol=0.1, k_maxit=500,
+          k_inner_rtol=1e-6):
     """Oracle counterpart of vem_mixed_upload + vem_mixed_solve; `block` is
     the number of pressure DOFs per element (layout.n_p_dof).  reorth = -1
-    (auto, reading R17): CGS1 for GMRES, CGS2 for FGMRES (Block-Reg)."""
+    (auto, reading R17): CGS1 for GMRES, CGS2 for the Block-Reg
+    FGMRES (kinds 2 and 5), CGS1 for the FP32-V-cycle FGMRES (kind 4)."""
     if reorth < 0:
-        reorth = 1 if precond_kind == PRECOND_BLOCK_REG else 0
+        reorth = 1 if precond_kind in (PRECOND_BLOCK_REG, PRECOND_BLOCK_REG_M) else 0
     P = Preconditioner(precond_kind, M, B, cheb_degree, cheb_ratio, eps, inner_rtol, inner_maxit,
-                       exact_schur, block=block)
+                       exact_schur, block=block, inner_precond=inner_precond, k_rtol=k_rtol, k_maxit=k_maxit,
+                       k_inner_rtol=k_inner_rtol)
     res = gmres(lambda x: spmv_saddle(M, B, x), P.apply, rhs, rtol, restart, maxit, P.flexible, reorth)
     res.inner_iterations = P.inner_iterations
+    res.k_iterations = P.k_iterations
     res.inner_failed = P.inner_failed
     return res
 

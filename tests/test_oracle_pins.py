@@ -288,3 +288,148 @@ def test_block_schur_amg_gmres_vs_lu():
         assert r.converged
         if xd is not None:
             assert np.abs(r.x - xd).max() <= 1e-8 * np.abs(xd).max()
+
+
+# ---------------------------------------------------------------------------
+# pins added in round 2: AMG bounds, the Block-Schur sign, the multigrid inner
+# PCG of Block-Reg (reading R23) and the M-aware Block-Reg (kind 5, R24)
+# ---------------------------------------------------------------------------
+def test_amg_gershgorin_bounds_every_level():
+    """The Chebyshev smoother interval top on every level is the Gershgorin bound; it
+    must be >= lambda_max(D^-1 A_l) (else the smoother diverges on that level)."""
+    from oracle import amg
+    import scipy.sparse.linalg as spl
+    s, SD = _c3s_sd()
+    h = amg.AMG(SD)
+    for lev in h.levels:
+        A = lev.A
+        d = A.diagonal()
+        Dh = sp.diags(1 / np.sqrt(d))
+        lam = spl.eigsh(Dh @ A @ Dh, k=1, which="LA", return_eigenvectors=False, tol=1e-10)[0]
+        assert amg.gershgorin(A) >= lam * (1 - 1e-10)
+        assert abs(lev.lmax - amg.gershgorin(A)) == 0.0
+
+
+def test_amg_vcycle_symmetric_with_chebyshev_coarsest():
+    """max_levels = 2 leaves a coarsest level above COARSE_SIZE on C3s-sized grids
+    only if coarse_size is lowered: force it, so the coarsest is the Chebyshev(32)
+    branch (amg.py: coarse_inv None), and check the V-cycle stays symmetric positive
+    definite (the Chebyshev polynomial in D^-1 A is D-symmetric)."""
+    from oracle import amg
+    s, SD = _c3s_sd()
+    h = amg.AMG(SD, coarse_size=64, max_levels=2)
+    assert len(h.levels) == 2 and h.coarse_inv is None
+    n = SD.shape[0]
+    u, v = RNG.normal(size=n), RNG.normal(size=n)
+    assert abs(u @ h.vcycle(v) - v @ h.vcycle(u)) <= 1e-10 * abs(u @ h.vcycle(v))
+    assert v @ h.vcycle(v) > 0 and u @ h.vcycle(u) > 0
+
+
+def test_block_schur_sign_tends_to_minus_exact_inverse():
+    """Kind 1 applies B_2^-1 = S^-1 with S = -S_D: as the Chebyshev degree
+    grows the pressure part of the apply tends to -S_D^-1 v_p (a sign error would
+    converge to +S_D^-1 v_p)."""
+    s = configs.CONFIGS["C1"].build()
+    SD = O.schur_diag(s.M, s.B).toarray()
+    v = RNG.normal(size=s.n)
+    nu = s.layout.n_u
+    ref = -np.linalg.solve(SD, v[nu:])
+    errs = []
+    for deg in (8, 32, 128):
+        P = O.Preconditioner(O.PRECOND_BLOCK_SCHUR, s.M, s.B, cheb_degree=deg, cheb_ratio=400.0)
+        errs.append(np.abs(P.apply(v)[nu:] - ref).max() / np.abs(ref).max())
+    assert errs[0] > errs[1] > errs[2] and errs[2] < 1e-4
+    assert np.abs(P.apply(v)[:nu] - v[:nu] / s.M.diagonal()).max() == 0.0
+
+
+@pytest.mark.parametrize("name", ["C3s", "C5s"])
+def test_block_jacobi_lambda_max_bound_large(name):
+    """lambda_max(D_B^-1 S_D) <= 2 (reading R15) on the configs too large for dense
+    eigenvalues, by a Lanczos estimate of the symmetric form D_B^-1/2 S_D D_B^-1/2."""
+    import scipy.sparse.linalg as spl
+    s = configs.CONFIGS[name].build()
+    nb = s.layout.n_p_dof
+    SD = O.schur_diag(s.M, s.B)
+    # symmetric square root of the block inverse, element by element
+    ne = SD.shape[0] // nb
+    blocks = []
+    for e in range(ne):
+        sl = slice(e * nb, (e + 1) * nb)
+        w, U = np.linalg.eigh(SD[sl, sl].toarray())
+        blocks.append((U / np.sqrt(w)) @ U.T)
+    R = sp.block_diag(blocks).tocsr()
+    lam = spl.eigsh(R @ SD @ R, k=1, which="LA", return_eigenvectors=False, tol=1e-10)[0]
+    assert lam <= 2.0 + 1e-9
+    assert lam > 1.0   # S_D couples elements: the bound is not vacuous
+    # R is the symmetric square root of D_B^-1 (so R S_D R is similar to D_B^-1 S_D)
+    Dinv = O.block_jacobi_inv(SD, nb)
+    sl = slice(0, 3 * nb)
+    assert np.abs((R @ R)[sl, sl].toarray() - Dinv[sl, sl].toarray()).max() <= 1e-10 * abs(Dinv).max()
+
+
+@pytest.mark.parametrize("name", ["C2s", "C4s", "C3s"])
+def test_schur_mg_is_symmetric_positive_definite(name):
+    """The inner-PCG preconditioner of Block-Reg (reading R23) must be SPD: probe its
+    matrix column by column (dense) and check symmetry and the smallest eigenvalue."""
+    from oracle.amg import SchurMG
+    s = configs.CONFIGS[name].build()
+    nb = s.layout.n_p_dof
+    SD = O.schur_diag(s.M, s.B)
+    V = SchurMG(SD, nb)
+    n = SD.shape[0]
+    Vm = np.stack([V(e) for e in np.eye(n)], axis=1)
+    assert np.abs(Vm - Vm.T).max() <= 1e-10 * np.abs(Vm).max()
+    assert np.linalg.eigvalsh(0.5 * (Vm + Vm.T)).min() > 0
+    if nb > 1:   # the coarse operator is S_D restricted to the element-mean moments
+        assert np.abs((V.Sc - SD[0::nb, 0::nb]).toarray()).max() == 0.0
+
+
+@pytest.mark.parametrize("name", ["C2s", "C4s", "C3s"])
+def test_mg_pcg_dense_solve_and_fewer_steps(name):
+    """PCG with the V-cycle preconditioner solves S_D + eps W to the dense solution,
+    in fewer steps than the element-block Jacobi PCG (the N1 point of the V-cycle)."""
+    from oracle.amg import SchurMG
+    s = configs.CONFIGS[name].build()
+    nb = s.layout.n_p_dof
+    eps = configs.eps_for(s)
+    SD = O.schur_diag(s.M, s.B)
+    Se = (SD + eps * sp.identity(SD.shape[0])).tocsr()
+    b = s.B @ (RNG.normal(size=s.layout.n_u) / s.M.diagonal())
+    x, its_mg, ok = O.pcg(Se, SchurMG(SD, nb), b, 1e-14, 1000)
+    xd = np.linalg.solve(Se.toarray(), b)
+    assert ok and np.abs(x - xd).max() <= 1e-10 * np.abs(xd).max()
+    _, its_j, ok_j = O.pcg(Se, O.block_jacobi_inv(Se, nb), b, 1e-14, 10000)
+    assert ok_j and its_mg < its_j
+
+
+def test_pcg_k_exact_preconditioner_and_limit():
+    """pcg_k (kind 5, reading R24): with the exact inverse as preconditioner it stops
+    after one step with the exact solution; with the Woodbury-diag preconditioner and
+    a small tolerance it converges to the dense K^-1 b, K = M + B^T (eps W)^-1 B."""
+    s = configs.CONFIGS["C5t"].build()
+    eps = configs.eps_for(s)
+    P = O.Preconditioner(O.PRECOND_BLOCK_REG_M, s.M, s.B, eps=eps, block=s.layout.n_p_dof)
+    K = (s.M + s.B.T @ s.B / eps).toarray()
+    b = RNG.normal(size=s.layout.n_u)
+    xd = np.linalg.solve(K, b)
+    Kinv = np.linalg.inv(K)
+    y, its, ok = O.pcg_k(P.kmul, lambda r: Kinv @ r, b, 1e-8, 10)
+    assert ok and its == 1 and np.abs(y - xd).max() <= 1e-7 * np.abs(xd).max()
+    y, its, ok = O.pcg_k(P.kmul, lambda r: P.woodbury_d(r, 1e-14), b, 1e-9, 2000)
+    assert ok and np.abs(y - xd).max() <= 1e-6 * np.abs(xd).max()
+    assert np.abs(P.kmul(b) - K @ b).max() <= 1e-12 * np.abs(K @ b).max()
+
+
+def test_block_reg_m_gmres_vs_lu_c5t():
+    """Kind 5 converges on the C5-type mesh where the diag(M) Block-Reg stagnates
+    (DESIGN.md §7), to the LU solution."""
+    s = configs.CONFIGS["C5t"].build()
+    eps = configs.eps_for(s)
+    xd = O.dense_solve(s.M, s.B, s.rhs)
+    r = O.solve(s.M, s.B, s.rhs, O.PRECOND_BLOCK_REG_M, 1e-10, 50, eps=eps, block=s.layout.n_p_dof)
+    assert r.converged and r.rel_residual_true <= 1e-10
+    nu = s.layout.n_u
+    for sl in (slice(0, nu), slice(nu, None)):
+        assert np.abs(r.x[sl] - xd[sl]).max() <= 1e-8 * np.abs(xd[sl]).max()
+    r2 = O.solve(s.M, s.B, s.rhs, O.PRECOND_BLOCK_REG, 1e-10, 50, eps=eps, block=s.layout.n_p_dof, maxit=100)
+    assert not r2.converged

@@ -85,6 +85,9 @@ CONFIGS = {
     "C3s": Config("C3s", "cube", 16, 0, (BLOCK_SCHUR,), 50, block=2, seed=3),
     "C4s": Config("C4s", "cube", 6, 2, (BLOCK_SCHUR, BLOCK_REG), 50),
     "C5s": Config("C5s", "pairs", 12, 1, (BLOCK_REG,), 50, block=3, seed=5),
+    # C5-type at 6^3 (two K blocks per axis): the size at which the oracle finishes the
+    # kind-5 solve (PCG on M + B^T (eps W)^-1 B inside FGMRES, R24) in seconds
+    "C5t": Config("C5t", "pairs", 6, 1, (BLOCK_REG,), 50, block=3, seed=5),
 }
 
 
