@@ -219,22 +219,26 @@ class AMG:
 
 
 class SchurMG:
-    """V-cycle of S_D used as the preconditioner of Block-Reg's inner PCG on
-    S_D + eps W ("use it ... as the PCG preconditioner inside
-    Block-Reg"; reading R23).  A fixed symmetric positive definite
-    operator, so plain PCG applies.
+    """V-cycle used as the preconditioner of Block-Reg's inner PCG on
+    S_eps = S_D + eps W ("use it ... as the PCG preconditioner
+    inside Block-Reg"; reading R23).  It is built on the matrix S handed
+    in, and oracle.solver hands in S_eps itself, not S_D: where K is small, eps W
+    exceeds the local spectrum of S_D, and a V-cycle of S_D alone leaves
+    cond(V S_eps) ~ 1 + eps / lambda_min (C5-type 12^3: 38 PCG steps to 1e-6 with
+    the V-cycle of S_D, 8 with the V-cycle of S_eps, 58 with block Jacobi).
+    A fixed symmetric positive definite operator, so plain PCG applies.
 
-      * n_p = 1 (k = 0): one V-cycle of AMG(S_D), exactly the kind-3 V-cycle above.
+      * n_p = 1 (k = 0): one V-cycle of AMG(S), the kind-3 construction above.
       * n_p > 1 (k >= 1), two-grid p-multigrid onto the element-mean moment:
-          C(b)  = degree-DEGREE Chebyshev with the element-block Jacobi D_B of S_D
-                  on [2/RATIO, 2] (oracle.solver.chebyshev; lambda_max(D_B^-1 S_D) <= 2,
-                  reading R15), x0 = 0
+          C(b)  = degree-DEGREE Chebyshev with the element-block Jacobi D_B of S
+                  on [2/RATIO, 2] (oracle.solver.chebyshev; lambda_max(D_B^-1 S) <= 2,
+                  reading R15: x'S_eps x <= 2 x'D_B x + eps x'W x), x0 = 0
           R r   = r[0::n_p]   (pressure moments are element-major with the mean
                   moment (1/|P|) int q first: a constant pressure has zero
                   higher moments, so injection of the mean is the P_0 coarse space)
-          S_c   = R S_D R^T = S_D[0::n_p, 0::n_p], solved by one V-cycle of AMG(S_c)
-          V(b)  : x = C(b); r = b - S_D x; x[0::n_p] += AMG(S_c).vcycle(r[0::n_p]);
-                  x += C(b - S_D x)
+          S_c   = R S R^T = S[0::n_p, 0::n_p], solved by one V-cycle of AMG(S_c)
+          V(b)  : x = C(b); r = b - S x; x[0::n_p] += AMG(S_c).vcycle(r[0::n_p]);
+                  x += C(b - S x)
     """
 
     def __init__(self, S, nb, DBinv=None):

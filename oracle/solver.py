@@ -13,7 +13,7 @@ Plain fp64 numpy/scipy, written in the order of the paper / SURVEY.md §8(c):
   * block_reg        B_2^-1 = (eps W)^-1, B_1^-1 by Woodbury with diag(M)
                      and an inner PCG on S_D + eps W             (reading R16)
                      whose preconditioner is the element-block Jacobi of
-                     S_D + eps W (inner_precond = 0) or one V-cycle of S_D
+                     S_D + eps W (inner_precond = 0) or one V-cycle of S_D + eps W
                      (inner_precond = 1, oracle/amg.py SchurMG; N1, reading R23)
   * block_reg_m      kind 5: B_2^-1 = (eps W)^-1, B_1^-1 y = PCG on
                      K = M + B^T (eps W)^-1 B (the paper's regularised velocity
@@ -44,7 +44,7 @@ PRECOND_BLOCK_SCHUR_AMG = 3     # Block-Schur with one aggregation V-cycle on S_
 PRECOND_BLOCK_SCHUR_AMG_F32 = 4  # the same V-cycle in FP32 inside the FP64 GMRES
 PRECOND_BLOCK_REG_M = 5          # Block-Reg with an M-aware velocity block: PCG on M + B^T (eps W)^-1 B (R24)
 INNER_JACOBI = 0                 # Block-Reg inner PCG preconditioner: element-block Jacobi of S_D + eps W
-INNER_MG = 1                     # ... one V-cycle of S_D (oracle/amg.py SchurMG)
+INNER_MG = 1                     # ... one V-cycle of S_D + eps W (oracle/amg.py SchurMG)
 
 
 def spmv_saddle(M, B, x):
@@ -230,7 +230,7 @@ class Preconditioner:
             self.Seps = (self.SD + self.eps * sp.identity(self.SD.shape[0], format="csr")).tocsr()
             if self.inner_precond == INNER_MG:
                 from .amg import SchurMG
-                self.inner_prec = SchurMG(self.SD, self.block, self.DBinv if self.block > 1 else None)
+                self.inner_prec = SchurMG(self.Seps, self.block)
             else:
                 self.inner_prec = block_jacobi_inv(self.Seps, self.block)
 
