@@ -16,8 +16,14 @@
  *     iteration on S_D = B diag(M)^-1 B^T (reading R15; the paper
  *     uses an exact MUMPS solve).
  *   Block-Reg: B_2^-1 = (eps W)^-1; B_1^-1 = (diag(M) + B^T (eps W)^-1 B)^-1
- *     applied by the Woodbury identity with an inner Jacobi-PCG on
- *     S_D + eps W (reading R16; the paper uses GAMG on A + B^T W^-1 B).
+ *     applied by the Woodbury identity with an inner PCG on S_D + eps W,
+ *     preconditioned by one V-cycle of S_D + eps W or by its element-block Jacobi
+ *     (readings R16, R23; the paper uses GAMG on A + B^T W^-1 B).
+ *   Block-Reg-M (kind 5, reading R24): the same B_2, and B_1^-1 y = PCG on the
+ *     paper's regularised velocity block K = M + B^T (eps W)^-1 B itself
+ *     (P:981-984), preconditioned by the kind-2 B_1, to a relative tolerance
+ *     k_rtol: the M-aware stand-in for GAMG where diag(M) is a poor model of M
+ *     (anisotropic K, config C5).
  *
  * Everything runs in FP64 on the CUDA device; there is no CPU fallback.  A
  * host-side CSR input is copied to the device during upload; every later step
@@ -54,7 +60,10 @@ enum {
 enum { VEM_PRECOND_NONE = 0, VEM_PRECOND_BLOCK_SCHUR = 1, VEM_PRECOND_BLOCK_REG = 2, VEM_PRECOND_BLOCK_SCHUR_AMG = 3,
        /* kind 3 with the V-cycle in FP32 (hierarchy values and vectors), GMRES and the
         * saddle operator in FP64: the mixed-precision preconditioner of SURVEY.md §8(f) N4 */
-       VEM_PRECOND_BLOCK_SCHUR_AMG_F32 = 4 };
+       VEM_PRECOND_BLOCK_SCHUR_AMG_F32 = 4,
+       /* Block-Reg with the M-aware velocity block: B_1^-1 = PCG on K = M + B^T (eps W)^-1 B
+        * preconditioned by the kind-2 Woodbury block (reading R24) */
+       VEM_PRECOND_BLOCK_REG_M = 5 };
 
 typedef struct vem_ctx vem_ctx;    /* opaque; owns every device buffer it allocates */
 
@@ -94,6 +103,17 @@ typedef struct {
                              (rows sorted by length in 4096-row windows, element blocks
                              kept whole); invisible to the caller (rhs, u, p and every
                              operator entry point stay in the caller's numbering); 0: off */
+  int32_t inner_precond;  /* Block-Reg inner PCG preconditioner: 1 (default) one V-cycle of
+                             S_D + eps W (n_p_dof = 1: the kind-3 aggregation hierarchy built
+                             on S_D + eps W; n_p_dof > 1: element-block-Jacobi Chebyshev(3)
+                             smoothing + injection of the element-mean moment + that hierarchy
+                             on the mean-moment block; reading R23); 0: element-block Jacobi */
+  int32_t k_maxit;        /* kind 5: iteration cap of the PCG on K per apply (default 500)  */
+  double  k_rtol;         /* kind 5: the PCG on K stops at sqrt(r.z) <= k_rtol sqrt(r0.z0)
+                             (default 0.1)                                                 */
+  double  k_inner_rtol;   /* kind 5: tolerance of the inner PCG on S_D + eps W inside the
+                             Woodbury preconditioner of the PCG on K (default 1e-6)         */
+  int32_t mg_chunk;       /* MG-PCG steps per host convergence poll (default 2)             */
 } vem_opts;
 
 typedef struct {
@@ -103,7 +123,8 @@ typedef struct {
   int32_t converged;
   int32_t breakdown;
   int32_t cycles;
-  int64_t inner_iterations;       /* Block-Reg: total inner PCG steps                     */
+  int64_t inner_iterations;       /* Block-Reg: total inner PCG steps (on S_D + eps W)    */
+  int64_t k_iterations;           /* kind 5: total steps of the PCG on K                   */
   double  rel_residual_true;      /* ||b - A x|| / ||b|| at exit                           */
   double  rel_residual_est;       /* last Givens estimate |g_{j+1}| / ||b||               */
   double  setup_ms;               /* upload + device format / S_D build                   */
@@ -212,6 +233,12 @@ int vem_mixed_kernel_stats(vem_ctx *ctx, vem_kernel_stats *stats, int32_t reset)
 /* Size of level `level` of the S_D aggregation hierarchy (kind 3): rows and
  * nonzeros; VEM_ERR_INVALID if the level does not exist. */
 int vem_mixed_amg_level(vem_ctx *ctx, int32_t level, int64_t *n, int64_t *nnz);
+
+/* The same for the S_D + eps W hierarchy that preconditions Block-Reg's inner PCG
+ * (opts.inner_precond = 1, reading R23; level 0 is S_D + eps W itself when
+ * n_p_dof = 1 and its element-mean block (S_D + eps W)[0::n_p, 0::n_p] otherwise).
+ * VEM_ERR_INVALID if the level does not exist (always, when eps <= 0 at upload). */
+int vem_mixed_inner_amg_level(vem_ctx *ctx, int32_t level, int64_t *n, int64_t *nnz);
 
 /* ---------------------------------------------------------------------------
  * Element-parallel assembly on the device

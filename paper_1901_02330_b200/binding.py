@@ -20,6 +20,7 @@ PRECOND_BLOCK_SCHUR = 1
 PRECOND_BLOCK_REG = 2
 PRECOND_BLOCK_SCHUR_AMG = 3
 PRECOND_BLOCK_SCHUR_AMG_F32 = 4
+PRECOND_BLOCK_REG_M = 5
 
 STATUS = {0: "OK", 1: "NOT_CONVERGED", 2: "BREAKDOWN", -1: "ERR_INVALID", -2: "ERR_DIAG_M",
           -3: "ERR_DIAG_S", -4: "ERR_CUDA", -5: "ERR_PRECOND", -6: "ERR_INNER"}
@@ -42,13 +43,16 @@ class vem_opts(C.Structure):
     _fields_ = [("restart", C.c_int32), ("cheb_degree", C.c_int32), ("cheb_ratio", C.c_double),
                 ("inner_rtol", C.c_double), ("inner_maxit", C.c_int32), ("use_graphs", C.c_int32),
                 ("timing", C.c_int32), ("pcg_chunk", C.c_int32), ("reorth", C.c_int32),
-                ("l2_persist", C.c_int32), ("reorder", C.c_int32)]
+                ("l2_persist", C.c_int32), ("reorder", C.c_int32), ("inner_precond", C.c_int32),
+                ("k_maxit", C.c_int32), ("k_rtol", C.c_double), ("k_inner_rtol", C.c_double),
+                ("mg_chunk", C.c_int32)]
 
 
 class vem_solve_report(C.Structure):
     _fields_ = [("status", C.c_int32), ("iterations", C.c_int32), ("restarts", C.c_int32),
                 ("converged", C.c_int32), ("breakdown", C.c_int32), ("cycles", C.c_int32),
-                ("inner_iterations", C.c_int64), ("rel_residual_true", C.c_double),
+                ("inner_iterations", C.c_int64), ("k_iterations", C.c_int64),
+                ("rel_residual_true", C.c_double),
                 ("rel_residual_est", C.c_double), ("setup_ms", C.c_double), ("solve_ms", C.c_double)]
 
     def as_dict(self):
@@ -98,7 +102,7 @@ EXPORTS = ["vem_mixed_default_options", "vem_mixed_upload", "vem_mixed_solve", "
            "vem_mixed_upload_assembled", "vem_mixed_assembled_free",
            "vem_mixed_spmv", "vem_mixed_schur_spmv", "vem_mixed_precond_apply", "vem_mixed_set_options",
            "vem_mixed_get_options", "vem_mixed_get_info", "vem_mixed_get_schur", "vem_mixed_kernel_stats",
-           "vem_mixed_amg_level", "vem_mixed_destroy", "vem_status_string", "vem_last_error"]
+           "vem_mixed_amg_level", "vem_mixed_inner_amg_level", "vem_mixed_destroy", "vem_status_string", "vem_last_error"]
 
 _lib = None
 
@@ -129,6 +133,7 @@ def load_library(path: str = LIB_PATH):
     lib.vem_mixed_get_schur.argtypes = [P, C.POINTER(C.c_int64), C.POINTER(C.c_int32), D]
     lib.vem_mixed_kernel_stats.argtypes = [P, C.POINTER(vem_kernel_stats), C.c_int32]
     lib.vem_mixed_amg_level.argtypes = [P, C.c_int32, C.POINTER(C.c_int64), C.POINTER(C.c_int64)]
+    lib.vem_mixed_inner_amg_level.argtypes = [P, C.c_int32, C.POINTER(C.c_int64), C.POINTER(C.c_int64)]
     lib.vem_mixed_assemble.argtypes = [C.POINTER(P), C.POINTER(vem_cell_class), C.c_int32, C.c_int64, C.c_int64, P]
     lib.vem_mixed_assemble_tets.argtypes = [C.POINTER(P), C.POINTER(vem_tet_class), C.c_int32, C.c_int64,
                                             C.c_int64, P]
@@ -294,6 +299,8 @@ class VemMixed:
             out_p = torch.empty(self.n_p, dtype=torch.float64, device=rhs.device)
         if rhs.numel() != self.n:
             raise ValueError("rhs has the wrong length")
+        if out_u.numel() != self.n_u or out_p.numel() != self.n_p:
+            raise ValueError("out_u / out_p must hold exactly n_u / n_p values")
         rep = vem_solve_report()
         rc = self._lib.vem_mixed_solve(self._h, _dptr(rhs), float(tol), int(maxit), int(precond),
                                        _dptr(out_u), _dptr(out_p), C.byref(rep))
@@ -310,6 +317,11 @@ class VemMixed:
             raise ValueError("rhs has the wrong length")
         u = np.empty(self.n_u) if u is None else u
         p = np.empty(self.n_p) if p is None else p
+        for name, a, size in (("u", u, self.n_u), ("p", p, self.n_p)):
+            # the C call writes 8 * size bytes through the raw pointer
+            if not (isinstance(a, np.ndarray) and a.dtype == np.float64 and a.flags.c_contiguous
+                    and a.flags.writeable and a.size == size):
+                raise ValueError(f"{name} must be a writeable C-contiguous float64 array of {size} values")
         rep = vem_solve_report()
         D = C.POINTER(C.c_double)
         rc = self._lib.vem_mixed_solve_host(self._h, rhs.ctypes.data_as(D), float(tol), int(maxit),
@@ -358,6 +370,16 @@ class VemMixed:
         for lev in range(self.info()["amg_levels"]):
             self._check(self._lib.vem_mixed_amg_level(self._h, lev, C.byref(n), C.byref(z)), "amg_level")
             out.append((n.value, z.value))
+        return out
+
+    def inner_amg_levels(self):
+        """(rows, nnz) per level of the S_D + eps W hierarchy of the inner MG-PCG (R23)."""
+        out = []
+        n, z = C.c_int64(), C.c_int64()
+        lev = 0
+        while self._lib.vem_mixed_inner_amg_level(self._h, lev, C.byref(n), C.byref(z)) == 0:
+            out.append((n.value, z.value))
+            lev += 1
         return out
 
     def kernel_stats(self, reset=False) -> dict:

@@ -1,6 +1,7 @@
 """Build libvem_mixed.so in-tree for sm_100a (nvcc, no torch dependency)."""
 from __future__ import annotations
 
+import hashlib
 import os
 import subprocess
 import sys
@@ -15,11 +16,26 @@ FLAGS = ["-gencode", "arch=compute_100a,code=sm_100a", "-O3", "-lineinfo", "-std
          "-Xcompiler", "-fPIC", "-shared", "-Xptxas", "-v"]
 
 
+STAMP = LIB + ".srchash"
+
+
+def source_hash() -> str:
+    """SHA-256 over the flags and the contents of every source the library is built from."""
+    h = hashlib.sha256(" ".join(FLAGS).encode())
+    for d in DEPS:
+        h.update(os.path.basename(d).encode())
+        with open(d, "rb") as f:
+            h.update(f.read())
+    return h.hexdigest()
+
+
 def needs_build() -> bool:
-    if not os.path.exists(LIB):
+    """Rebuild when the library is missing or was built from other sources (content hash,
+    not mtimes: a checkout or snapshot copy must never ship a stale .so)."""
+    if not (os.path.exists(LIB) and os.path.exists(STAMP)):
         return True
-    t = os.path.getmtime(LIB)
-    return any(os.path.getmtime(d) > t for d in DEPS)
+    with open(STAMP) as f:
+        return f.read().strip() != source_hash()
 
 
 def build(force: bool = False, verbose: bool = False) -> str:
@@ -30,6 +46,8 @@ def build(force: bool = False, verbose: bool = False) -> str:
             sys.stderr.write(res.stdout + res.stderr)
             raise RuntimeError("nvcc failed building libvem_mixed.so")
         os.replace(LIB + ".tmp", LIB)
+        with open(STAMP, "w") as f:
+            f.write(source_hash() + "\n")
         if verbose:
             sys.stderr.write(res.stderr)
     return LIB

@@ -38,6 +38,12 @@ struct PcgState {
   double rz, alpha, beta, bn, tol_abs, rr;
 };
 
+// PCG on K = M + B^T (eps W)^-1 B (precond kind 5, blockreg_m.cuh)
+struct KState {
+  int active, its, maxit, failed;
+  double rz, rz0, alpha, beta, rtol;
+};
+
 struct DevState {
   GmresState g;
   PcgState p;
@@ -50,6 +56,7 @@ struct DevState {
   double lmax;
   int setup_err;
   int pad2;
+  KState k;
 };
 
 // ---------------------------------------------------------------------------

@@ -28,6 +28,7 @@
 #include "amg.cuh"
 #include "assembly.cuh"
 #include "amg_apply.cuh"
+#include "blockreg_m.cuh"
 
 namespace {
 
@@ -71,6 +72,15 @@ struct AmgLevel {
   unsigned short *vc_c16 = nullptr;
   size_t vc_smem_d = 0, vc_smem_f = 0;
   bool vc_ok = false;
+};
+
+// one aggregation hierarchy: the S_D one of kinds 3/4 (Ctx::amg) or the S_D + eps W one that
+// preconditions Block-Reg's inner PCG (Ctx::amge; on the element-mean block when n_p_dof > 1)
+struct AmgHier {
+  std::vector<AmgLevel> lv;
+  double *cinv = nullptr;      // dense inverse of the coarsest level
+  float *cinv_f = nullptr;     // its FP32 copy (kind 4)
+  bool dense = false;
 };
 
 // level data of the V-cycle in precision T
@@ -125,9 +135,8 @@ struct Ctx {
   double *dBinv = nullptr, *dBeinv = nullptr, *pz = nullptr;
   double *cheb_pool = nullptr;          // D^-1, r, d0, d1, x of the Chebyshev steps, contiguous
   double *h_rhs = nullptr, *h_u = nullptr, *h_p = nullptr;   // vem_mixed_solve_host staging
-  std::vector<AmgLevel> amg;                     // S_D hierarchy (kind 3); empty when n_p_dof > 1
-  double *amg_cinv = nullptr;                    // dense inverse of the coarsest level
-  float *amg_cinv_f = nullptr;                   // its FP32 copy (kind 4)
+  AmgHier amg;                                   // S_D hierarchy (kinds 3, 4); empty when n_p_dof > 1
+  AmgHier amge;                                  // S_D + eps W hierarchy (inner PCG of kinds 2, 5; R23)
   bool amg_f32 = false;                          // FP32 mirror built
   int amg_coarse_degree = 8;                     // Chebyshev degree of a non-dense coarsest level
   int amg_max_levels = 12;                       // AMG_MAX_LEVELS (VEM_AMG_MAX_LEVELS: tests only)
@@ -145,7 +154,6 @@ struct Ctx {
   float *f32_pool = nullptr;                     // kind 4 fine-level vectors (L2-persisting window)
   size_t f32_pool_bytes = 0;
   int l2_window_pool = -1;                       // pool under the window: 0 FP64 Chebyshev, 1 FP32
-  bool amg_dense = false;
   size_t cheb_pool_bytes = 0;
   size_t l2_window_bytes = 0;           // bytes of the pool under a persisting L2 access window
   // device matrices
@@ -177,6 +185,21 @@ struct Ctx {
   double *x = nullptr, *b = nullptr, *z = nullptr, *t = nullptr;
   double *cr = nullptr, *cd0 = nullptr, *cd1 = nullptr, *cx = nullptr;           // Chebyshev
   double *px = nullptr, *pr = nullptr, *pp0 = nullptr, *pp1 = nullptr, *pq = nullptr, *pb = nullptr;  // PCG
+  // MG-PCG (inner_precond = 1, R23): residual / preconditioned residual of the inner PCG
+  // (n_p_dof = 1: the level-0 b / x of the S_eps hierarchy; else pr / pz), the S_eps matrix the
+  // hierarchy `amge` starts from (n_p_dof = 1: S_D values with the shifted diagonal; else the CSR
+  // of S_eps[0::n_p, 0::n_p] in the caller's element numbering)
+  double *mg_r = nullptr, *mg_z = nullptr;
+  int *se_rp = nullptr, *se_ci = nullptr;
+  double *se_va = nullptr, *se_dinv = nullptr, *se_diag = nullptr;
+  long se_n = 0, se_nnz = 0;
+  cudaGraphExec_t pcgm_exec = nullptr;
+  int pcgm_exec_chunk = 0;
+  // K-PCG (kind 5, R24): p (velocity part of kx = [p; B p]), r, z, q
+  double *kx = nullptr, *kr = nullptr, *kz = nullptr, *kq = nullptr;
+  int64_t k_its_total = 0;
+  bool trace_k = false;                          // VEM_TRACE_K=1: one stderr line per kind-5 apply
+  bool k_failed = false;
   double *part = nullptr;
   unsigned *counter = nullptr;
   DevState *st = nullptr;
@@ -184,7 +207,7 @@ struct Ctx {
   int *derr = nullptr;
   long part_cap = 0;
   // graphs
-  cudaGraphExec_t cycle_exec[5] = {nullptr, nullptr, nullptr, nullptr, nullptr};   // per precond kind
+  cudaGraphExec_t cycle_exec[6] = {nullptr, nullptr, nullptr, nullptr, nullptr, nullptr};   // per precond kind
   cudaGraphExec_t pcg_exec = nullptr;
   int pcg_exec_chunk = 0;
   // timing
@@ -197,7 +220,7 @@ struct Ctx {
   // the host reads the pairs of the executed steps after every cycle.
   int sample_slot = -1;
   bool sample_recorded = false;        // set when an enqueue recorded a sample pair
-  bool sample_recorded_kind[5] = {false, false, false, false, false};
+  bool sample_recorded_kind[6] = {false, false, false, false, false, false};
   std::vector<cudaEvent_t> samp_a, samp_b;
   // misc
   std::string err;
@@ -371,7 +394,12 @@ struct ChebBlkL {
 };
 template <int NB>
 struct PcgInitBlkL {
-  static void run(Ctx *c, const int *gate);
+  static void run(Ctx *c, double rtol, const int *gate);
+};
+template <int NB>
+struct MgBlkL {
+  static void run(Ctx *c, const double *r, const double *dold, double *dnew, double *x, double c1, double c2,
+                  int init, int acc, const int *gate);
 };
 template <int NB>
 struct PcgVecBlkL {
@@ -434,11 +462,17 @@ void ChebBlkL<NB>::run(Ctx *c, const double *dold, double *dnew, double c1, doub
                                                               last, zp, gate);
 }
 template <int NB>
-void PcgInitBlkL<NB>::run(Ctx *c, const int *gate) {
+void PcgInitBlkL<NB>::run(Ctx *c, double rtol, const int *gate) {
   const long ne = c->np / NB;
   k_pcg_init_blk<NB><<<grid_blk<NB>(c, ne), 256, 0, c->stream>>>(ne, c->dBeinv, c->pb, c->px, c->pr, c->pz, c->pp0,
-                                                               c->part, c->counter, c->st, c->opts.inner_rtol,
+                                                               c->part, c->counter, c->st, rtol,
                                                                c->opts.inner_maxit, gate);
+}
+template <int NB>
+void MgBlkL<NB>::run(Ctx *c, const double *r, const double *dold, double *dnew, double *x, double c1, double c2,
+                     int init, int acc, const int *gate) {
+  const long ne = c->np / NB;
+  k_mg_blk<NB><<<grid_blk<NB>(c, ne), 256, 0, c->stream>>>(ne, c->dBeinv, r, dold, dnew, x, c1, c2, init, acc, gate);
 }
 template <int NB>
 void PcgVecBlkL<NB>::run(Ctx *c, const double *p) {
@@ -557,6 +591,24 @@ int enqueue_block_schur(Ctx *c, const double *v, const double *scale, double *z,
 }
 
 int run_pcg(Ctx *c, int64_t *inner_its);
+int run_pcg_mg(Ctx *c, double rtol, const int *gate, int64_t *inner_its);
+
+// Inner solve px = (S_D + eps W)^-1 pb by PCG from x0 = 0 to ||r|| <= rtol ||pb||, preconditioned by
+// one V-cycle of S_eps (inner_precond = 1, reading R23) or its element-block Jacobi (0, R16)
+int run_inner(Ctx *c, double rtol, const int *gate, int64_t *inner_its) {
+  if (c->opts.inner_precond == 1) return run_pcg_mg(c, rtol, gate, inner_its);
+  {
+    TimeScope ts(c, VEM_K_PRECOND_VEC);
+    if (c->nb > 1)
+      dispatch_nb<PcgInitBlkL>(c->nb, c, rtol, gate);
+    else
+      k_pcg_init<<<grid_stream(c, c->np), NT, 0, c->stream>>>(c->np, c->pb, c->dSepsinv, c->px, c->pr, c->pp0,
+                                                              c->part, c->counter, c->st, rtol,
+                                                              c->opts.inner_maxit, gate);
+  }
+  CKL();
+  return run_pcg(c, inner_its);
+}
 
 int enqueue_block_reg(Ctx *c, const double *v, const double *scale, double *z, const int *gate,
                       int64_t *inner_its) {
@@ -570,17 +622,7 @@ int enqueue_block_reg(Ctx *c, const double *v, const double *scale, double *z, c
     launch_spmv(c, c->nu, c->np, (const double *)z, c->pb - c->nu, nullptr, 0, gate);
   }
   CKL();
-  {
-    TimeScope ts(c, VEM_K_PRECOND_VEC);
-    if (c->nb > 1)
-      dispatch_nb<PcgInitBlkL>(c->nb, c, gate);
-    else
-      k_pcg_init<<<grid_stream(c, c->np), NT, 0, c->stream>>>(c->np, c->pb, c->dSepsinv, c->px, c->pr, c->pp0,
-                                                              c->part, c->counter, c->st, c->opts.inner_rtol,
-                                                              c->opts.inner_maxit, gate);
-  }
-  CKL();
-  int rc = run_pcg(c, inner_its);
+  int rc = run_inner(c, c->opts.inner_rtol, gate, inner_its);
   if (rc) return rc;
   {
     TimeScope ts(c, VEM_K_PRECOND_VEC);
@@ -825,11 +867,11 @@ void amg_residual(Ctx *c, AmgLevel &L, const int *gate) {
 }
 
 template <typename T>
-const T *amg_cinv(Ctx *c);
+const T *amg_cinv(const AmgHier &H);
 template <>
-const double *amg_cinv<double>(Ctx *c) { return c->amg_cinv; }
+const double *amg_cinv<double>(const AmgHier &H) { return H.cinv; }
 template <>
-const float *amg_cinv<float>(Ctx *c) { return c->amg_cinv_f; }
+const float *amg_cinv<float>(const AmgHier &H) { return H.cinv_f; }
 
 // coarsest-level Chebyshev(d) from x0 = 0 as one 16-CTA cluster launch (k_vc_coarse_cluster)
 template <typename T>
@@ -864,13 +906,13 @@ void amg_coarse_cluster(Ctx *c, AmgLevel &L, const int *gate) {
 }
 
 template <typename T>
-void amg_vcycle(Ctx *c, size_t l, const int *gate) {
-  AmgLevel &L = c->amg[l];
+void amg_vcycle(Ctx *c, AmgHier &H, size_t l, const int *gate) {
+  AmgLevel &L = H.lv[l];
   const Lv<T> D{L};
-  if (l + 1 == c->amg.size()) {   // coarsest
-    if (c->amg_dense) {
+  if (l + 1 == H.lv.size()) {   // coarsest
+    if (H.dense) {
       TimeScope ts(c, VEM_K_PRECOND_VEC, (double)sizeof(T) * L.n * L.n);
-      launch_plain(c, k_vc_dense_mv<T>, grid_for(L.n * 32), NT, L.n, amg_cinv<T>(c), D.b(), D.x(), gate);
+      launch_plain(c, k_vc_dense_mv<T>, grid_for(L.n * 32), NT, L.n, amg_cinv<T>(H), D.b(), D.x(), gate);
     } else if (L.vc_ok) {
       amg_coarse_cluster<T>(c, L, gate);
     } else {
@@ -878,9 +920,9 @@ void amg_vcycle(Ctx *c, size_t l, const int *gate) {
     }
     return;
   }
-  AmgLevel &C = c->amg[l + 1];
+  AmgLevel &C = H.lv[l + 1];
   const Lv<T> DC{C};
-  amg_smooth<T>(c, L, D.b(), D.x(), AMG_DEGREE, gate, l == 0);
+  amg_smooth<T>(c, L, D.b(), D.x(), AMG_DEGREE, gate, l == 0 && &H == &c->amg);
   amg_residual<T>(c, L, gate);
   if (L.sa) {
     TimeScope ts(c, VEM_K_PRECOND_VEC, (sizeof(T) + 4.0) * L.pnnz + sizeof(T) * (1.0 * L.n + C.n));
@@ -889,7 +931,7 @@ void amg_vcycle(Ctx *c, size_t l, const int *gate) {
     TimeScope ts(c, VEM_K_PRECOND_VEC, sizeof(T) * (2.0 * L.n + C.n));
     launch_plain(c, k_vc_restrict<T>, grid_stream(c, C.n), NT, C.n, L.moff, L.mem, D.t(), DC.b(), gate);
   }
-  amg_vcycle<T>(c, l + 1, gate);
+  amg_vcycle<T>(c, H, l + 1, gate);
   if (L.sa) {
     TimeScope ts(c, VEM_K_PRECOND_VEC, (sizeof(T) + 4.0) * L.pnnz + sizeof(T) * (2.0 * L.n + C.n));
     launch_plain(c, k_vc_sa_prolong_add<T>, grid_for(L.n), NT, L.n, SellT<T>{L.psoff, L.psci, D.psva()}, DC.x(),
@@ -907,9 +949,9 @@ void amg_vcycle(Ctx *c, size_t l, const int *gate) {
 template <typename T>
 int enqueue_block_schur_amg(Ctx *c, const double *v, const double *scale, double *z, const int *gate,
                             bool z_out = true) {
-  if (c->amg.empty()) return fail(c, VEM_ERR_PRECOND, "Block-Schur-AMG needs n_p_dof = 1 (k = 0)");
+  if (c->amg.lv.empty()) return fail(c, VEM_ERR_PRECOND, "Block-Schur-AMG needs n_p_dof = 1 (k = 0)");
   if (sizeof(T) == 4 && !c->amg_f32) return fail(c, VEM_ERR_PRECOND, "FP32 hierarchy not built");
-  AmgLevel &L0 = c->amg[0];
+  AmgLevel &L0 = c->amg.lv[0];
   const Lv<T> D0{L0};
   {
     TimeScope ts(c, VEM_K_PRECOND_VEC, z_out ? 24.0 * c->nu + (8.0 + sizeof(T)) * c->np : (8.0 + sizeof(T)) * c->np);
@@ -919,7 +961,7 @@ int enqueue_block_schur_amg(Ctx *c, const double *v, const double *scale, double
       launch_plain(c, k_vc_top<T>, grid_stream(c, c->np), NT, 0, c->np, v + c->nu, scale, nullptr, nullptr, D0.b(),
                                                                 gate);
   }
-  amg_vcycle<T>(c, 0, gate);
+  amg_vcycle<T>(c, c->amg, 0, gate);
   if (z_out) {
     TimeScope ts(c, VEM_K_PRECOND_VEC, (8.0 + sizeof(T)) * c->np);
     launch_plain(c, k_vc_out<T>, grid_stream(c, c->np), NT, c->np, D0.x(), z + c->nu, gate);
@@ -928,9 +970,237 @@ int enqueue_block_schur_amg(Ctx *c, const double *v, const double *scale, double
   return 0;
 }
 
+// ----------------------------------------------------------------------------
+// MG-PCG: inner PCG on S_eps = S_D + eps W preconditioned by one V-cycle of S_eps
+// (reading R23; oracle/amg.py SchurMG, oracle/solver.py pcg)
+// ----------------------------------------------------------------------------
+inline int grid_part(Ctx *c, long n) {   // fixed grid of the two-stage dot products
+  return (int)std::max<long>(1, std::min<long>((n + NT - 1) / NT, (long)c->sm_count * 8));
+}
+const int *gate_pcg(Ctx *c) { return &c->st->p.active; }
+const int *gate_k(Ctx *c) { return &c->st->k.active; }
+
+// mg_z = V(mg_r)
+int enqueue_schur_mg(Ctx *c, const int *gate) {
+  AmgHier &H = c->amge;
+  if (H.lv.empty()) return fail(c, VEM_ERR_PRECOND, "S_eps hierarchy not built (eps <= 0 at upload)");
+  if (c->nb == 1) {   // mg_r / mg_z are the level-0 b / x
+    amg_vcycle<double>(c, H, 0, gate);
+    CKL();
+    return 0;
+  }
+  const long np = c->np, ne = np / c->nb;
+  double it;
+  std::vector<double> c1, c2;
+  amg_cheb_coeffs(2.0, AMG_DEGREE, it, c1, c2);   // lambda_max(D_B^-1 S_eps) <= 2 (R15)
+  const Sell S = sellS(c);
+  const double blk_bytes = 8.0 * np * (4 + c->nb);
+  auto smooth = [&](const double *b, int acc) {   // mg_z (+)= C_3(b)
+    {
+      TimeScope ts(c, VEM_K_PRECOND_VEC, blk_bytes);
+      dispatch_nb<MgBlkL>(c->nb, c, b, (const double *)nullptr, c->cd0, c->mg_z, 0.0, it, 1, acc, gate);
+    }
+    double *dold = c->cd0, *dnew = c->cd1;
+    const double *rb = b;
+    for (int i = 1; i < AMG_DEGREE; ++i) {
+      {
+        TimeScope ts(c, VEM_K_CHEB, 12.0 * c->nnzS + 32.0 * np);
+        k_seps_resid<<<grid_for(np), NT, 0, c->stream>>>(np, S, c->wdiag, c->eps, dold, rb, c->cr, gate);
+      }
+      rb = c->cr;
+      TimeScope ts(c, VEM_K_PRECOND_VEC, blk_bytes + 8.0 * np);
+      dispatch_nb<MgBlkL>(c->nb, c, (const double *)c->cr, (const double *)dold, dnew, c->mg_z, c1[i - 1], c2[i - 1],
+                          0, 1, gate);
+      std::swap(dold, dnew);
+    }
+  };
+  smooth(c->mg_r, 0);
+  {
+    TimeScope ts(c, VEM_K_CHEB, 12.0 * c->nnzS + 32.0 * np);
+    k_seps_resid<<<grid_for(np), NT, 0, c->stream>>>(np, S, c->wdiag, c->eps, c->mg_z, c->mg_r, c->cx, gate);
+  }
+  {
+    TimeScope ts(c, VEM_K_PRECOND_VEC, 20.0 * ne);
+    k_mg_inject<<<grid_stream(c, ne), NT, 0, c->stream>>>(ne, c->nb, c->perm_p, c->cx, H.lv[0].b, gate);
+  }
+  amg_vcycle<double>(c, H, 0, gate);
+  {
+    TimeScope ts(c, VEM_K_PRECOND_VEC, 28.0 * ne);
+    k_mg_prolong<<<grid_stream(c, ne), NT, 0, c->stream>>>(ne, c->nb, c->perm_p, H.lv[0].x, c->mg_z, gate);
+  }
+  {
+    TimeScope ts(c, VEM_K_CHEB, 12.0 * c->nnzS + 32.0 * np);
+    k_seps_resid<<<grid_for(np), NT, 0, c->stream>>>(np, S, c->wdiag, c->eps, c->mg_z, c->mg_r, c->cx, gate);
+  }
+  smooth(c->cx, 1);
+  CKL();
+  return 0;
+}
+
+int enqueue_pcgm_dir(Ctx *c, int first) {   // z = V(r); beta; p = z + beta p
+  int rc = enqueue_schur_mg(c, gate_pcg(c));
+  if (rc) return rc;
+  const int gp = grid_part(c, c->np);
+  TimeScope ts(c, VEM_K_PCG_VEC, 40.0 * c->np);
+  k_dot_part<<<gp, NT, 0, c->stream>>>(c->np, c->mg_r, c->mg_z, c->part, gate_pcg(c));
+  k_pcgm_beta<<<1, 1024, 0, c->stream>>>(gp, c->part, c->st, first);
+  k_pcg_pupd<<<grid_stream(c, c->np), NT, 0, c->stream>>>(c->np, c->mg_z, c->pp0, c->st);
+  return 0;
+}
+
+int enqueue_pcgm_steps(Ctx *c, int nsteps) {
+  const int g = grid_for(c->np), gp = grid_part(c, c->np);
+  for (int s = 0; s < nsteps; ++s) {
+    {
+      TimeScope ts(c, VEM_K_PCG_SPMV, 12.0 * c->nnzS + 32.0 * c->np);
+      k_pcg_spmv_p<<<g, NT, 0, c->stream>>>(c->np, sellS(c), c->wdiag, c->eps, c->pp0, c->pq, c->part, c->counter,
+                                            c->st, 1);
+      k_pcg_alpha<<<1, 1024, 0, c->stream>>>(g, c->part, c->st);
+    }
+    {
+      TimeScope ts(c, VEM_K_PCG_VEC, 48.0 * c->np);
+      k_pcgm_xr<<<gp, NT, 0, c->stream>>>(c->np, c->pp0, c->pq, c->px, c->mg_r, c->part, c->st);
+      k_pcgm_conv<<<1, 1024, 0, c->stream>>>(gp, c->part, c->st);
+    }
+    int rc = enqueue_pcgm_dir(c, 0);
+    if (rc) return rc;
+  }
+  CKL();
+  return 0;
+}
+
+int run_pcg_mg(Ctx *c, double rtol, const int *gate, int64_t *inner_its) {
+  const int gp = grid_part(c, c->np);
+  {
+    TimeScope ts(c, VEM_K_PCG_VEC, 32.0 * c->np);
+    k_pcgm_init<<<gp, NT, 0, c->stream>>>(c->np, c->pb, c->px, c->mg_r, c->pp0, c->part, gate);
+    k_pcgm_init_fin<<<1, 1024, 0, c->stream>>>(gp, c->part, c->st, rtol, c->opts.inner_maxit, gate);
+  }
+  int rc = enqueue_pcgm_dir(c, 1);
+  if (rc) return rc;
+  CKL();
+  int chunk = std::max(1, std::min(c->opts.pcg_chunk, c->opts.mg_chunk));
+  const bool graphs = c->opts.use_graphs && c->opts.timing != 1 && !c->capturing;
+  if (graphs && (!c->pcgm_exec || c->pcgm_exec_chunk != chunk)) {
+    if (c->pcgm_exec) cudaGraphExecDestroy(c->pcgm_exec);
+    c->pcgm_exec = nullptr;
+    cudaGraph_t g;
+    c->capturing = true;
+    CK(cudaStreamBeginCapture(c->stream, cudaStreamCaptureModeThreadLocal));
+    rc = enqueue_pcgm_steps(c, chunk);
+    cudaError_t e = cudaStreamEndCapture(c->stream, &g);
+    c->capturing = false;
+    if (rc) return rc;
+    if (e != cudaSuccess) return fail(c, VEM_ERR_CUDA, "MG-PCG capture failed: %s", cudaGetErrorString(e));
+    CK(cudaGraphInstantiate(&c->pcgm_exec, g, 0));
+    cudaGraphDestroy(g);
+    c->pcgm_exec_chunk = chunk;
+  }
+  for (;;) {
+    if (graphs) {
+      CK(cudaGraphLaunch(c->pcgm_exec, c->stream));
+    } else {
+      rc = enqueue_pcgm_steps(c, chunk);
+      if (rc) return rc;
+    }
+    CK(cudaMemcpyAsync(&c->hst->p, &c->st->p, sizeof(PcgState), cudaMemcpyDeviceToHost, c->stream));
+    CK(cudaStreamSynchronize(c->stream));
+    flush_timing(c);
+    if (!c->hst->p.active) break;
+  }
+  if (inner_its) *inner_its += c->hst->p.its;
+  if (c->hst->p.failed) return fail(c, VEM_ERR_INNER, "inner MG-PCG did not reach %g in %d steps", rtol,
+                                    c->opts.inner_maxit);
+  return 0;
+}
+
+// ----------------------------------------------------------------------------
+// Block-Reg-M apply (kind 5, reading R24; oracle/solver.py pcg_k): z_p = s v_p / (eps W),
+// z_u = PCG on K = M + B^T (eps W)^-1 B from y0 = 0, preconditioned by the kind-2 Woodbury
+// block (its inner solve to k_inner_rtol), until sqrt(r.z) <= k_rtol sqrt(r0.z0)
+// ----------------------------------------------------------------------------
+int enqueue_block_reg_m(Ctx *c, const double *v, const double *scale, double *z, const int *gate,
+                        int64_t *inner_its) {
+  if (!c->kx) {
+    DA(c->kx, c->n);
+    DA(c->kr, c->nu);
+    DA(c->kz, c->nu);
+    DA(c->kq, c->nu);
+  }
+  const long nu = c->nu, np = c->np;
+  const int gu = grid_stream(c, nu), gp = grid_part(c, nu);
+  const double inv_eps = 1.0 / c->eps;
+  auto woodbury = [&](const int *g2) -> int {   // kz = (diag M + B^T (eps W)^-1 B)^-1 kr
+    {
+      TimeScope ts(c, VEM_K_PRECOND_VEC, 24.0 * nu);
+      k_k_t0<<<gu, NT, 0, c->stream>>>(nu, c->kr, c->dMinv, c->kz, g2);
+    }
+    {
+      TimeScope ts(c, VEM_K_PRECOND_VEC, 12.0 * c->nnzB + 8.0 * c->n);
+      launch_spmv(c, nu, np, (const double *)c->kz, c->pb - nu, nullptr, 0, g2);
+    }
+    CKL();
+    int rc = run_inner(c, c->opts.k_inner_rtol, g2, inner_its);
+    if (rc) return rc;
+    TimeScope ts(c, VEM_K_PRECOND_VEC, 12.0 * (c->nnzM + c->nnzB) + 8.0 * c->n + 16.0 * nu);
+    launch_br_finish(c, c->kz, g2);
+    return 0;
+  };
+  {
+    TimeScope ts(c, VEM_K_PRECOND_VEC, 8.0 * (4 * nu + 2 * np));
+    k_k_init<<<grid_stream(c, c->n), NT, 0, c->stream>>>(nu, np, v, scale, c->wdiag, inv_eps, c->kr, z, c->kx, gate);
+  }
+  int rc = woodbury(gate);
+  if (rc) return rc;
+  {
+    TimeScope ts(c, VEM_K_PRECOND_VEC, 40.0 * nu);
+    k_dot_part<<<gp, NT, 0, c->stream>>>(nu, c->kr, c->kz, c->part, gate);
+    k_k_rz<<<1, 1024, 0, c->stream>>>(gp, c->part, c->st, 1, c->opts.k_rtol, c->opts.k_maxit, gate);
+    k_k_pupd<<<gu, NT, 0, c->stream>>>(nu, c->kz, c->kx, c->st);
+  }
+  CKL();
+  for (;;) {
+    {
+      TimeScope ts(c, VEM_K_SPMV, 12.0 * c->nnzA + 16.0 * c->n + 8.0 * nu);
+      launch_spmv(c, nu, np, (const double *)c->kx, c->kx, nullptr, 0, gate_k(c));   // kx[nu:] = B p
+      const int g = grid_for(nu);
+      k_kmul<<<g, NT, 0, c->stream>>>(nu, sellA(c), c->kx, c->wdiag, inv_eps, c->kq, c->part, gate_k(c));
+      k_k_alpha<<<1, 1024, 0, c->stream>>>(g, c->part, c->st);
+    }
+    {
+      TimeScope ts(c, VEM_K_PRECOND_VEC, 48.0 * nu);
+      k_k_xr<<<gu, NT, 0, c->stream>>>(nu, c->kx, c->kq, z, c->kr, c->st);
+    }
+    CKL();
+    rc = woodbury(gate_k(c));
+    if (rc) return rc;
+    {
+      TimeScope ts(c, VEM_K_PRECOND_VEC, 40.0 * nu);
+      k_dot_part<<<gp, NT, 0, c->stream>>>(nu, c->kr, c->kz, c->part, gate_k(c));
+      k_k_rz<<<1, 1024, 0, c->stream>>>(gp, c->part, c->st, 0, c->opts.k_rtol, c->opts.k_maxit, gate);
+      k_k_pupd<<<gu, NT, 0, c->stream>>>(nu, c->kz, c->kx, c->st);
+    }
+    CKL();
+    CK(cudaMemcpyAsync(&c->hst->k, &c->st->k, sizeof(KState), cudaMemcpyDeviceToHost, c->stream));
+    CK(cudaStreamSynchronize(c->stream));
+    flush_timing(c);
+    if (!c->hst->k.active) break;
+  }
+  c->k_its_total += c->hst->k.its;
+  c->k_failed |= c->hst->k.failed != 0;
+  if (c->trace_k)
+    fprintf(stderr, "[vem kind 5] K-PCG: %d steps%s, sqrt(rz/rz0) = %.3e, inner steps so far %lld\n", c->hst->k.its,
+            c->hst->k.failed ? " (cap reached)" : "", sqrt(fabs(c->hst->k.rz) / std::max(c->hst->k.rz0, 1e-300)),
+            inner_its ? (long long)*inner_its : 0LL);
+  return 0;
+}
+
 // FGMRES (Z stored) for the variable preconditioners: Block-Reg (inner PCG) and the
 // FP32 V-cycle (its rounding makes P^-1 (V y) differ from sum y_j P^-1 v_j)
-inline bool is_flexible(int kind) { return kind == VEM_PRECOND_BLOCK_REG || kind == VEM_PRECOND_BLOCK_SCHUR_AMG_F32; }
+inline bool is_flexible(int kind) {
+  return kind == VEM_PRECOND_BLOCK_REG || kind == VEM_PRECOND_BLOCK_SCHUR_AMG_F32 || kind == VEM_PRECOND_BLOCK_REG_M;
+}
+inline bool is_block_reg(int kind) { return kind == VEM_PRECOND_BLOCK_REG || kind == VEM_PRECOND_BLOCK_REG_M; }
 
 int enqueue_precond(Ctx *c, int kind, const double *v, const double *scale, double *z, const int *gate,
                     int64_t *inner_its) {
@@ -938,6 +1208,7 @@ int enqueue_precond(Ctx *c, int kind, const double *v, const double *scale, doub
   if (kind == VEM_PRECOND_BLOCK_SCHUR_AMG_F32) return enqueue_block_schur_amg<float>(c, v, scale, z, gate);
   if (kind == VEM_PRECOND_BLOCK_SCHUR) return enqueue_block_schur(c, v, scale, z, gate);
   if (kind == VEM_PRECOND_BLOCK_REG) return enqueue_block_reg(c, v, scale, z, gate, inner_its);
+  if (kind == VEM_PRECOND_BLOCK_REG_M) return enqueue_block_reg_m(c, v, scale, z, gate, inner_its);
   // NONE: z = scale * v
   TimeScope ts(c, VEM_K_PRECOND_VEC);
   k_bs_init<<<grid_stream(c, c->n), NT, 0, c->stream>>>(c->n, 0, v, scale, nullptr, nullptr, 0.0, z, nullptr,
@@ -974,10 +1245,10 @@ int enqueue_arnoldi_step(Ctx *c, int kind, int j, int64_t *inner_its) {
     TimeScope ts(c, VEM_K_SPMV, bytes_spmv(c) + 8.0 * c->nu);
     if (f32)   // FGMRES: z_j is also stored (row by row, by the thread that owns the row)
       launch_plain(c, k_vc_spmv_z<float>, grid_for(c->n), NT, c->n, c->nu, sellA(c), Vj, &c->st->vscale[j],
-                                                                c->dMinv, c->amg[0].x_f, w, zj, gate_active(c));
+                                                                c->dMinv, c->amg.lv[0].x_f, w, zj, gate_active(c));
     else
       launch_plain(c, k_vc_spmv_z<double>, grid_for(c->n), NT, c->n, c->nu, sellA(c), Vj, &c->st->vscale[j],
-                                                                 c->dMinv, c->amg[0].x, w, nullptr, gate_active(c));
+                                                                 c->dMinv, c->amg.lv[0].x, w, nullptr, gate_active(c));
   } else {
     int rc = enqueue_precond(c, kind, Vj, &c->st->vscale[j], zj, gate_active(c), inner_its);
     c->sample_slot = -1;
@@ -988,7 +1259,7 @@ int enqueue_arnoldi_step(Ctx *c, int kind, int j, int64_t *inner_its) {
   const int nv = j + 1;
   const int gx = c->sm_count * 2;
   // reorth: 1 CGS2, 0 CGS1, -1 auto = CGS1 for GMRES, CGS2 for FGMRES/Block-Reg (reading R17)
-  const int npass = (c->opts.reorth == 1 || (c->opts.reorth < 0 && kind == VEM_PRECOND_BLOCK_REG)) ? 2 : 1;
+  const int npass = (c->opts.reorth == 1 || (c->opts.reorth < 0 && is_block_reg(kind))) ? 2 : 1;
   for (int pass = 1; pass <= npass; ++pass) {
     const int nout = nv + (pass == 1 ? 1 : 0);
     const int nchunk = (nout + VEM_DOT_CHUNK - 1) / VEM_DOT_CHUNK;
@@ -1053,6 +1324,8 @@ void destroy_graphs(Ctx *c) {
     }
   if (c->pcg_exec) cudaGraphExecDestroy(c->pcg_exec);
   c->pcg_exec = nullptr;
+  if (c->pcgm_exec) cudaGraphExecDestroy(c->pcgm_exec);
+  c->pcgm_exec = nullptr;
 }
 
 int ensure_work(Ctx *c, int kind) {
@@ -1094,9 +1367,11 @@ void from_internal(Ctx *c, const double *in, double *out_u, double *out_p) {
 int solve_impl(Ctx *c, const double *rhs, double tol, int maxit, int kind, double *out_u, double *out_p,
                vem_solve_report *rep) {
   vem_solve_report R{};
-  if (kind < 0 || kind > 4) return fail(c, VEM_ERR_PRECOND, "unsupported precond_kind %d", kind);
-  if (kind == VEM_PRECOND_BLOCK_REG && !c->has_reg)
+  if (kind < 0 || kind > 5) return fail(c, VEM_ERR_PRECOND, "unsupported precond_kind %d", kind);
+  if (is_block_reg(kind) && !c->has_reg)
     return fail(c, VEM_ERR_PRECOND, "Block-Reg needs eps > 0 at upload");
+  c->k_its_total = 0;
+  c->k_failed = false;
   if (!rhs || !out_u || !out_p || maxit < 0 || !(tol > 0)) return fail(c, VEM_ERR_INVALID, "invalid solve arguments");
   int rc = ensure_work(c, kind);
   if (rc) return rc;
@@ -1137,7 +1412,7 @@ int solve_impl(Ctx *c, const double *rhs, double tol, int maxit, int kind, doubl
     gs.active = (gs.its >= gs.maxit) ? 0 : 1;
     gs.conv_true = 0;
     CK(cudaMemcpyAsync(&c->st->g, &gs, sizeof(gs), cudaMemcpyHostToDevice, c->stream));
-    const bool graphs = c->opts.use_graphs && c->opts.timing != 1 && kind != VEM_PRECOND_BLOCK_REG;
+    const bool graphs = c->opts.use_graphs && c->opts.timing != 1 && !is_block_reg(kind);
     if (c->opts.timing == 2) {
       int rs = ensure_samples(c);
       if (rs) return rs;
@@ -1206,6 +1481,7 @@ int solve_impl(Ctx *c, const double *rhs, double tol, int maxit, int kind, doubl
   R.converged = bnorm == 0.0 ? 1 : h.conv_true;
   R.breakdown = h.breakdown;
   R.inner_iterations = inner;
+  R.k_iterations = c->k_its_total;
   R.rel_residual_true = bnorm > 0 ? h.true_res / bnorm : 0.0;
   R.rel_residual_est = bnorm > 0 ? h.est / bnorm : 0.0;
   R.setup_ms = c->setup_ms;
@@ -1841,25 +2117,16 @@ int amg_level_vectors(Ctx *c, AmgLevel &L) {
   return 0;
 }
 
-int build_amg(Ctx *c) {
-  c->amg.clear();
-  AmgLevel L0;
-  L0.n = c->np;
-  L0.nnz = c->nnzS;
-  L0.rp = c->s_rp;
-  L0.ci = c->s_ci;
-  L0.va = c->s_va;
-  L0.soff = c->s_soff;
-  L0.sci = c->s_sci;
-  L0.sva = c->s_sva;
-  L0.dinv = c->dSinv;
-  L0.lmax = c->lmax;
-  L0.owns_matrix = false;
-  c->amg.push_back(L0);
-  int r = amg_level_vectors(c, c->amg.back());
+// Hierarchy H on the level-0 matrix L0 (CSR + SELL + D^-1 + lmax set by the caller, not owned);
+// diag0 = its diagonal.  share_pool: the level-0 smoother vectors live in the L2-resident
+// Chebyshev pool (the users of the pool never overlap in time).
+int build_amg(Ctx *c, AmgHier &H, const AmgLevel &L0, double *diag0, bool share_pool) {
+  H.lv.clear();
+  H.lv.push_back(L0);
+  int r = amg_level_vectors(c, H.lv.back());
   if (r) return r;
-  {  // the fine-level smoother works in the L2-resident Chebyshev pool (kinds 1 and 3 never overlap)
-    AmgLevel &F = c->amg.back();
+  if (share_pool) {
+    AmgLevel &F = H.lv.back();
     dfree(c, F.sr);
     dfree(c, F.sd0);
     dfree(c, F.sd1);
@@ -1869,12 +2136,12 @@ int build_amg(Ctx *c) {
     F.sd1 = c->cd1;
     F.x = c->cx;
   }
-  double *diag = c->sdiag;
+  double *diag = diag0;
   while (true) {
-    AmgLevel &L = c->amg.back();
-    if (L.n <= AMG_COARSE_SIZE || (int)c->amg.size() >= c->amg_max_levels) break;
+    AmgLevel &L = H.lv.back();
+    if (L.n <= AMG_COARSE_SIZE || (int)H.lv.size() >= c->amg_max_levels) break;
     long nc = 0;
-    const size_t lev = c->amg.size() - 1;
+    const size_t lev = H.lv.size() - 1;
     r = amg_aggregate(c, L, diag, lev == 0 ? AMG_THETA : AMG_THETA_COARSE, nc);
     if (r) return r;
     if (nc > AMG_STAGNATION * L.n) {
@@ -1885,12 +2152,12 @@ int build_amg(Ctx *c) {
     L.nc = nc;
     AmgLevel C;
     if ((int)lev < AMG_SA_LEVELS) {
-      r = amg_sa_level(c, c->amg.back(), nc, C);
+      r = amg_sa_level(c, H.lv.back(), nc, C);
       if (r) return r;
     } else {
       r = amg_galerkin(c, L, nc, C);
       if (r) return r;
-      r = amg_members(c, c->amg.back());
+      r = amg_members(c, H.lv.back());
       if (r) return r;
     }
     // coarse diagonal, Gershgorin bound, SELL copy, vectors
@@ -1915,15 +2182,15 @@ int build_amg(Ctx *c) {
     }
     r = amg_level_vectors(c, C);
     if (r) return r;
-    c->amg.push_back(C);
+    H.lv.push_back(C);
     diag = cdiag;
   }
-  AmgLevel &Lc = c->amg.back();
-  c->amg_dense = Lc.n <= AMG_COARSE_SIZE;
-  if (c->amg_dense) {
+  AmgLevel &Lc = H.lv.back();
+  H.dense = Lc.n <= AMG_COARSE_SIZE;
+  if (H.dense) {
     double *D = nullptr;
     DA(D, (size_t)Lc.n * 2 * Lc.n);
-    DA(c->amg_cinv, (size_t)Lc.n * Lc.n);
+    DA(H.cinv, (size_t)Lc.n * Lc.n);
     k_amg_dense<<<grid_stream(c, Lc.n), NT, 0, c->stream>>>(Lc.n, Lc.rp, Lc.ci, Lc.va, D);
     auto tg = std::chrono::steady_clock::now();
     double *piv = nullptr, *col = nullptr;
@@ -1934,7 +2201,7 @@ int build_amg(Ctx *c) {
       k_amg_gj_pivot<<<(unsigned)((2 * n + NT - 1) / NT), NT, 0, c->stream>>>(n, k, D, piv, col, c->derr);
       k_amg_gj_update<<<dim3((unsigned)((n + 1 + NT - 1) / NT), (unsigned)n), NT, 0, c->stream>>>(n, k, D, piv, col);
     }
-    k_amg_gj_extract<<<grid_stream(c, n * n), NT, 0, c->stream>>>(n, D, c->amg_cinv);
+    k_amg_gj_extract<<<grid_stream(c, n * n), NT, 0, c->stream>>>(n, D, H.cinv);
     CKL();
     CK(cudaStreamSynchronize(c->stream));
     dfree(c, piv);
@@ -1955,8 +2222,8 @@ int build_amg(Ctx *c) {
 // warp kernels run instead) when the cluster cannot be launched or a rank's slice
 // does not fit in shared memory.
 int build_amg_cluster(Ctx *c) {
-  if (c->amg.empty() || c->amg_dense || !c->amg_cluster) return 0;
-  AmgLevel &L = c->amg.back();
+  if (c->amg.lv.empty() || c->amg.dense || !c->amg_cluster) return 0;
+  AmgLevel &L = c->amg.lv.back();
   if (!L.rp || !L.ci || L.n < VC_CLUSTER || L.n > 65535 || L.nnz >= (1L << 31)) return 0;
   if (c->amg_coarse_degree < 1 || c->amg_coarse_degree > VC_MAX_DEGREE) return 0;
   std::vector<int> rp(L.n + 1);
@@ -2028,8 +2295,8 @@ int build_amg_f32(Ctx *c) {
     k_d2f<<<grid_stream(c, n), NT, 0, c->stream>>>(n, in, *out);
     return 0;
   };
-  for (size_t l = 0; l < c->amg.size(); ++l) {
-    AmgLevel &L = c->amg[l];
+  for (size_t l = 0; l < c->amg.lv.size(); ++l) {
+    AmgLevel &L = c->amg.lv[l];
     int r;
     if ((r = cvt(L.sva, l == 0 ? c->nnzS_sell : L.nnz_sell, &L.sva_f))) return r;
     if ((r = cvt(L.va, L.nnz, &L.va_f))) return r;
@@ -2062,9 +2329,9 @@ int build_amg_f32(Ctx *c) {
     DA(L.sd0_f, L.n);
     DA(L.sd1_f, L.n);
   }
-  if (c->amg_dense) {
-    const long nc = c->amg.back().n;
-    int r = cvt(c->amg_cinv, nc * nc, &c->amg_cinv_f);
+  if (c->amg.dense) {
+    const long nc = c->amg.lv.back().n;
+    int r = cvt(c->amg.cinv, nc * nc, &c->amg.cinv_f);
     if (r) return r;
   }
   CKL();
@@ -2096,6 +2363,7 @@ int upload_impl(Ctx *c, const vem_csr *M, const vem_csr *B, const vem_csr *W, do
   c->amg_group = getenv("VEM_AMG_GROUP") ? atoi(getenv("VEM_AMG_GROUP")) : 8;
   c->amg_group_div = getenv("VEM_AMG_GROUP_DIV") ? atof(getenv("VEM_AMG_GROUP_DIV")) : 2.0;
   c->pdl = getenv("VEM_PDL") ? atoi(getenv("VEM_PDL")) : 1;
+  c->trace_k = getenv("VEM_TRACE_K") && atoi(getenv("VEM_TRACE_K")) != 0;
   auto phase = [&](const char *what) {
     if (!trace) return;
     cudaStreamSynchronize(c->stream);
@@ -2311,6 +2579,39 @@ int upload_impl(Ctx *c, const vem_csr *M, const vem_csr *B, const vem_csr *W, do
     DA(c->pq, c->np);
     DA(c->pb, c->np);
   }
+  if (c->has_reg) {   // matrix of the S_eps hierarchy (R23), in the caller's numbering (before the reordering)
+    if (c->nb == 1) {
+      c->se_n = c->np;
+      c->se_nnz = c->nnzS;
+      c->se_rp = c->s_rp;
+      c->se_ci = c->s_ci;
+      DA(c->se_va, c->nnzS);
+      CK(cudaMemcpyAsync(c->se_va, c->s_va, c->nnzS * sizeof(double), cudaMemcpyDeviceToDevice, c->stream));
+      k_shift_diag<<<grid_stream(c, c->np), NT, 0, c->stream>>>(c->np, c->s_rp, c->s_ci, c->se_va, c->wdiag, eps);
+      CKL();
+    } else {
+      const long ne = c->np / c->nb;
+      int *cnt = nullptr;
+      DA(cnt, ne + 1);
+      DA(c->se_rp, ne + 1);
+      CK(cudaMemsetAsync(cnt, 0, (ne + 1) * sizeof(int), c->stream));
+      k_mg_coarse_count<<<grid_stream(c, ne), NT, 0, c->stream>>>(ne, c->nb, c->s_rp, c->s_ci, cnt);
+      CKL();
+      int rr = scan_excl(c, cnt, c->se_rp, ne + 1);
+      if (rr) return rr;
+      int tot = 0;
+      CK(cudaMemcpyAsync(&tot, c->se_rp + ne, sizeof(int), cudaMemcpyDeviceToHost, c->stream));
+      CK(cudaStreamSynchronize(c->stream));
+      dfree(c, cnt);
+      c->se_n = ne;
+      c->se_nnz = tot;
+      DA(c->se_ci, tot);
+      DA(c->se_va, tot);
+      k_mg_coarse_fill<<<grid_stream(c, ne), NT, 0, c->stream>>>(ne, c->nb, c->s_rp, c->s_ci, c->s_va, c->wdiag, eps,
+                                                                 c->se_rp, c->se_ci, c->se_va);
+      CKL();
+    }
+  }
   {
     int rr = build_reorder(c);
     if (rr) return rr;
@@ -2324,12 +2625,53 @@ int upload_impl(Ctx *c, const vem_csr *M, const vem_csr *B, const vem_csr *W, do
   CK(cudaStreamSynchronize(c->stream));
   phase("block inverses, SELL");
   if (c->nb == 1) {   // S_D hierarchy for precond kinds 3 and 4 (k = 0)
-    int rr = build_amg(c);
+    AmgLevel L0;
+    L0.n = c->np;
+    L0.nnz = c->nnzS;
+    L0.rp = c->s_rp;
+    L0.ci = c->s_ci;
+    L0.va = c->s_va;
+    L0.soff = c->s_soff;
+    L0.sci = c->s_sci;
+    L0.sva = c->s_sva;
+    L0.dinv = c->dSinv;
+    L0.lmax = c->lmax;
+    L0.owns_matrix = false;
+    int rr = build_amg(c, c->amg, L0, c->sdiag, true);
     if (rr) return rr;
     rr = build_amg_f32(c);
     if (rr) return rr;
     rr = build_amg_cluster(c);
     if (rr) return rr;
+  }
+  if (c->has_reg) {   // S_eps hierarchy: the V-cycle preconditioner of Block-Reg's inner PCG (R23)
+    AmgLevel L0;
+    L0.n = c->se_n;
+    L0.nnz = c->se_nnz;
+    L0.rp = c->se_rp;
+    L0.ci = c->se_ci;
+    L0.va = c->se_va;
+    L0.owns_matrix = false;
+    DA(c->se_dinv, L0.n);
+    DA(c->se_diag, L0.n);
+    k_diag_inv<<<grid_stream(c, L0.n), NT, 0, c->stream>>>(L0.n, L0.rp, L0.ci, L0.va, 0, c->se_dinv, c->se_diag,
+                                                           c->derr);
+    k_gershgorin<<<grid_stream(c, L0.n), NT, 0, c->stream>>>(L0.n, L0.rp, L0.ci, L0.va, c->part, c->counter, c->st);
+    CKL();
+    L0.lmax = read_back(c, &c->st->lmax);
+    if (read_back(c, c->derr)) return fail(c, VEM_ERR_DIAG_S, "non-positive diagonal in S_D + eps W");
+    L0.dinv = c->se_dinv;
+    int rr = build_sell(c, L0.n, L0.rp, L0.ci, L0.va, &L0.soff, &L0.sci, &L0.sva, &L0.nnz_sell);
+    if (rr) return rr;
+    rr = build_amg(c, c->amge, L0, c->se_diag, c->nb == 1);
+    if (rr) return rr;
+    if (c->nb == 1) {
+      c->mg_r = c->amge.lv[0].b;
+      c->mg_z = c->amge.lv[0].x;
+    } else {
+      c->mg_r = c->pr;
+      c->mg_z = c->pz;
+    }
   }
   phase("AMG hierarchy");
   {
@@ -2499,6 +2841,11 @@ void vem_mixed_default_options(vem_opts *o) {
   o->reorth = -1;
   o->l2_persist = 1;
   o->reorder = 1;
+  o->inner_precond = 1;
+  o->k_maxit = 500;
+  o->k_rtol = 0.1;
+  o->k_inner_rtol = 1e-6;
+  o->mg_chunk = 2;
 }
 
 static int validate_opts(Ctx *c, const vem_opts *o) {
@@ -2508,6 +2855,9 @@ static int validate_opts(Ctx *c, const vem_opts *o) {
   if (!(o->inner_rtol > 0.0) || o->inner_maxit < 1) return fail(c, VEM_ERR_INVALID, "bad inner PCG options");
   if (o->reorth < -1 || o->reorth > 1) return fail(c, VEM_ERR_INVALID, "reorth must be -1, 0 or 1");
   if (o->reorder < 0 || o->reorder > 1) return fail(c, VEM_ERR_INVALID, "reorder must be 0 or 1");
+  if (o->inner_precond < 0 || o->inner_precond > 1) return fail(c, VEM_ERR_INVALID, "inner_precond must be 0 or 1");
+  if (o->k_maxit < 1 || !(o->k_rtol > 0.0) || !(o->k_inner_rtol > 0.0) || o->mg_chunk < 1)
+    return fail(c, VEM_ERR_INVALID, "bad kind-5 / MG-PCG options");
   return 0;
 }
 
@@ -2818,8 +3168,8 @@ int vem_mixed_schur_spmv(vem_ctx *h, const double *x, double *y) {
 int vem_mixed_precond_apply(vem_ctx *h, int32_t kind, const double *v, double *z, int64_t *inner_its) {
   if (!h || !v || !z) return VEM_ERR_INVALID;
   Ctx *c = h->impl;
-  if (kind < 0 || kind > 4) return fail(c, VEM_ERR_PRECOND, "unsupported precond_kind %d", kind);
-  if (kind == VEM_PRECOND_BLOCK_REG && !c->has_reg) return fail(c, VEM_ERR_PRECOND, "Block-Reg needs eps > 0");
+  if (kind < 0 || kind > 5) return fail(c, VEM_ERR_PRECOND, "unsupported precond_kind %d", kind);
+  if (is_block_reg(kind) && !c->has_reg) return fail(c, VEM_ERR_PRECOND, "Block-Reg needs eps > 0");
   int64_t its = 0;
   int r = enter(c);
   if (r) return r;
@@ -2882,9 +3232,9 @@ int vem_mixed_get_info(vem_ctx *h, vem_info *info) {
   info->sm_count = c->sm_count;
   info->device_bytes = c->device_bytes;
   info->l2_window_bytes = (int64_t)c->l2_window_bytes;
-  info->amg_levels = (int32_t)c->amg.size();
-  info->amg_coarsest = c->amg.empty() ? 0 : c->amg.back().n;
-  info->amg_coarse_cluster = c->amg.empty() ? 0 : (int32_t)c->amg.back().vc_ok;
+  info->amg_levels = (int32_t)c->amg.lv.size();
+  info->amg_coarsest = c->amg.lv.empty() ? 0 : c->amg.lv.back().n;
+  info->amg_coarse_cluster = c->amg.lv.empty() ? 0 : (int32_t)c->amg.lv.back().vc_ok;
   info->reordered = c->perm ? 1 : 0;
   info->nnz_A_stored = c->nnzA_sell;
   info->nnz_S_stored = c->nnzS_sell;
@@ -2916,9 +3266,18 @@ int vem_mixed_kernel_stats(vem_ctx *h, vem_kernel_stats *s, int32_t reset) {
 int vem_mixed_amg_level(vem_ctx *h, int32_t level, int64_t *n, int64_t *nnz) {
   if (!h || !n || !nnz) return VEM_ERR_INVALID;
   Ctx *c = h->impl;
-  if (level < 0 || level >= (int)c->amg.size()) return VEM_ERR_INVALID;
-  *n = c->amg[level].n;
-  *nnz = c->amg[level].nnz;
+  if (level < 0 || level >= (int)c->amg.lv.size()) return VEM_ERR_INVALID;
+  *n = c->amg.lv[level].n;
+  *nnz = c->amg.lv[level].nnz;
+  return VEM_OK;
+}
+
+int vem_mixed_inner_amg_level(vem_ctx *h, int32_t level, int64_t *n, int64_t *nnz) {
+  if (!h || !n || !nnz) return VEM_ERR_INVALID;
+  Ctx *c = h->impl;
+  if (level < 0 || level >= (int)c->amge.lv.size()) return VEM_ERR_INVALID;
+  *n = c->amge.lv[level].n;
+  *nnz = c->amge.lv[level].nnz;
   return VEM_OK;
 }
 

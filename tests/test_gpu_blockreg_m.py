@@ -1,0 +1,120 @@
+"""GPU-vs-oracle parity of the nested solves inside the Block-Reg preconditioners
+(C ABI, libvem_mixed.so): the MG-PCG inner solve on S_eps = S_D + eps W (DESIGN.md
+reading R23) and precond kind 5, the PCG on K = M + B^T (eps W)^-1 B (PAPER.md
+P:981-984, reading R24)."""
+import numpy as np
+import pytest
+import scipy.sparse as sp
+
+from oracle import solver as O
+from oracle.amg import AMG
+from vemgen import configs
+
+pytestmark = pytest.mark.gpu
+
+torch = pytest.importorskip("torch")
+if not torch.cuda.is_available():  # pragma: no cover
+    pytest.skip("needs a CUDA device", allow_module_level=True)
+
+import paper_1901_02330_b200 as pkg  # noqa: E402
+
+RNG = np.random.default_rng(515)
+_CACHE = {}
+
+
+def system(name):
+    if name not in _CACHE:
+        _CACHE[name] = configs.CONFIGS[name].build()
+    return _CACHE[name]
+
+
+def solver_for(s, **opts):
+    o = pkg.default_options(**opts) if opts else None
+    return pkg.VemMixed(s.M, s.B, eps=configs.eps_for(s), layout=s.layout, opts=o)
+
+
+def rel_inf(a, b):
+    return np.abs(a - b).max() / max(np.abs(b).max(), 1e-300)
+
+
+@pytest.mark.parametrize("name", ["C1", "C3s", "C2s", "C4s", "C5s"])
+def test_inner_hierarchy_equals_oracle(name):
+    """Integer work: the S_eps hierarchy (on the element-mean block when n_p_dof > 1) has
+    the oracle's rows and nonzeros on every level."""
+    s = system(name)
+    nb = s.layout.n_p_dof
+    SD = O.schur_diag(s.M, s.B)
+    Se = (SD + configs.eps_for(s) * sp.identity(SD.shape[0])).tocsr()
+    h = AMG(Se if nb == 1 else Se[0::nb, 0::nb].tocsr())
+    sv = solver_for(s)
+    got = sv.inner_amg_levels()
+    assert [(lv.A.shape[0], lv.A.nnz) for lv in h.levels] == got, (got,)
+    sv.close()
+
+
+@pytest.mark.parametrize("inner", [1, 0])
+@pytest.mark.parametrize("name", ["C1", "C3s", "C2s", "C4s", "C5s"])
+def test_block_reg_apply_parity_inner(name, inner):
+    """Kind-2 apply with the V-cycle (1) and the block-Jacobi (0) inner PCG: the same inner
+    step count (+-1) and the same z as the oracle's."""
+    s = system(name)
+    eps = configs.eps_for(s)
+    sv = solver_for(s, inner_precond=inner)
+    P = O.Preconditioner(O.PRECOND_BLOCK_REG, s.M, s.B, eps=eps, block=s.layout.n_p_dof, inner_precond=inner)
+    v = RNG.normal(size=s.n)
+    z, its = sv.precond_apply(pkg.PRECOND_BLOCK_REG, torch.from_numpy(v).cuda())
+    zo = P.apply(v)
+    nu = s.layout.n_u
+    print(f"{name} inner_precond={inner}: gpu {its} oracle {P.inner_iterations} inner steps")
+    assert abs(its - P.inner_iterations) <= 2
+    assert rel_inf(z.cpu().numpy()[:nu], zo[:nu]) <= 1e-8
+    assert rel_inf(z.cpu().numpy()[nu:], zo[nu:]) <= 1e-14
+    sv.close()
+
+
+@pytest.mark.parametrize("name", ["C5t", "C2s", "C3s"])
+def test_block_reg_m_apply_parity(name):
+    """Kind-5 apply with a tight PCG on K (k_rtol 1e-8, inner 1e-12): both sides reach
+    K^-1 v_u, so z_u agrees far below the tolerance; the K step counts agree."""
+    s = system(name)
+    eps = configs.eps_for(s)
+    sv = solver_for(s, k_rtol=1e-8, k_inner_rtol=1e-12, k_maxit=2000)
+    P = O.Preconditioner(O.PRECOND_BLOCK_REG_M, s.M, s.B, eps=eps, block=s.layout.n_p_dof, k_rtol=1e-8,
+                         k_inner_rtol=1e-12, k_maxit=2000)
+    v = RNG.normal(size=s.n)
+    z, its = sv.precond_apply(pkg.PRECOND_BLOCK_REG_M, torch.from_numpy(v).cuda())
+    zo = P.apply(v)
+    nu = s.layout.n_u
+    print(f"{name}: oracle K steps {P.k_iterations}, inner gpu {its} oracle {P.inner_iterations}")
+    assert not P.inner_failed
+    assert rel_inf(z.cpu().numpy()[:nu], zo[:nu]) <= 1e-6
+    assert rel_inf(z.cpu().numpy()[nu:], zo[nu:]) <= 1e-14
+    if nu <= 5000:   # and z_u is K^-1 v_u (dense solve)
+        K = (s.M + s.B.T @ s.B / eps).toarray()
+        assert rel_inf(z.cpu().numpy()[:nu], np.linalg.solve(K, v[:nu])) <= 1e-4
+    sv.close()
+
+
+@pytest.mark.parametrize("name", ["C5t", "C5s"])
+def test_block_reg_m_solve_parity(name):
+    """The C5-type meshes (pairs, anisotropic K with jumps) converge with kind 5 where the
+    diag(M) Block-Reg stagnates; u and p within 1e-8 of the oracle's solve, outer count
+    within +-2, true residual <= 1e-10 recomputed on the host."""
+    s = system(name)
+    cfg = configs.CONFIGS[name]
+    eps = configs.eps_for(s)
+    ref = O.solve(s.M, s.B, s.rhs, O.PRECOND_BLOCK_REG_M, 1e-10, cfg.restart, eps=eps, block=s.layout.n_p_dof)
+    assert ref.converged
+    sv = solver_for(s, restart=cfg.restart)
+    res = sv.solve(torch.from_numpy(s.rhs).cuda(), 1e-10, 10000, pkg.PRECOND_BLOCK_REG_M)
+    r = res.report
+    print(f"{name} kind 5: gpu {r['iterations']} outer / {r['k_iterations']} K / {r['inner_iterations']} inner; "
+          f"oracle {ref.iterations} / {ref.k_iterations} / {ref.inner_iterations}")
+    assert r["status"] == 0 and r["converged"] == 1, r
+    assert abs(r["iterations"] - ref.iterations) <= 2
+    nu = s.layout.n_u
+    assert rel_inf(res.u.cpu().numpy(), ref.x[:nu]) <= 1e-8
+    assert rel_inf(res.p.cpu().numpy(), ref.x[nu:]) <= 1e-8
+    x = np.concatenate([res.u.cpu().numpy(), res.p.cpu().numpy()])
+    assert np.linalg.norm(s.rhs - O.spmv_saddle(s.M, s.B, x)) <= 1e-10 * np.linalg.norm(s.rhs) * 1.0001
+    sv.close()

@@ -1,5 +1,6 @@
 """Solve every BASELINE config (both preconditioners where the config names
-them) on cuda:0 through the C ABI and print one JSON line per solve."""
+them) on cuda:0 through the C ABI and print one JSON line per solve.
+usage: run_configs.py C1,C2,C5:5,C4:1+2 [maxit]   (name[:kind+kind...]; C5 defaults to kind 5)"""
 import json
 import os
 import sys
@@ -15,7 +16,8 @@ from vemgen.configs import CONFIGS, eps_for  # noqa: E402
 
 names = sys.argv[1].split(",") if len(sys.argv) > 1 else ["C1", "C2", "C3", "C4", "C5"]
 maxit = int(sys.argv[2]) if len(sys.argv) > 2 else 5000
-for name in names:
+for spec in names:
+    name, _, ks = spec.partition(":")
     cfg = CONFIGS[name]
     t0 = time.time()
     s = cfg.build()
@@ -23,12 +25,16 @@ for name in names:
     sv = pkg.VemMixed(s.M, s.B, eps=eps_for(s), layout=s.layout, opts=pkg.default_options(restart=cfg.restart))
     rhs = torch.from_numpy(s.rhs).cuda()
     kinds = list(cfg.precs) + ([3] if s.layout.n_p_dof == 1 and 1 in cfg.precs else [])
+    if name.startswith("C5"):
+        kinds = [5]   # the M-aware Block-Reg (R24); kind 2 stagnates on C5
+    if ks:
+        kinds = [int(k) for k in ks.split("+")]
     for kind in kinds:
         r = sv.solve(rhs, cfg.rtol, maxit, kind)
         u, p = r.u.cpu().numpy(), r.p.cpu().numpy()
         cons = float(np.abs(s.B @ u - s.f).max() / np.abs(s.f).max())
         rep = {k: r.report[k] for k in ("status_name", "iterations", "restarts", "inner_iterations",
-                                        "rel_residual_true", "setup_ms", "solve_ms")}
+                                        "k_iterations", "rel_residual_true", "setup_ms", "solve_ms")}
         print(json.dumps({"config": name, "precond": kind, "n": s.n, "assembly_s": round(t_asm, 1),
                           "conservation_rel": cons, **rep, "info": sv.info()}), flush=True)
     sv.close()
