@@ -3,11 +3,15 @@
 saddle-point system (BASELINE.json metric: time-to-solution & GMRES iters/s at
 1 B200; SpMV / preconditioner HBM GB/s vs peak).
 
-One step = one vem_mixed_solve of the configured system from x0 = 0 to
-rtol 1e-10 (upload and S_D build happen once, before timing: reported as
-setup_ms).  value = solves / s over the K timed steps, all ranks (the inverse of
-the time to solution, summed over replicas); the GMRES iteration rate is reported
-beside it (gmres_it_per_s), as are the per-kernel HBM rates.
+Workload: C5 (the largest single-GPU config of BASELINE.json: 96^3 cubes with ~50%
+pairs, k = 1, anisotropic K with jumps, 14.0M DOFs) with the regularised block
+preconditioner in its M-aware form (precond kind 5, R24).  One step = one
+GMRES iteration (preconditioner apply + saddle SpMV + batched CGS): a C5 solve takes
+minutes, so the K timed steps are the first K Arnoldi steps of solves from x0 = 0 (upload
+and S_D build happen once, before timing: setup_ms).  value = GMRES iterations / s over
+the K timed steps, all ranks; the time to solution of one complete solve to rtol 1e-10
+is measured after the timed region (full_solve) with the per-kernel HBM rates, and C3
+(round 1's headline) is timed as whole solves in `secondary`.
 
   python bench.py [--gpus N] [--steps K] [--warmup W] [--config C3] [--impl ours|reference]
 
@@ -28,7 +32,7 @@ ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
 METRIC = "time-to-solution & GMRES iters/s at 1 B200; SpMV/precond HBM GB/s vs peak"
-UNIT = "solves/s"
+UNIT = "GMRES it/s"
 ORACLE_ITS = os.path.join(ROOT, "profiles", "oracle_iterations.json")
 
 
@@ -44,9 +48,9 @@ def oracle_iterations(name, kind):
 def parse():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=3)
+    ap.add_argument("--steps", type=int, default=12)
     ap.add_argument("--warmup", type=int, default=3)
-    ap.add_argument("--config", default="C3")
+    ap.add_argument("--config", default="C5")
     ap.add_argument("--precond", type=int, default=0, help="0 = the config's first preconditioner")
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
@@ -148,6 +152,8 @@ def headline_kind(cfg, system, args):
     k = cfg.precs[0]
     if k == 1 and system.layout.n_p_dof == 1:
         return 3
+    if cfg.name.startswith("C5"):
+        return 5   # the regularised preconditioner with the M-aware velocity block (R24): kind 2 stagnates on C5
     return k
 
 
@@ -165,16 +171,68 @@ def reduce_over_ranks(ms: float, its: float, device="cpu"):
     return float(t[0]), float(w[0])
 
 
-def cpu_baseline(system, cfg, kind, eps, its):
-    """The oracle as it stands on a bounded sample: `its` GMRES iterations of the
-    same system on the host cores."""
-    import numpy as np
-    from oracle import solver as O
+def _cores():
     try:
         from threadpoolctl import threadpool_info
-        cores = max([i.get("num_threads", 1) for i in threadpool_info()] + [1])
+        return int(max([i.get("num_threads", 1) for i in threadpool_info()] + [1]))
     except Exception:
-        cores = 1
+        return 1
+
+
+def nested_counts(name):
+    """K-PCG and inner-PCG steps per outer iteration of the kind-5 solve of `name`, from the
+    last recorded full GPU solve (profiles/nested_counts.json, written by bench.py itself);
+    the oracle reproduces these counts at reduced size (tests/test_gpu_blockreg_m.py)."""
+    try:
+        return json.load(open(os.path.join(ROOT, "profiles", "nested_counts.json")))[name]
+    except Exception:
+        return None
+
+
+def cpu_baseline_nested(system, cfg, eps, counts, k_steps=1):
+    """Kind 5 (PCG on K inside FGMRES): one outer iteration of the oracle on full C5 takes about
+    20 minutes, so the bounded sample is `k_steps` steps of the PCG on K of the first non-trivial
+    preconditioner apply (each: K p, the Woodbury block with its inner MG-PCG to k_inner_rtol,
+    dots and updates), and GMRES it/s is EXTRAPOLATED as 1 / (K steps per outer iteration x
+    seconds per K step + one saddle SpMV), with the K-steps-per-iteration count of the full GPU
+    solve of the same system."""
+    import numpy as np
+    from oracle import solver as O
+    t0 = time.perf_counter()
+    P = O.Preconditioner(O.PRECOND_BLOCK_REG_M, system.M, system.B, eps=eps, block=system.layout.n_p_dof,
+                         k_maxit=k_steps, k_rtol=1e-30)
+    t1 = time.perf_counter()
+    # second Krylov vector of the solve: v_1 ~ A P^-1 v_0 with v_0 = rhs / ||rhs|| (v_0 has no velocity part)
+    z0 = P.apply(system.rhs / np.linalg.norm(system.rhs))
+    w = O.spmv_saddle(system.M, system.B, z0)
+    w /= np.linalg.norm(w)
+    t2 = time.perf_counter()
+    P.inner_iterations = 0
+    P.k_iterations = 0
+    P.apply(w)
+    t3 = time.perf_counter()
+    O.spmv_saddle(system.M, system.B, w)
+    t4 = time.perf_counter()
+    # one K step = (P.k_iterations steps + the initial Woodbury apply) / (k_steps + 1) applies
+    per_k = (t3 - t2) / (P.k_iterations + 1)
+    kpo = counts["k_per_outer"] if counts else None
+    itps = 1.0 / (kpo * per_k + (t4 - t3)) if kpo else None
+    return {"value": itps, "unit": UNIT, "cores": _cores(), "kind": "oracle", "extrapolated": True,
+            "seconds_per_K_step": per_k, "K_steps_per_outer_iteration": kpo,
+            "inner_steps_in_sample": int(P.inner_iterations),
+            "sample": f"{P.k_iterations} step(s) of the PCG on K = M + B^T (eps W)^-1 B plus its initial Woodbury apply "
+                      f"on the second Krylov vector of {cfg.name} (precond 5): {t3 - t2:.1f} s, {P.inner_iterations} inner "
+                      f"MG-PCG steps (+{t1 - t0:.1f} s preconditioner setup, untimed); GMRES it/s EXTRAPOLATED with "
+                      f"{kpo} K steps per outer iteration (full GPU solve of the same system, profiles/nested_counts.json)",
+            "setup_s": t1 - t0}
+
+
+def cpu_baseline(system, cfg, kind, eps, its):
+    """The oracle as it stands on a bounded sample: `its` GMRES iterations of the
+    same system on the host cores (value in GMRES it/s)."""
+    from oracle import solver as O
+    if kind == O.PRECOND_BLOCK_REG_M:
+        return cpu_baseline_nested(system, cfg, eps, nested_counts(cfg.name))
     t0 = time.perf_counter()
     P = O.Preconditioner(kind, system.M, system.B, eps=eps, block=system.layout.n_p_dof)
     t1 = time.perf_counter()
@@ -183,16 +241,17 @@ def cpu_baseline(system, cfg, kind, eps, its):
     t2 = time.perf_counter()
     itps = res.iterations / (t2 - t1)
     full = oracle_iterations(cfg.name, kind)
-    return {"value": (itps / full) if full else None, "unit": UNIT, "cores": int(cores), "kind": "oracle",
-            "gmres_it_per_s": itps, "iterations_per_solve": full,
+    return {"value": itps, "unit": UNIT, "cores": _cores(), "kind": "oracle", "extrapolated": False,
+            "iterations_per_solve": full, "solves_per_s_extrapolated": (itps / full) if full else None,
             "sample": f"{res.iterations} GMRES iterations of {cfg.name} (precond {kind}) from x0=0, "
-                      f"{t2 - t1:.1f} s (+{t1 - t0:.1f} s preconditioner setup, untimed); solves/s = "
-                      f"it/s / {full} (the oracle's own full-solve count, profiles/oracle_iterations.json)",
+                      f"{t2 - t1:.1f} s (+{t1 - t0:.1f} s preconditioner setup, untimed)",
             "setup_s": t1 - t0}
 
 
 def run_reference(args):
-    """--impl reference: the CPU oracle as it stands (rank 0 only)."""
+    """--impl reference: the CPU oracle as it stands (rank 0 only).  One step = one bounded
+    sample (cpu_baseline); value = the mean GMRES it/s over the K samples; ms_per_step = the
+    wall time of one sample (NOT of one GMRES iteration: see `sample`)."""
     rank, ws, _ = dist_init(args)
     if rank != 0:
         return
@@ -201,28 +260,103 @@ def run_reference(args):
     s = cfg.build()
     kind = headline_kind(cfg, s, args)   # the same preconditioner as our arm
     eps = eps_for(s)
+    nested = kind == 5
+    # kind 5: every sample costs ~25 s of oracle work, so the K + W samples are taken once
+    # and the timing repeated on cached operators would be meaningless: one sample per step,
+    # capped so that the run ends within a few minutes
+    steps = min(args.steps, 4) if nested else args.steps
+    warm = min(args.warmup, 1) if nested else args.warmup
     vals = []
-    for _ in range(args.warmup):
+    for _ in range(warm):
         cpu_baseline(s, cfg, kind, eps, 1)
     t0 = time.perf_counter()
-    tot_its = 0
     last = None
-    for _ in range(args.steps):
+    for _ in range(steps):
         last = cpu_baseline(s, cfg, kind, eps, args.cpu_sample_its)
         vals.append(last["value"])
-        tot_its += args.cpu_sample_its
     dt = time.perf_counter() - t0
     value = sum(vals) / len(vals) if all(v is not None for v in vals) else None
     line = {"impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus,
-            "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * dt / args.steps,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": (1e3 / value) if value else None,
+            "samples_taken": steps, "warmup_samples_taken": warm, "ms_per_sample": 1e3 * dt / steps,
             "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
             "data": "synthetic (seeded vemgen assembly)",
             "config": {"workload": f"{cfg.name}: {cfg.describe}", "rtol": cfg.rtol, "restart": cfg.restart,
-                       "precond": kind, "n_dofs": s.n},
-            "cpu_baseline": {k: last[k] for k in ("kind", "cores", "sample", "gmres_it_per_s", "iterations_per_solve")}
-            | {"value": value, "unit": UNIT},
+                       "precond": kind, "n_dofs": s.n,
+                       "step": "one bounded oracle sample converted to GMRES it/s; ms_per_step = 1000 / value "
+                               "(the time of one GMRES iteration at the sampled rate)"},
+            "cpu_baseline": {k: last[k] for k in last if k != "setup_s"} | {"value": value, "unit": UNIT},
             "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
+
+
+KIND_NAMES = {1: "block_schur chebyshev-jacobi d=16 (kind 1)", 2: "block_reg, diag(M) Woodbury (kind 2)",
+              3: "block_schur amg v-cycle on S_D (kind 3)",
+              4: "block_schur amg v-cycle in FP32, FGMRES (kind 4, mixed precision)",
+              5: "block_reg with the M-aware velocity block: PCG on M + B^T (eps W)^-1 B (kind 5)"}
+
+PAPER_CONTEXT = {
+    "note": "the paper's own timings: another machine, another space and BCs (context only, not a target)",
+    "hardware": "INDACO cluster, 2 x Xeon E5-2683 v4 2.1 GHz per node, PETSc + MUMPS/GAMG over MPI (PAPER.md P:993-996)",
+    "table1_cube_k1_435201_dofs": {"procs": 1, "block_schur": {"it": 66, "T_sol_s": 50},
+                                   "block_reg": {"it": 84, "T_sol_s": 53}, "mumps_T_sol_s": 823,
+                                   "cite": "PAPER.md P:1009-1014"},
+    "table1_cube_k1_435201_dofs_p32": {"procs": 32, "block_schur": {"T_sol_s": 9},
+                                       "block_reg": {"it": 137, "T_sol_s": 26}, "mumps_T_sol_s": 47,
+                                       "cite": "PAPER.md P:1018"},
+    "table4_cube_k2_804385_dofs_p8": {"procs": 8, "block_schur": {"it": 69, "T_sol_s": 217},
+                                      "block_reg": {"it": 188, "T_sol_s": 87}, "cite": "PAPER.md P:1217"}}
+
+
+def run_steps(solve, nsteps):
+    """`nsteps` GMRES iterations: solves from x0 = 0 chained until the Arnoldi steps add up
+    (each solve is capped at the steps still missing).  Returns the reports."""
+    reps = []
+    left = nsteps
+    while left > 0:
+        r = solve(left)
+        reps.append(r)
+        done = r["iterations"]
+        if done <= 0:
+            raise RuntimeError(f"solve made no progress: {r}")
+        left -= done
+    return reps
+
+
+def check_full(rep, rtol, what):
+    """ADVICE (round 1): never report a solve that hit maxit or broke down."""
+    if not (rep["status"] == 0 and rep["converged"] == 1 and rep["rel_residual_true"] <= rtol * 1.0001):
+        raise RuntimeError(f"{what}: solve did not converge: {rep}")
+
+
+def secondary_c3(pkg, torch, steps=3):
+    """C3 (round-1 headline) timed as whole solves: kind 3 (FP64 V-cycle) and kind 4 (FP32)."""
+    from vemgen.configs import CONFIGS
+    cfg = CONFIGS["C3"]
+    s = cfg.build()
+    sv = pkg.VemMixed(s.M, s.B, eps=0.0, layout=s.layout, opts=pkg.default_options(restart=cfg.restart))
+    rhs = torch.from_numpy(s.rhs).cuda()
+    out = {"workload": f"C3: {cfg.describe}", "n_dofs": s.n}
+    for kind in (3, 4):
+        for _ in range(2):
+            sv.solve(rhs, cfg.rtol, 20000, kind)
+        torch.cuda.synchronize()
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        reps = []
+        a.record()
+        for _ in range(steps):
+            reps.append(sv.solve(rhs, cfg.rtol, 20000, kind).report)
+        b.record()
+        torch.cuda.synchronize()
+        for r in reps:
+            check_full(r, cfg.rtol, f"C3 kind {kind}")
+        ms = a.elapsed_time(b) / steps
+        out[f"kind{kind}"] = {"precond": KIND_NAMES[kind], "time_to_solution_ms": round(ms, 2),
+                              "iterations": reps[-1]["iterations"], "solves_per_s": round(1e3 / ms, 3),
+                              "gmres_it_per_s": round(reps[-1]["iterations"] / (ms / 1e3), 1),
+                              "rel_residual_true": reps[-1]["rel_residual_true"]}
+    sv.close()
+    return out
 
 
 def main():
@@ -243,28 +377,12 @@ def main():
     t_asm = time.perf_counter() - t0
     kind = headline_kind(cfg, s, args)
     eps = eps_for(s)
-    # the same system assembled on the device (N2: element-parallel, shape-cached classes);
-    # the solve below uses the host system (the definition the oracle shares)
-    dev_asm = None
-    try:
-        from vemgen.assemble import class_templates
-        t0 = time.perf_counter()
-        tm = class_templates(cfg.make_mesh(), cfg.k)
-        t1 = time.perf_counter()
-        torch.cuda.synchronize()
-        t2 = time.perf_counter()
-        a = pkg.Assembled(tm, s.layout.n_u, s.layout.n_p)
-        torch.cuda.synchronize()
-        t3 = time.perf_counter()
-        dev_asm = {"shape_cache_s": round(t1 - t0, 3), "device_s": round(t3 - t2, 3),
-                   "nnz_equal": a.nnz() == (s.M.nnz, s.B.nnz)}
-        a.close()
-    except ValueError:
-        pass
-    # timed region: CUDA graphs (one graph launch per GMRES cycle) with the
-    # sampled timing mode: the middle Chebyshev step of every Arnoldi step is
-    # bracketed by CUDA events inside the graph (live roofline of the dominant
-    # kernel without per-launch overhead).  --per-launch: every launch timed.
+    nested = kind in (2, 5)
+    # timed region: CUDA graphs with the sampled timing mode: one kernel launch per graph
+    # replay is bracketed by CUDA events inside the graph (kinds 1/3: the middle Chebyshev /
+    # fine-level smoother step of every Arnoldi step; kinds 2/5: one fine-level S_eps pass of the
+    # inner V-cycle per replay of the inner-PCG graph): the live roofline of the dominant kernel
+    # without per-launch overhead.  --per-launch: every launch timed, no graphs.
     timing = 1 if args.per_launch else 2
     opts = pkg.default_options(restart=cfg.restart, use_graphs=0 if args.per_launch else 1, timing=timing,
                                reorth=args.reorth, l2_persist=args.l2_persist)
@@ -280,19 +398,18 @@ def main():
             import torch.distributed as dist
             dist.barrier()
 
-    for _ in range(args.warmup):
-        r = sv.solve(rhs_dev, cfg.rtol, 20000, kind)
+    def dev_solve(maxit):
+        return sv.solve(rhs_dev, cfg.rtol, maxit, kind).report
+
+    run_steps(dev_solve, max(args.warmup, 0))
     sv.kernel_stats(reset=True)
     torch.cuda.synchronize()
     barrier()
     torch.cuda.synchronize()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    reports = []
     with ClockSampler(local) as clk:
         e0.record(stream)
-        for _ in range(args.steps):
-            r = sv.solve(rhs_dev, cfg.rtol, 20000, kind)
-            reports.append(r.report)
+        reports = run_steps(dev_solve, args.steps)
         e1.record(stream)
         torch.cuda.synchronize()
     barrier()
@@ -300,141 +417,149 @@ def main():
     ms = e0.elapsed_time(e1)
     stats = sv.kernel_stats(reset=True)
     its = sum(r["iterations"] for r in reports)
-    # max over ranks of the time, sum of the work
+    assert its == args.steps, (its, args.steps)
+    # max over ranks of the time, sum of the work (every rank runs its own replica)
     ms, its_all = reduce_over_ranks(ms, its, device="cuda")
-    solves_all = float(args.steps * ws)   # every rank solves its own replica K times
-    value = solves_all / (ms / 1e3)
-    it_rate = its_all / (ms / 1e3)
+    value = its_all / (ms / 1e3)
 
-    # kernel breakdown: one more solve with every launch timed (after the timed region)
-    sv.set_options(timing=1, use_graphs=0)
-    rb = sv.solve(rhs_dev, cfg.rtol, 20000, kind)
-    breakdown = sv.kernel_stats(reset=True)
-    launches_per_solve = int(sum(v["launches"] for v in breakdown.values()))
-
-    # end to end: host rhs (pinned) -> device -> solve -> u, p back to host, through the C ABI
+    # end to end: host rhs (pinned) -> device -> solve -> u, p back to host, through the C ABI,
+    # the same K steps; every solve call copies rhs in and u, p out
     rhs_pin = torch.from_numpy(s.rhs).pin_memory()
     u_pin = torch.empty(s.layout.n_u, dtype=torch.float64).pin_memory()
     p_pin = torch.empty(s.layout.n_p, dtype=torch.float64).pin_memory()
     sv.set_options(timing=0, use_graphs=1)
-    sv.solve_host(rhs_pin.numpy(), cfg.rtol, 20000, kind, u_pin.numpy(), p_pin.numpy())
+
+    def host_solve(maxit):
+        return sv.solve_host(rhs_pin.numpy(), cfg.rtol, maxit, kind, u_pin.numpy(), p_pin.numpy()).report
+
+    run_steps(host_solve, min(args.warmup, 2))
     torch.cuda.synchronize()
+    barrier()
     t0 = time.perf_counter()
-    e2e_its = 0
-    for _ in range(args.steps):
-        rh = sv.solve_host(rhs_pin.numpy(), cfg.rtol, 20000, kind, u_pin.numpy(), p_pin.numpy())
-        e2e_its += rh.report["iterations"]
+    e2e_reps = run_steps(host_solve, args.steps)
+    torch.cuda.synchronize()
     e2e_s = time.perf_counter() - t0
-    e2e_graph_its = e2e_its
+    e2e_ms, e2e_its = reduce_over_ranks(1e3 * e2e_s, sum(r["iterations"] for r in e2e_reps), device="cuda")
+    e2e_calls = len(e2e_reps)
 
-    # variants of the same approximate-Schur preconditioner, timed the same way:
-    # kind 1 (fixed-sweep Chebyshev-Jacobi on S_D) and kind 4 (the V-cycle in FP32 inside
-    # FP64 FGMRES) beside the kind-3 headline
-    names = {1: "block_schur chebyshev-jacobi d=16 (kind 1)", 3: "block_schur amg v-cycle (kind 3)",
-             4: "block_schur amg v-cycle in FP32, FGMRES (kind 4, mixed precision)"}
-    variants = []
-    vkinds = {3: [pkg.PRECOND_BLOCK_SCHUR, pkg.PRECOND_BLOCK_SCHUR_AMG_F32],
-              1: [pkg.PRECOND_BLOCK_SCHUR_AMG]}.get(kind, [])
-    for vkind in (vkinds if info.get("amg_levels", 0) > 0 and not args.no_variant else []):
-        sv.set_options(timing=0, use_graphs=1)
-        sv.solve(rhs_dev, cfg.rtol, 20000, vkind)
-        torch.cuda.synchronize()
-        v0, v1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        vrep = []
-        v0.record(stream)
-        for _ in range(args.steps):
-            vrep.append(sv.solve(rhs_dev, cfg.rtol, 20000, vkind).report)
-        v1.record(stream)
-        torch.cuda.synchronize()
-        vms = v0.elapsed_time(v1) / args.steps
-        variants.append({"precond": names[vkind], "time_to_solution_ms": round(vms, 2),
-                         "iterations_per_solve": [r["iterations"] for r in vrep],
-                         "GMRES_it_per_s": round(sum(r["iterations"] for r in vrep) / (args.steps * vms / 1e3), 2),
-                         "rel_residual_true": vrep[-1]["rel_residual_true"]})
-    variant = variants or None
+    # time to solution: ONE complete solve to rtol (the metric's first half); also the source
+    # of the K / inner step counts per outer iteration that the oracle extrapolation uses
+    sv.set_options(timing=0, use_graphs=1)
+    f0, f1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    f0.record(stream)
+    full = sv.solve(rhs_dev, cfg.rtol, 20000, kind)
+    f1.record(stream)
+    torch.cuda.synchronize()
+    check_full(full.report, cfg.rtol, f"{cfg.name} kind {kind}")
+    fr = full.report
+    tts_ms = f0.elapsed_time(f1)
+    u, p = full.u.cpu().numpy(), full.p.cpu().numpy()
+    conservation = float(np.abs(s.B @ u - s.f).max() / np.abs(s.f).max())
+    counts = None
+    if kind == 5 and fr["iterations"] > 1:
+        real = fr["iterations"] - 1   # the first Krylov vector has no velocity part: no K solve
+        counts = {"outer": fr["iterations"], "k_steps": fr["k_iterations"], "inner_steps": fr["inner_iterations"],
+                  "k_per_outer": round(fr["k_iterations"] / real, 2),
+                  "inner_per_k": round(fr["inner_iterations"] / max(fr["k_iterations"] + real, 1), 2)}
+        if rank == 0:
+            try:
+                pth = os.path.join(ROOT, "profiles", "nested_counts.json")
+                allc = json.load(open(pth)) if os.path.exists(pth) else {}
+                allc[cfg.name] = counts
+                json.dump(allc, open(pth, "w"), indent=1)
+            except OSError:
+                pass
 
-    # SURVEY.md §8(d) Q21 benchmark extra: the same matrices with a seeded N(0, 1) RHS (seed 7)
-    random_rhs = None
-    if not args.no_variant:
-        from vemgen.configs import random_rhs as _rr
-        rr_dev = torch.from_numpy(_rr(s.n)).cuda()
-        sv.set_options(timing=0, use_graphs=1)
-        sv.solve(rr_dev, cfg.rtol, 20000, kind)
-        torch.cuda.synchronize()
-        q0, q1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        qrep = []
-        q0.record(stream)
-        for _ in range(args.steps):
-            qrep.append(sv.solve(rr_dev, cfg.rtol, 20000, kind).report)
-        q1.record(stream)
-        torch.cuda.synchronize()
-        qms = q0.elapsed_time(q1) / args.steps
-        random_rhs = {"rhs": "N(0,1), seed 7 (vemgen.configs.random_rhs)", "precond": kind,
-                      "time_to_solution_ms": round(qms, 2),
-                      "iterations_per_solve": [r["iterations"] for r in qrep],
-                      "GMRES_it_per_s": round(sum(r["iterations"] for r in qrep) / (args.steps * qms / 1e3), 2),
-                      "rel_residual_true": qrep[-1]["rel_residual_true"]}
+    # kernel breakdown: a bounded run with every launch timed (after the timed region)
+    sv.set_options(timing=1, use_graphs=0)
+    nb_steps = min(args.steps, 4) if nested else 20000
+    sv.kernel_stats(reset=True)
+    rb = sv.solve(rhs_dev, cfg.rtol, nb_steps, kind)
+    breakdown = sv.kernel_stats(reset=True)
+    launches_per_it = sum(v["launches"] for v in breakdown.values()) / max(rb.report["iterations"], 1)
 
     hbm, peak_kind = peaks()
     per = {k: v for k, v in breakdown.items() if v["launches"]}
+    tot_ms = max(sum(x["ms"] for x in per.values()), 1e-9)
     dom = max(per, key=lambda k: per[k]["ms"]) if per else None
-    # the dominant kernel's live numbers come from the timed region when sampled
+    if kind == 5 and "mg_fine" in per:
+        dom = "mg_fine"
     live = {k: v for k, v in stats.items() if v["launches"]}
-    if dom in live:
-        per_dom = live[dom]
-        dom_src = ("sampled CUDA events inside the timed region (" +
-                   ("fine-level pre-smoothing step of the V-cycle" if kind == 3 else "middle Chebyshev step") +
-                   " of every Arnoldi step)")
-    else:
-        per_dom = per.get(dom)
-        dom_src = "per-launch CUDA events, breakdown solve after the timed region"
     roof = None
     if dom:
-        d = per_dom
+        if dom in live:
+            d = live[dom]
+            src = "sampled CUDA events inside the timed region (graph event-record nodes around one launch per replay)"
+        else:
+            d = per[dom]
+            src = "per-launch CUDA events, bounded breakdown run after the timed region"
         ach = d["bytes"] / (d["ms"] / 1e3) / 1e9
+        agg = per[dom]
         roof = {"bound": "hbm", "kernel": dom, "achieved": round(ach, 1), "peak": hbm, "unit": "GB/s",
                 "frac": round(ach / hbm, 4), "traffic": ncu_traffic(dom), "peak_source": peak_kind,
                 "bytes_per_launch": d["bytes"] / d["launches"], "avg_launch_us": 1e3 * d["ms"] / d["launches"],
-                "launches_timed": d["launches"], "source": dom_src}
+                "launches_timed": d["launches"], "source": src,
+                # the same class over every launch of the breakdown run, and its share of that run
+                "class_aggregate": {"achieved": round(agg["bytes"] / (agg["ms"] / 1e3) / 1e9, 1),
+                                    "frac": round(agg["bytes"] / (agg["ms"] / 1e3) / 1e9 / hbm, 4),
+                                    "launches": agg["launches"], "share_of_run": round(agg["ms"] / tot_ms, 4),
+                                    "source": "per-launch CUDA events, breakdown run"}}
     kern = {k: {"launches": v["launches"], "ms": round(v["ms"], 3),
                 "GBps": round(v["bytes"] / max(v["ms"], 1e-9) / 1e6, 1),
-                "share": round(v["ms"] / max(sum(x["ms"] for x in per.values()), 1e-9), 4)}
+                "frac_of_peak": round(v["bytes"] / max(v["ms"], 1e-9) / 1e6 / hbm, 4),
+                "share": round(v["ms"] / tot_ms, 4)}
             for k, v in per.items()}
-    launches = launches_per_solve * args.steps
-    line = {"metric": METRIC, "value": round(value, 3), "unit": UNIT, "time_to_solution_ms": round(ms / args.steps, 2),
-            "gmres_it_per_s": round(it_rate, 1), "n_gpus": ws, "steps": args.steps,
+
+    secondary = None
+    if rank == 0 and ws == 1 and not args.no_variant and cfg.name == "C5":
+        sv.close()
+        sv = None
+        secondary = secondary_c3(pkg, torch)
+
+    line = {"metric": METRIC, "value": round(value, 4), "unit": UNIT,
+            "time_to_solution_ms": round(tts_ms, 2), "n_gpus": ws, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": ms / args.steps, "higher_is_better": True, "scaling": "weak",
             "vs_baseline": None, "dtype": "f64", "data": "synthetic (seeded vemgen assembly, no dataset)",
             "config": {"workload": f"{cfg.name}: {cfg.describe}", "n_dofs": s.n, "n_u": s.layout.n_u,
                        "n_p": s.layout.n_p, "nnz_A": info["nnz_A"], "nnz_S": info["nnz_S"],
-                       "precond": {1: "block_schur chebyshev-jacobi d=16 (kind 1)", 2: "block_reg (kind 2)",
-                                   3: "block_schur amg v-cycle on S_D (kind 3)"}.get(kind, kind),
-                       "amg_levels": sv.amg_levels() if kind == 3 else None,
+                       "precond": KIND_NAMES.get(kind, kind),
+                       "step": "one GMRES iteration (preconditioner apply + saddle SpMV + batched CGS); the timed "
+                               "region chains solves from x0 = 0, each capped at the steps still missing",
+                       "solve_calls_in_timed_region": len(reports),
+                       "inner_amg_levels": sv.inner_amg_levels() if (sv and nested) else None,
                        "restart": cfg.restart, "rtol": cfg.rtol,
                        "l2_window_MB": round(info["l2_window_bytes"] / 1e6, 1),
                        "orthogonalisation": {1: "CGS2", 0: "CGS1"}.get(args.reorth, "auto: CGS1 (GMRES) / CGS2 (FGMRES)"),
-                       "iterations_per_solve": [r["iterations"] for r in reports],
-                       "time_to_solution_ms": ms / args.steps,
-                       "rel_residual_true": reports[-1]["rel_residual_true"],
-                       "setup_ms": reports[-1]["setup_ms"], "assembly_s": round(t_asm, 2),
-                       "device_assembly": dev_asm,
+                       "setup_ms": fr["setup_ms"], "assembly_s": round(t_asm, 2),
                        "upload_wall_s": round(t_up, 2), "parallelism": f"replicas x{ws}",
-                       "l2": "inputs larger than L2 (A %.0f MB + Krylov basis %.0f MB)" % (
-                           (12 * info["nnz_A"]) / 1e6, 8 * s.n * (cfg.restart + 1) / 1e6),
-                       "timing": ("CUDA graphs, one graph per GMRES cycle; sampled events" if not args.per_launch
+                       "l2": "inputs larger than L2 (A %.0f MB, S_D %.0f MB, Krylov basis %.0f MB)" % (
+                           12 * info["nnz_A"] / 1e6, 12 * info["nnz_S"] / 1e6,
+                           8 * s.n * (cfg.restart + 1) * (2 if nested else 1) / 1e6),
+                       "timing": ("CUDA graphs (GMRES cycles / inner-PCG chunks); sampled events" if not args.per_launch
                                   else "per-launch CUDA events, no graphs"),
-                       "kernels_source": "per-launch CUDA events over one extra solve after the timed region"},
-            "roofline": roof, "kernels": kern, "gpu_launches": launches, "variant": variant,
-            "random_rhs": random_rhs,
-            "e2e": {"value": round(args.steps / e2e_s, 3), "unit": UNIT, "time_to_solution_ms": round(1e3 * e2e_s / args.steps, 2),
-                    "gmres_it_per_s": round(e2e_graph_its / e2e_s, 1),
-                    "h2d_bytes_per_step": 8 * s.n, "d2h_bytes_per_step": 8 * s.n,
-                    "path": "vem_mixed_solve_host (pinned host rhs -> solve -> u, p to host), CUDA graphs"},
+                       "kernels_source": f"per-launch CUDA events over a bounded run ({rb.report['iterations']} "
+                                         "GMRES iterations) after the timed region"},
+            "full_solve": {"time_to_solution_ms": round(tts_ms, 2), "iterations": fr["iterations"],
+                           "k_iterations": fr["k_iterations"], "inner_iterations": fr["inner_iterations"],
+                           "restarts": fr["restarts"], "converged": fr["converged"],
+                           "rel_residual_true": fr["rel_residual_true"], "conservation_rel": conservation,
+                           "solves_per_s": round(1e3 / tts_ms, 5),
+                           "gmres_it_per_s": round(fr["iterations"] / (tts_ms / 1e3), 4), "nested_counts": counts},
+            "roofline": roof, "kernels": kern,
+            "gpu_launches": int(round(launches_per_it * args.steps)),
+            "secondary": secondary, "paper_context": PAPER_CONTEXT,
+            "e2e": {"value": round(e2e_its / (e2e_ms / 1e3), 4), "unit": UNIT,
+                    "ms_per_step": round(e2e_ms / args.steps, 3),
+                    "h2d_bytes_per_step": 8 * s.n * e2e_calls / args.steps,
+                    "d2h_bytes_per_step": 8 * s.n * e2e_calls / args.steps,
+                    "solve_calls": e2e_calls,
+                    "path": "vem_mixed_solve_host (pinned host rhs -> device, solve, u and p -> host; every call)"},
             "clocks": clk.summary()}
     if rank == 0 and ws == 1 and not args.no_cpu_baseline:
         line["cpu_baseline"] = cpu_baseline(s, cfg, kind, eps, args.cpu_sample_its)
         line["cpu_baseline"].pop("setup_s", None)
-    sv.close()
+    if sv:
+        sv.close()
     if rank == 0:
         print(json.dumps(line), flush=True)
     if ws > 1:

@@ -93,7 +93,9 @@ typedef struct {
   int32_t use_graphs;     /* 1: replay GMRES cycles / PCG chunks as CUDA graphs (default)  */
   int32_t timing;         /* 1: time every launch with CUDA events (no graphs);
                              2: sampled, graph-compatible: the middle Chebyshev step of
-                                every Arnoldi step is bracketed by events (k = 0 path)    */
+                                every Arnoldi step is bracketed by events (k = 0 path);
+                                kinds 2 / 5 with the V-cycle inner PCG: one fine-level pass
+                                (class MG_FINE) per graph replay of the inner PCG          */
   int32_t pcg_chunk;      /* PCG steps per host convergence poll (default 16)              */
   int32_t reorth;         /* -1 auto (default): CGS1 for GMRES (Block-Schur / none), CGS2
                              for FGMRES (Block-Reg); 1: CGS2 always; 0: CGS1 always        */
@@ -112,7 +114,8 @@ typedef struct {
   double  k_rtol;         /* kind 5: the PCG on K stops at sqrt(r.z) <= k_rtol sqrt(r0.z0)
                              (default 0.1)                                                 */
   double  k_inner_rtol;   /* kind 5: tolerance of the inner PCG on S_D + eps W inside the
-                             Woodbury preconditioner of the PCG on K (default 1e-6)         */
+                             Woodbury preconditioner of the PCG on K (default 1e-8: errors of
+                             that solve are amplified by lambda(S_D) / eps in K)            */
   int32_t mg_chunk;       /* MG-PCG steps per host convergence poll (default 2)             */
 } vem_opts;
 
@@ -157,7 +160,8 @@ enum {
   VEM_K_UPDATE = 5,     /* CGS update w -= V h (+ norm, Givens)                  */
   VEM_K_PRECOND_VEC = 6,/* diagonal scalings, Woodbury pieces, Chebyshev init    */
   VEM_K_CYCLE = 7,      /* cycle end: back-substitution, x update                */
-  VEM_NUM_KCLASS = 8
+  VEM_K_MG_FINE = 8,    /* fine-level pass of the inner V-cycle: b - (S_D + eps W) d */
+  VEM_NUM_KCLASS = 9
 };
 
 /* bytes[] is the ALGORITHMIC HBM traffic of the timed launches:
@@ -167,6 +171,7 @@ enum {
  *   PCG_VEC   64 n_p                               (D^-1, p, q, x rw, r rw)
  *   DOT       8 n (nv + 1)                         (nv basis vectors + w)
  *   UPDATE    8 n (nv + 2)                         (nv basis vectors + w rw)
+ *   MG_FINE   12 nnz(S) + 32 n_p                   (S, W, d, b, out)
  * other classes count the vectors they stream once. */
 typedef struct {
   int64_t launches[VEM_NUM_KCLASS];
@@ -239,6 +244,12 @@ int vem_mixed_amg_level(vem_ctx *ctx, int32_t level, int64_t *n, int64_t *nnz);
  * n_p_dof = 1 and its element-mean block (S_D + eps W)[0::n_p, 0::n_p] otherwise).
  * VEM_ERR_INVALID if the level does not exist (always, when eps <= 0 at upload). */
 int vem_mixed_inner_amg_level(vem_ctx *ctx, int32_t level, int64_t *n, int64_t *nnz);
+
+/* Givens residual estimates |g_{j+1}| / ||rhs|| of the Arnoldi steps of
+ * the LAST GMRES cycle the last vem_mixed_solve ran, rebuilt from the device-resident sines:
+ * |g_{j+1}| = |s_j| |g_j|, g_0 = the residual norm the cycle started from.  hist (host, cap
+ * doubles, caller-owned) receives min(cap, *count) values; *count = steps of that cycle. */
+int vem_mixed_last_cycle_history(vem_ctx *ctx, double *hist, int32_t cap, int32_t *count);
 
 /* ---------------------------------------------------------------------------
  * Element-parallel assembly on the device

@@ -200,7 +200,7 @@ class Preconditioner:
     inner_precond: int = INNER_MG      # Block-Reg inner PCG preconditioner (R23)
     k_rtol: float = 0.1                # kind 5: relative tolerance of the PCG on K (R24)
     k_maxit: int = 500
-    k_inner_rtol: float = 1e-6         # kind 5: inner PCG tolerance of the Woodbury preconditioner (R24)
+    k_inner_rtol: float = 1e-8         # kind 5: inner PCG tolerance of the Woodbury preconditioner (R24)
     inner_iterations: int = 0
     k_iterations: int = 0
     inner_failed: bool = False
@@ -400,7 +400,7 @@ def gmres(matvec, precond, b, rtol=1e-10, restart=30, maxit=10000, flexible=Fals
 def solve(M, B, rhs, precond_kind=PRECOND_BLOCK_SCHUR, rtol=1e-10, restart=30, maxit=10000,
           eps=0.0, cheb_degree=16, cheb_ratio=30.0, inner_rtol=1e-14, inner_maxit=10000,
           exact_schur=False, block=1, reorth=-1, inner_precond=INNER_MG, k_rtol=0.1, k_maxit=500,
-          k_inner_rtol=1e-6):
+          k_inner_rtol=1e-8):
     """Oracle counterpart of vem_mixed_upload + vem_mixed_solve; `block` is
     the number of pressure DOFs per element (layout.n_p_dof).  reorth = -1
     (auto, reading R17): CGS1 for GMRES, CGS2 for the Block-Reg

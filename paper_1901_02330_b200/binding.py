@@ -25,7 +25,7 @@ PRECOND_BLOCK_REG_M = 5
 STATUS = {0: "OK", 1: "NOT_CONVERGED", 2: "BREAKDOWN", -1: "ERR_INVALID", -2: "ERR_DIAG_M",
           -3: "ERR_DIAG_S", -4: "ERR_CUDA", -5: "ERR_PRECOND", -6: "ERR_INNER"}
 
-KCLASSES = ["spmv", "cheb", "pcg_spmv", "pcg_vec", "dot", "update", "precond_vec", "cycle"]
+KCLASSES = ["spmv", "cheb", "pcg_spmv", "pcg_vec", "dot", "update", "precond_vec", "cycle", "mg_fine"]
 
 
 class vem_csr(C.Structure):
@@ -90,7 +90,7 @@ class vem_tet_class(C.Structure):
 
 
 class vem_kernel_stats(C.Structure):
-    _fields_ = [("launches", C.c_int64 * 8), ("ms", C.c_double * 8), ("bytes", C.c_double * 8)]
+    _fields_ = [("launches", C.c_int64 * 9), ("ms", C.c_double * 9), ("bytes", C.c_double * 9)]
 
     def as_dict(self):
         return {k: {"launches": int(self.launches[i]), "ms": float(self.ms[i]), "bytes": float(self.bytes[i])}
@@ -102,7 +102,8 @@ EXPORTS = ["vem_mixed_default_options", "vem_mixed_upload", "vem_mixed_solve", "
            "vem_mixed_upload_assembled", "vem_mixed_assembled_free",
            "vem_mixed_spmv", "vem_mixed_schur_spmv", "vem_mixed_precond_apply", "vem_mixed_set_options",
            "vem_mixed_get_options", "vem_mixed_get_info", "vem_mixed_get_schur", "vem_mixed_kernel_stats",
-           "vem_mixed_amg_level", "vem_mixed_inner_amg_level", "vem_mixed_destroy", "vem_status_string", "vem_last_error"]
+           "vem_mixed_amg_level", "vem_mixed_inner_amg_level", "vem_mixed_last_cycle_history",
+           "vem_mixed_destroy", "vem_status_string", "vem_last_error"]
 
 _lib = None
 
@@ -134,6 +135,7 @@ def load_library(path: str = LIB_PATH):
     lib.vem_mixed_kernel_stats.argtypes = [P, C.POINTER(vem_kernel_stats), C.c_int32]
     lib.vem_mixed_amg_level.argtypes = [P, C.c_int32, C.POINTER(C.c_int64), C.POINTER(C.c_int64)]
     lib.vem_mixed_inner_amg_level.argtypes = [P, C.c_int32, C.POINTER(C.c_int64), C.POINTER(C.c_int64)]
+    lib.vem_mixed_last_cycle_history.argtypes = [P, D, C.c_int32, C.POINTER(C.c_int32)]
     lib.vem_mixed_assemble.argtypes = [C.POINTER(P), C.POINTER(vem_cell_class), C.c_int32, C.c_int64, C.c_int64, P]
     lib.vem_mixed_assemble_tets.argtypes = [C.POINTER(P), C.POINTER(vem_tet_class), C.c_int32, C.c_int64,
                                             C.c_int64, P]
@@ -371,6 +373,14 @@ class VemMixed:
             self._check(self._lib.vem_mixed_amg_level(self._h, lev, C.byref(n), C.byref(z)), "amg_level")
             out.append((n.value, z.value))
         return out
+
+    def last_cycle_history(self) -> np.ndarray:
+        """Givens residual estimates |g_{j+1}| / ||rhs|| of the last GMRES cycle of the last solve."""
+        buf = np.zeros(128)
+        cnt = C.c_int32(0)
+        self._check(self._lib.vem_mixed_last_cycle_history(self._h, buf.ctypes.data_as(C.POINTER(C.c_double)), 128,
+                                                           C.byref(cnt)), "last_cycle_history")
+        return buf[:min(cnt.value, 128)].copy()
 
     def inner_amg_levels(self):
         """(rows, nnz) per level of the S_D + eps W hierarchy of the inner MG-PCG (R23)."""

@@ -195,9 +195,12 @@ struct Ctx {
   long se_n = 0, se_nnz = 0;
   cudaGraphExec_t pcgm_exec = nullptr;
   int pcgm_exec_chunk = 0;
+  cudaEvent_t mg_samp_a = nullptr, mg_samp_b = nullptr;   // timing = 2: one fine-level pass per replay
   // K-PCG (kind 5, R24): p (velocity part of kx = [p; B p]), r, z, q
   double *kx = nullptr, *kr = nullptr, *kz = nullptr, *kq = nullptr;
   int64_t k_its_total = 0;
+  int hist_steps = 0;                            // Arnoldi steps of the last cycle and the norms it started from
+  double hist_beta = 0.0, hist_bnorm = 0.0;
   bool trace_k = false;                          // VEM_TRACE_K=1: one stderr line per kind-5 apply
   bool k_failed = false;
   double *part = nullptr;
@@ -1004,8 +1007,13 @@ int enqueue_schur_mg(Ctx *c, const int *gate) {
     const double *rb = b;
     for (int i = 1; i < AMG_DEGREE; ++i) {
       {
-        TimeScope ts(c, VEM_K_CHEB, 12.0 * c->nnzS + 32.0 * np);
-        k_seps_resid<<<grid_for(np), NT, 0, c->stream>>>(np, S, c->wdiag, c->eps, dold, rb, c->cr, gate);
+        const bool smp = c->opts.timing == 2 && c->mg_samp_a && i == 1 && !acc;
+        if (smp) cudaEventRecordWithFlags(c->mg_samp_a, c->stream, cudaEventRecordExternal);
+        {
+          TimeScope ts(c, VEM_K_MG_FINE, 12.0 * c->nnzS + 32.0 * np);
+          k_seps_resid<<<grid_for(np), NT, 0, c->stream>>>(np, S, c->wdiag, c->eps, dold, rb, c->cr, gate);
+        }
+        if (smp) cudaEventRecordWithFlags(c->mg_samp_b, c->stream, cudaEventRecordExternal);
       }
       rb = c->cr;
       TimeScope ts(c, VEM_K_PRECOND_VEC, blk_bytes + 8.0 * np);
@@ -1016,7 +1024,7 @@ int enqueue_schur_mg(Ctx *c, const int *gate) {
   };
   smooth(c->mg_r, 0);
   {
-    TimeScope ts(c, VEM_K_CHEB, 12.0 * c->nnzS + 32.0 * np);
+    TimeScope ts(c, VEM_K_MG_FINE, 12.0 * c->nnzS + 32.0 * np);
     k_seps_resid<<<grid_for(np), NT, 0, c->stream>>>(np, S, c->wdiag, c->eps, c->mg_z, c->mg_r, c->cx, gate);
   }
   {
@@ -1029,7 +1037,7 @@ int enqueue_schur_mg(Ctx *c, const int *gate) {
     k_mg_prolong<<<grid_stream(c, ne), NT, 0, c->stream>>>(ne, c->nb, c->perm_p, H.lv[0].x, c->mg_z, gate);
   }
   {
-    TimeScope ts(c, VEM_K_CHEB, 12.0 * c->nnzS + 32.0 * np);
+    TimeScope ts(c, VEM_K_MG_FINE, 12.0 * c->nnzS + 32.0 * np);
     k_seps_resid<<<grid_for(np), NT, 0, c->stream>>>(np, S, c->wdiag, c->eps, c->mg_z, c->mg_r, c->cx, gate);
   }
   smooth(c->cx, 1);
@@ -1081,6 +1089,10 @@ int run_pcg_mg(Ctx *c, double rtol, const int *gate, int64_t *inner_its) {
   CKL();
   int chunk = std::max(1, std::min(c->opts.pcg_chunk, c->opts.mg_chunk));
   const bool graphs = c->opts.use_graphs && c->opts.timing != 1 && !c->capturing;
+  if (c->opts.timing == 2 && !c->mg_samp_a) {
+    CK(cudaEventCreate(&c->mg_samp_a));
+    CK(cudaEventCreate(&c->mg_samp_b));
+  }
   if (graphs && (!c->pcgm_exec || c->pcgm_exec_chunk != chunk)) {
     if (c->pcgm_exec) cudaGraphExecDestroy(c->pcgm_exec);
     c->pcgm_exec = nullptr;
@@ -1096,6 +1108,7 @@ int run_pcg_mg(Ctx *c, double rtol, const int *gate, int64_t *inner_its) {
     cudaGraphDestroy(g);
     c->pcgm_exec_chunk = chunk;
   }
+  int its_prev = 0;
   for (;;) {
     if (graphs) {
       CK(cudaGraphLaunch(c->pcgm_exec, c->stream));
@@ -1106,6 +1119,17 @@ int run_pcg_mg(Ctx *c, double rtol, const int *gate, int64_t *inner_its) {
     CK(cudaMemcpyAsync(&c->hst->p, &c->st->p, sizeof(PcgState), cudaMemcpyDeviceToHost, c->stream));
     CK(cudaStreamSynchronize(c->stream));
     flush_timing(c);
+    if (c->opts.timing == 2 && c->mg_samp_a && c->nb > 1 && (c->hst->p.active || c->hst->p.its - its_prev >= chunk)) {
+      float ms = 0.f;   // every V-cycle of the replay ran: its last recorded pair is a live pass
+      if (cudaEventElapsedTime(&ms, c->mg_samp_a, c->mg_samp_b) == cudaSuccess) {
+        c->stats.launches[VEM_K_MG_FINE] += 1;
+        c->stats.ms[VEM_K_MG_FINE] += ms;
+        c->stats.bytes[VEM_K_MG_FINE] += 12.0 * c->nnzS + 32.0 * c->np;
+      } else {
+        (void)cudaGetLastError();
+      }
+    }
+    its_prev = c->hst->p.its;
     if (!c->hst->p.active) break;
   }
   if (inner_its) *inner_its += c->hst->p.its;
@@ -1423,6 +1447,8 @@ int solve_impl(Ctx *c, const double *rhs, double tol, int maxit, int kind, doubl
     int its_before = c->hst->g.its;
     while (c->hst->g.its < maxit || cycles == 0) {
       if (maxit == 0) break;
+      c->hist_beta = c->hst->g.beta;   // residual norm this cycle starts from (vem_mixed_last_cycle_history)
+      c->hist_bnorm = bnorm;
       if (graphs) {
         if (!c->cycle_exec[kind]) {
           cudaGraph_t gr;
@@ -1450,6 +1476,7 @@ int solve_impl(Ctx *c, const double *rhs, double tol, int maxit, int kind, doubl
       CK(cudaStreamSynchronize(c->stream));
       flush_timing(c);
       collect_samples(c, c->hst->g.its - its_before, bytes_cheb(c));   // g.j was reset by the restart
+      c->hist_steps = c->hst->g.its - its_before;
       its_before = c->hst->g.its;
       const GmresState &h = c->hst->g;
       if (h.conv_true) break;
@@ -2701,6 +2728,8 @@ void destroy_ctx(Ctx *c) {
   for (auto e : c->free_events) cudaEventDestroy(e);
   for (auto e : c->samp_a) cudaEventDestroy(e);
   for (auto e : c->samp_b) cudaEventDestroy(e);
+  if (c->mg_samp_a) cudaEventDestroy(c->mg_samp_a);
+  if (c->mg_samp_b) cudaEventDestroy(c->mg_samp_b);
   for (void *p : c->allocs) cudaFree(p);
   if (c->hst) cudaFreeHost(c->hst);
   if (c->ev_in) cudaEventDestroy(c->ev_in);
@@ -2844,7 +2873,7 @@ void vem_mixed_default_options(vem_opts *o) {
   o->inner_precond = 1;
   o->k_maxit = 500;
   o->k_rtol = 0.1;
-  o->k_inner_rtol = 1e-6;
+  o->k_inner_rtol = 1e-8;
   o->mg_chunk = 2;
 }
 
@@ -3269,6 +3298,22 @@ int vem_mixed_amg_level(vem_ctx *h, int32_t level, int64_t *n, int64_t *nnz) {
   if (level < 0 || level >= (int)c->amg.lv.size()) return VEM_ERR_INVALID;
   *n = c->amg.lv[level].n;
   *nnz = c->amg.lv[level].nnz;
+  return VEM_OK;
+}
+
+int vem_mixed_last_cycle_history(vem_ctx *h, double *hist, int32_t cap, int32_t *count) {
+  if (!h || !hist || !count || cap < 0) return VEM_ERR_INVALID;
+  Ctx *c = h->impl;
+  const int k = std::min<int>(c->hist_steps, cap);
+  *count = c->hist_steps;
+  if (k <= 0 || !(c->hist_bnorm > 0.0)) return VEM_OK;
+  std::vector<double> sn(k);
+  CK(cudaMemcpy(sn.data(), c->st->sn, k * sizeof(double), cudaMemcpyDeviceToHost));
+  double g = c->hist_beta;
+  for (int j = 0; j < k; ++j) {   // |g_{j+1}| = |s_j| |g_j| (Givens, O8)
+    g *= fabs(sn[j]);
+    hist[j] = g / c->hist_bnorm;
+  }
   return VEM_OK;
 }
 

@@ -103,12 +103,32 @@ def test_block_reg_apply_parity(name):
 SOLVE_CASES = [("C1", 1), ("C1", 2), ("C3s", 1), ("C3s", 2), ("C2s", 1), ("C2s", 2), ("C4s", 1), ("C4s", 2)]
 
 
-def oracle_iteration_band(s, kind, restart, eps, trials=8):
-    """DESIGN.md reading R20: restarted GMRES iteration counts can be
-    ill-conditioned (a cycle that ends with the estimate just above rtol
-    restarts; just below, it stops).  The oracle's own count is therefore taken
-    as the set of counts over the unperturbed RHS and `trials` (8) RHS perturbed by
-    1e-15 relative (a few ulps); the GPU must land within +-2 of that band."""
+# Oracle counts under 8 RHS perturbations of 1e-15 relative (a few ulps), /tmp-measured with the
+# oracle alone and recorded in DESIGN.md R20: every case below has a spread of at most 1 except
+# C4s Block-Schur (198..216: GMRES(50) on the k = 2 cube ends cycles with the estimate within
+# rounding of rtol).  Only that case is compared with a band; the others are strict +-2.
+BAND_CASES = {("C4s", 1): 8}
+
+
+def log_counts(**kw):
+    """Per-case iteration counts, appended to gpurun_out/parity_counts.jsonl (copied to
+    profiles/ after a GPU run): the record `pytest -q` does not keep."""
+    import json
+    import os
+    d = os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))), "gpurun_out")
+    try:
+        os.makedirs(d, exist_ok=True)
+        with open(os.path.join(d, "parity_counts.jsonl"), "a") as f:
+            f.write(json.dumps(kw) + "\n")
+    except OSError:
+        pass
+
+
+def oracle_iteration_band(s, kind, restart, eps, trials=0):
+    """The oracle's solve and its iteration count.  trials > 0 (BAND_CASES only, DESIGN.md
+    reading R20): the count is the set over the unperturbed RHS and `trials` RHS perturbed
+    by 1e-15 relative, for the one case whose restarted-GMRES count is ill-conditioned in
+    the oracle itself; trials = 0: the band is the single unperturbed count (strict +-2)."""
     rng = np.random.default_rng(99)
     its = []
     ref = None
@@ -126,12 +146,14 @@ def test_solve_parity(name, kind):
     s = system(name)
     cfg = configs.CONFIGS[name]
     eps = configs.eps_for(s)
-    ref, lo, hi = oracle_iteration_band(s, kind, cfg.restart, eps)
+    ref, lo, hi = oracle_iteration_band(s, kind, cfg.restart, eps, BAND_CASES.get((name, kind), 0))
     sv = solver_for(s, restart=cfg.restart)
     res = sv.solve(torch.from_numpy(s.rhs).cuda(), 1e-10, 10000, kind)
     r = res.report
     assert r["status"] == 0 and r["converged"] == 1, r
     print(f"{name} precond={kind}: gpu {r['iterations']} oracle {ref.iterations} band [{lo}, {hi}] its")
+    log_counts(test="solve_parity", config=name, precond=kind, gpu=r["iterations"], oracle=ref.iterations,
+               band=[lo, hi], gpu_inner=r["inner_iterations"], oracle_inner=ref.inner_iterations)
     assert lo - 2 <= r["iterations"] <= hi + 2, (r["iterations"], lo, hi)
     nu = s.layout.n_u
     assert rel_inf(res.u.cpu().numpy(), ref.x[:nu]) <= 1e-8
@@ -142,10 +164,36 @@ def test_solve_parity(name, kind):
     sv.close()
 
 
+@pytest.mark.parametrize("name,kind", [("C1", 1), ("C3s", 1), ("C3s", 3), ("C2s", 1), ("C4s", 1), ("C3s", 2), ("C2s", 2)])
+def test_first_cycle_residual_history(name, kind):
+    """Element-wise parity of the Givens residual history |g_{j+1}| / ||b|| of the first
+    GMRES(m) cycle (one cycle from x0 = 0 on both sides): every Arnoldi step of the cycle,
+    not only the count.  The estimates agree to 1e-6 relative while they are above 1e-8 (below,
+    the rounding of ~1e-16 ||b|| in w is amplified by 1 / est)."""
+    s = system(name)
+    cfg = configs.CONFIGS[name]
+    eps = configs.eps_for(s)
+    m = cfg.restart
+    ref = O.solve(s.M, s.B, s.rhs, kind, 1e-10, m, maxit=m, eps=eps, block=s.layout.n_p_dof)
+    sv = solver_for(s, restart=m)
+    sv.solve(torch.from_numpy(s.rhs).cuda(), 1e-10, m, kind)
+    h = sv.last_cycle_history()
+    ho = np.array(ref.history[:len(h)])
+    assert len(h) == min(m, ref.iterations) == len(ho)
+    big = ho > 1e-8
+    err = np.abs(h - ho) / ho
+    log_counts(test="first_cycle_history", config=name, precond=kind, steps=len(h),
+               max_rel_err=float(err[big].max()) if big.any() else 0.0, last=float(h[-1]), oracle_last=float(ho[-1]))
+    assert err[big].max() <= 1e-6, (err.max(), int(err.argmax()))
+    assert np.all(err[~big] <= 1e-2)
+    sv.close()
+
+
 def test_block_reg_fixed_budget_c5s():
-    """C5 (pairs, anisotropic K with 1e-3 jumps) does not converge with the
-    diag(M)-Woodbury Block-Reg stand-in in this round, so parity
-    is checked on a fixed budget: one FGMRES(50) cycle from x0 = 0 on both sides."""
+    """C5 (pairs, anisotropic K with 1e-3 jumps) stagnates with the diag(M)-Woodbury
+    Block-Reg (kind 2; kind 5 is the converging form, tests/test_gpu_blockreg_m.py), so
+    kind-2 parity on this mesh is checked on a fixed budget: one FGMRES(50) cycle from
+    x0 = 0 on both sides."""
     s = system("C5s")
     eps = configs.eps_for(s)
     ref = O.solve(s.M, s.B, s.rhs, 2, 1e-10, 50, maxit=50, eps=eps, block=s.layout.n_p_dof)
@@ -326,7 +374,7 @@ def test_amg_three_level_group_csr(monkeypatch, group):
     zo32 = -h.to_float32().vcycle(v[nu:].astype(np.float32)).astype(np.float64)
     assert rel_inf(z32.cpu().numpy()[nu:], zo32) <= 2e-5
     if group == 8:
-        ref, lo, hi = oracle_iteration_band(s, 3, 50, 0.0, trials=2)
+        ref, lo, hi = oracle_iteration_band(s, 3, 50, 0.0)
         res = sv.solve(torch.from_numpy(s.rhs).cuda(), 1e-10, 10000, 3)
         assert res.report["converged"] == 1
         assert lo - 2 <= res.report["iterations"] <= hi + 2, (res.report["iterations"], lo, hi)
@@ -347,12 +395,79 @@ def test_random_rhs_parity(name, kind):
     class _S:   # the system with the random RHS (same matrices)
         M, B, layout = s.M, s.B, s.layout
     _S.rhs = rhs
-    ref, lo, hi = oracle_iteration_band(_S, kind, cfg.restart, eps, trials=2)
+    ref, lo, hi = oracle_iteration_band(_S, kind, cfg.restart, eps)
     sv = solver_for(s, restart=cfg.restart)
     res = sv.solve(torch.from_numpy(rhs).cuda(), 1e-10, 10000, kind)
     assert res.report["converged"] == 1
     assert lo - 2 <= res.report["iterations"] <= hi + 2, (res.report["iterations"], lo, hi)
     nu = s.layout.n_u
+    assert rel_inf(res.u.cpu().numpy(), ref.x[:nu]) <= 1e-8 and rel_inf(res.p.cpu().numpy(), ref.x[nu:]) <= 1e-8
+    sv.close()
+
+
+@pytest.mark.parametrize("name", ["C2s", "C4s", "C5s"])
+def test_split_block_pcg_path(monkeypatch, name):
+    """The split block-PCG kernels (k_pcg_spmv_p / k_pcg_alpha / k_pcg_vec_blk / k_pcg_beta /
+    k_pcg_pupd, graph chunks): the form every k >= 1 system above 262,144 pressure unknowns
+    runs (full C4, C5) when the inner preconditioner is the element-block Jacobi.  The reduced
+    cases take the one-launch persistent kernel by default, so it is switched off here."""
+    monkeypatch.setenv("VEM_PCG_PERSIST", "0")
+    s = system(name)
+    eps = configs.eps_for(s)
+    sv = solver_for(s, inner_precond=0, restart=configs.CONFIGS[name].restart)
+    P = O.Preconditioner(O.PRECOND_BLOCK_REG, s.M, s.B, eps=eps, block=s.layout.n_p_dof, inner_precond=0)
+    v = RNG.normal(size=s.n)
+    z, its = sv.precond_apply(pkg.PRECOND_BLOCK_REG, torch.from_numpy(v).cuda())
+    zo = P.apply(v)
+    nu = s.layout.n_u
+    log_counts(test="split_block_pcg_apply", config=name, gpu_inner=its, oracle_inner=P.inner_iterations)
+    assert abs(its - P.inner_iterations) <= 2
+    assert rel_inf(z.cpu().numpy()[:nu], zo[:nu]) <= 1e-8
+    if name != "C5s":   # kind 2 stagnates on the C5 type (DESIGN.md R24)
+        ref = O.solve(s.M, s.B, s.rhs, 2, 1e-10, configs.CONFIGS[name].restart, eps=eps, block=s.layout.n_p_dof,
+                      inner_precond=0)
+        res = sv.solve(torch.from_numpy(s.rhs).cuda(), 1e-10, 10000, 2)
+        log_counts(test="split_block_pcg_solve", config=name, gpu=res.report["iterations"], oracle=ref.iterations)
+        assert res.report["converged"] == 1
+        assert rel_inf(res.u.cpu().numpy(), ref.x[:nu]) <= 1e-8 and rel_inf(res.p.cpu().numpy(), ref.x[nu:]) <= 1e-8
+    sv.close()
+
+
+def test_amg_sell_coarse_levels(monkeypatch):
+    """VEM_AMG_WARP_ROWS=0: every coarse level of the C3m hierarchy runs the SELL-32
+    one-thread-per-row kernels, the form full C3's 206,540-row level 1 takes (levels with at
+    least 100,000 rows); by default every C3m coarse level takes the CSR group kernels."""
+    from oracle.amg import AMG
+    monkeypatch.setenv("VEM_AMG_WARP_ROWS", "0")
+    if "C3m" not in _CACHE:
+        _CACHE["C3m"] = C3M.build()
+    s = _CACHE["C3m"]
+    h = AMG(O.schur_diag(s.M, s.B))
+    sv = solver_for(s, restart=50)
+    assert sv.amg_levels() == [(lev.A.shape[0], lev.A.nnz) for lev in h.levels]
+    nu = s.layout.n_u
+    v = RNG.normal(size=s.n)
+    z, _ = sv.precond_apply(pkg.PRECOND_BLOCK_SCHUR_AMG, torch.from_numpy(v).cuda())
+    assert rel_inf(z.cpu().numpy()[nu:], -h.vcycle(v[nu:])) <= 1e-10
+    ref = O.solve(s.M, s.B, s.rhs, 3, 1e-10, 50)
+    res = sv.solve(torch.from_numpy(s.rhs).cuda(), 1e-10, 10000, 3)
+    log_counts(test="amg_sell_coarse_levels", config="C3m", gpu=res.report["iterations"], oracle=ref.iterations)
+    assert res.report["converged"] == 1 and abs(res.report["iterations"] - ref.iterations) <= 2
+    assert rel_inf(res.u.cpu().numpy(), ref.x[:nu]) <= 1e-8 and rel_inf(res.p.cpu().numpy(), ref.x[nu:]) <= 1e-8
+    sv.close()
+
+
+def test_fixed_grid_cgs_fallback(monkeypatch):
+    """ADVICE (round 1): the fixed-grid k_mdot / k_update launch forms (VEM_MDOT_WAVE=0,
+    VEM_UPDATE_WAVE=0) stay tested: same count, same solution as the oracle on C3s."""
+    monkeypatch.setenv("VEM_MDOT_WAVE", "0")
+    monkeypatch.setenv("VEM_UPDATE_WAVE", "0")
+    s = system("C3s")
+    ref = O.solve(s.M, s.B, s.rhs, 3, 1e-10, 50)
+    sv = solver_for(s, restart=50)
+    res = sv.solve(torch.from_numpy(s.rhs).cuda(), 1e-10, 10000, 3)
+    nu = s.layout.n_u
+    assert res.report["converged"] == 1 and abs(res.report["iterations"] - ref.iterations) <= 2
     assert rel_inf(res.u.cpu().numpy(), ref.x[:nu]) <= 1e-8 and rel_inf(res.p.cpu().numpy(), ref.x[nu:]) <= 1e-8
     sv.close()
 
@@ -511,4 +626,30 @@ def test_full_c3_sampled_and_properties():
     r = s.rhs - A @ np.concatenate([u, p])
     assert np.linalg.norm(r) <= 1.0001e-10 * np.linalg.norm(s.rhs)
     assert np.abs(s.B @ u - s.f).max() <= 1e-8 * np.abs(s.f).max()
+    sv.close()
+
+
+def test_full_c3_block_schur_amg_vs_oracle():
+    """The round-1 headline path at its stated size: C3 (8.4M DOFs), kind 3, against the
+    oracle's own full solve (about two minutes of numpy): level-by-level hierarchy rows,
+    iteration count +-2, u and p to 1e-8."""
+    from oracle.amg import AMG
+    s = system("C3")
+    SD = O.schur_diag(s.M, s.B)
+    h = AMG(SD)
+    sv = solver_for(s, restart=50)
+    got = sv.amg_levels()
+    want = [(lev.A.shape[0], lev.A.nnz) for lev in h.levels]
+    log_counts(test="full_c3_hierarchy", gpu=got, oracle=want)
+    assert [g[0] for g in got] == [w[0] for w in want]
+    # nonzeros: equal except where a Galerkin sum cancels to an exact zero on one side only
+    # (scipy's product drops exact zeros, the device run-reduce keeps every structural entry)
+    for g, w in zip(got, want):
+        assert 0 <= g[1] - w[1] <= 4, (got, want)
+    ref = O.solve(s.M, s.B, s.rhs, 3, 1e-10, 50)
+    res = sv.solve(torch.from_numpy(s.rhs).cuda(), 1e-10, 20000, 3)
+    log_counts(test="full_c3_kind3", gpu=res.report["iterations"], oracle=ref.iterations)
+    assert res.report["converged"] == 1 and abs(res.report["iterations"] - ref.iterations) <= 2
+    nu = s.layout.n_u
+    assert rel_inf(res.u.cpu().numpy(), ref.x[:nu]) <= 1e-8 and rel_inf(res.p.cpu().numpy(), ref.x[nu:]) <= 1e-8
     sv.close()
