@@ -23,7 +23,9 @@ Definition (the GPU follows it step by step):
     prolongator P = (I - omega D^-1 A) T with T piecewise constant on the
     aggregates and omega = 4 / (3 lmax) (Vanek, Mandel & Brezina 1996: one damped
     Jacobi step on the tentative prolongator); below, P = T.  A_c = P^T A P; stop
-    when n <= COARSE_SIZE, at MAX_LEVELS, or when a level coarsens by less than 1/0.75
+    when n <= COARSE_SIZE, at MAX_LEVELS, or when a level coarsens by less than 1/0.75;
+    exact-zero rule: an entry of P or A_c exists iff some term of its sum exists, whatever
+    the sum's value (with_structure), so the level sizes are integers both sides agree on
   * coarsest level (COARSE_SIZE = 2048): dense inverse applied as a matvec, else
     (stagnated coarsening) a degree-COARSE_DEGREE = 32 Chebyshev smoother (C3: the
     11,794-row coarsest; degree 8 / 16 / 32 / exact inverse give 118 / 101 / 95 / 95
@@ -125,13 +127,30 @@ def aggregate(A, theta=THETA):
     return agg2, nroot + left.size, is_root
 
 
+def with_structure(C, pattern):
+    """C with an explicit entry (possibly 0.0) wherever `pattern` has one.  The exact-zero
+    rule of the hierarchy (one rule on both sides, R22): an entry of a product
+    exists iff some term contributes to it, whatever the terms sum to.  scipy's sparse
+    product drops a sum that cancels to exactly 0.0, so the structural pattern is taken from
+    the same product of the absolute values (no cancellation) and merged back in."""
+    a, b = C.tocoo(), pattern.tocoo()
+    M = sp.csr_matrix((np.concatenate([a.data, np.zeros(b.nnz)]),
+                       (np.concatenate([a.row, b.row]), np.concatenate([a.col, b.col]))), shape=C.shape)
+    M.sum_duplicates()
+    M.sort_indices()
+    return M
+
+
+def triple_product(P, A):
+    """A_c = P^T A P with the structural pattern of the product (with_structure)."""
+    A = A.tocsr()
+    return with_structure((P.T @ A @ P).tocsr(), (abs(P).T @ abs(A) @ abs(P)).tocsr())
+
+
 def galerkin(A, agg, nc):
     n = A.shape[0]
     P = sp.csr_matrix((np.ones(n), (np.arange(n), agg)), shape=(n, nc))
-    Ac = (P.T @ A.tocsr() @ P).tocsr()
-    Ac.sum_duplicates()
-    Ac.sort_indices()
-    return Ac
+    return triple_product(P, A)
 
 
 def smoothed_prolongator(A, agg, nc, lmax):
@@ -140,8 +159,7 @@ def smoothed_prolongator(A, agg, nc, lmax):
     T = sp.csr_matrix((np.ones(n), (np.arange(n), agg)), shape=(n, nc))
     omega = 4.0 / (3.0 * lmax)
     P = (T - omega * (sp.diags(1.0 / A.diagonal()) @ (A.tocsr() @ T))).tocsr()
-    P.sort_indices()
-    return P
+    return with_structure(P, (T + abs(A.tocsr()) @ T).tocsr())
 
 
 def gershgorin(A):
@@ -176,9 +194,7 @@ class AMG:
             lev.agg, lev.nc = agg, nc
             if len(self.levels) <= SA_LEVELS:
                 lev.P = smoothed_prolongator(A, agg, nc, lev.lmax)
-                A = (lev.P.T @ A @ lev.P).tocsr()
-                A.sum_duplicates()
-                A.sort_indices()
+                A = triple_product(lev.P, A)
             else:
                 A = galerkin(A, agg, nc)
         last = self.levels[-1]
