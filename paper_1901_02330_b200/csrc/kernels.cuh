@@ -142,6 +142,9 @@ struct Sell {
 };
 __device__ __forceinline__ long sell_row(const Sell &A, long slot) { return A.perm ? (long)A.perm[slot] : slot; }
 
+// The matrix stream (values, column indices: read once per pass) uses __ldcs (evict-first).
+// Tried and rejected (R2_06): L1::no_allocate for the stream, to keep the gathered sectors of x in
+// L1: C5 fine-level pass 4.64 -> 4.11 TB/s, C3 solve 143.5 -> 157.5 ms.
 template <typename Gather>
 __device__ __forceinline__ double sell_dot(const Sell &A, long row, Gather g) {
   const long s = row >> 5;
@@ -1107,9 +1110,12 @@ __global__ void __launch_bounds__(256) k_pcg_spmv_p(long n, Sell S, const double
     q[row] = qi;
     v[0] = pi * qi;
   }
-  if (split) {   // partials only; k_pcg_alpha reduces them (no fence / atomic tail here)
-    block_sum_n<1>(v, sh);
-    if (threadIdx.x == 0) part[blockIdx.x] = v[0];
+  if (split) {
+    // partials only, one per WARP (no block barrier: a CTA retires warp by warp instead of
+    // holding its slots until its longest rows finish; ncu R2_04: 14% of the stalls were
+    // the barrier); k_pcg_alpha sums the 8 gridDim.x partials in a fixed order
+    const double w = warp_sum(v[0]);
+    if ((threadIdx.x & 31) == 0) part[(size_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5)] = w;
     return;
   }
   block_sum_n<1>(v, sh);
