@@ -508,7 +508,7 @@ def main():
                 "GBps": round(v["bytes"] / max(v["ms"], 1e-9) / 1e6, 1),
                 "frac_of_peak": round(v["bytes"] / max(v["ms"], 1e-9) / 1e6 / hbm, 4),
                 "share": round(v["ms"] / tot_ms, 4)}
-            for k, v in per.items()}
+            for k, v in per.items() if v["ms"] / tot_ms >= 1e-3}   # (gated no-op launches of a bounded run)
 
     secondary = None
     if rank == 0 and ws == 1 and not args.no_variant and cfg.name == "C5":

@@ -97,8 +97,11 @@ typedef struct {
                                 kinds 2 / 5 with the V-cycle inner PCG: one fine-level pass
                                 (class MG_FINE) per graph replay of the inner PCG          */
   int32_t pcg_chunk;      /* PCG steps per host convergence poll (default 16)              */
-  int32_t reorth;         /* -1 auto (default): CGS1 for GMRES (Block-Schur / none), CGS2
-                             for FGMRES (Block-Reg); 1: CGS2 always; 0: CGS1 always        */
+  int32_t reorth;         /* -1 auto (default): CGS2 for the Block-Reg FGMRES (kinds 2, 5), CGS1
+                             otherwise, including the FP32-V-cycle FGMRES (kind 4); 1: CGS2
+                             always; 0: CGS1 always.  The CGS grids are sized to one wave of
+                             resident CTAs (env VEM_MDOT_WAVE / VEM_UPDATE_WAVE = 0: fixed grids),
+                             so the partial-sum tree depends on the device and the build    */
   int32_t l2_persist;     /* 1 (default): persisting L2 window over the Chebyshev vectors  */
   int32_t reorder;        /* 1 (default): SELL-C-sigma symmetric reordering of the unknowns
                              at upload when n_p_dof > 1 and it removes >= 5% slice padding

@@ -194,7 +194,7 @@ __global__ void __launch_bounds__(1024) k_pcgm_conv(int nblk, const double *__re
     p.rr = v[0];
     if (sqrt(v[0]) <= p.tol_abs) {
       p.active = 0;
-    } else if (p.its >= p.maxit) {
+    } else if (p.its >= p.maxit || !(v[0] == v[0])) {   // cap reached, or NaN: stop at once
       p.active = 0;
       p.failed = 1;
     }
@@ -328,7 +328,7 @@ __global__ void __launch_bounds__(1024) k_k_rz(int nblk, const double *__restric
       k.its += 1;
       if (sqrt(fabs(v[0])) <= k.rtol * sqrt(k.rz0)) {
         k.active = 0;
-      } else if (k.its >= k.maxit) {
+      } else if (k.its >= k.maxit || !(v[0] == v[0])) {   // cap reached, or NaN: stop at once
         k.active = 0;
         k.failed = 1;
       } else {

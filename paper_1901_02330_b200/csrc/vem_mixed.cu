@@ -144,11 +144,11 @@ struct Ctx {
   double amg_warp_nnz = 1e30;                    // ... or with at least this many nnz per row (off: r8 A/B,
                                                  // SELL-32 beats group CSR on C3's 35-nnz/row level 1)
   int amg_group = 8;                             // lanes per CSR row (0: by the mean row length; r8 A/B)
-  double amg_group_div = 2.0;
+  double amg_group_div = 2.0;                    // ... G = power of two >= mean row length / this
   int pdl = 1;                                   // programmatic dependent launch of the V-cycle kernels
   int mdot_slots = 0;                            // >0: k_mdot grid = one full wave of this many resident CTAs
   int update_slots = 0;                          // >0: k_update grid = one full wave (VEM_UPDATE_WAVE)
-  bool pdl_skip = false;                         // next launch follows an event record: plain edge                    // ... G = power of two >= mean row length / this
+  bool pdl_skip = false;                         // next launch follows an event record: plain edge
   int amg_cluster = 0;                           // coarsest smoother as one cluster launch (VEM_AMG_CLUSTER=1;
                                                  // off by default: slower than the per-step launches)
   float *f32_pool = nullptr;                     // kind 4 fine-level vectors (L2-persisting window)
@@ -230,6 +230,7 @@ struct Ctx {
   double setup_ms = 0.0;
   int64_t device_bytes = 0;
   std::vector<void *> allocs;
+  std::vector<size_t> alloc_bytes;
 };
 
 int fail(Ctx *c, int code, const char *fmt, ...) {
@@ -269,6 +270,7 @@ int dalloc(Ctx *c, T **p, size_t count) {
   cudaError_t e = cudaMalloc((void **)p, bytes);
   if (e != cudaSuccess) return fail(c, VEM_ERR_CUDA, "cudaMalloc(%zu) failed: %s", bytes, cudaGetErrorString(e));
   c->allocs.push_back(*p);
+  c->alloc_bytes.push_back(bytes);
   c->device_bytes += bytes;
   return 0;
 }
@@ -281,7 +283,12 @@ int dalloc(Ctx *c, T **p, size_t count) {
 void dfree(Ctx *c, void *p) {
   if (!p) return;
   auto it = std::find(c->allocs.begin(), c->allocs.end(), p);
-  if (it != c->allocs.end()) c->allocs.erase(it);
+  if (it != c->allocs.end()) {
+    const size_t i = it - c->allocs.begin();
+    c->device_bytes -= (int64_t)c->alloc_bytes[i];
+    c->alloc_bytes.erase(c->alloc_bytes.begin() + i);
+    c->allocs.erase(it);
+  }
   cudaFree(p);
 }
 
@@ -1406,9 +1413,16 @@ int solve_impl(Ctx *c, const double *rhs, double tol, int maxit, int kind, doubl
       if (rc) return rc;
     }
   }
-  cudaEvent_t e0, e1;
-  CK(cudaEventCreate(&e0));
-  CK(cudaEventCreate(&e1));
+  struct EvPair {   // destroyed on every exit path
+    cudaEvent_t a = nullptr, b = nullptr;
+    ~EvPair() {
+      if (a) cudaEventDestroy(a);
+      if (b) cudaEventDestroy(b);
+    }
+  } ev;
+  CK(cudaEventCreate(&ev.a));
+  CK(cudaEventCreate(&ev.b));
+  cudaEvent_t e0 = ev.a, e1 = ev.b;
   CK(cudaEventRecord(e0, c->stream));
   to_internal(c, rhs, c->b);
   CK(cudaMemsetAsync(c->x, 0, c->n * sizeof(double), c->stream));
@@ -1500,8 +1514,6 @@ int solve_impl(Ctx *c, const double *rhs, double tol, int maxit, int kind, doubl
   flush_timing(c);
   float ms = 0.f;
   cudaEventElapsedTime(&ms, e0, e1);
-  cudaEventDestroy(e0);
-  cudaEventDestroy(e1);
   const GmresState &h = c->hst->g;
   R.status = status;
   R.iterations = h.its;
@@ -1604,6 +1616,7 @@ int build_schur(Ctx *c, const int64_t *brp, const int *bci, const double *bva, c
                                                               k0, v0);
     CKL();
     size_t tb = 0;
+    if (tot >= (1LL << 31)) return fail(c, VEM_ERR_INVALID, "S_D expansion chunk exceeds 2^31 entries");
     CK(cub::DeviceSegmentedSort::StableSortPairs(nullptr, tb, k0, k1, v0, v1, (int)tot, (int)nr, off, off + 1,
                                                  c->stream));
     char *tmp = nullptr;
@@ -1899,6 +1912,7 @@ int build_reorder(Ctx *c) {
 // ----------------------------------------------------------------------------
 template <typename T>
 int scan_excl(Ctx *c, const T *in, T *out, long n) {
+  if (n >= (1L << 31)) return fail(c, VEM_ERR_INVALID, "scan of %ld items exceeds the 32-bit CUB count", n);
   size_t tb = 0;
   CK(cub::DeviceScan::ExclusiveSum(nullptr, tb, in, out, (int)n, c->stream));
   char *tmp = nullptr;
@@ -1991,6 +2005,7 @@ int sort_reduce_csr(Ctx *c, unsigned long long *k0, double *v0, long m, long nro
   DA(v1, m);
   DA(flag, m + 1);
   DA(pos, m + 1);
+  if (m >= (1L << 31)) return fail(c, VEM_ERR_INVALID, "Galerkin expansion of %ld entries exceeds the 32-bit CUB count", m);
   int bits = 1;
   while ((1ULL << bits) < (unsigned long long)nrows * (unsigned long long)ncols) ++bits;
   if (m_valid >= 0) bits = 64;   // the drop marker is the largest key
