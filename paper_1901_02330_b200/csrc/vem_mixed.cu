@@ -1865,7 +1865,7 @@ int build_reorder(Ctx *c) {
       if (getenv("VEM_SETUP_TRACE"))
         fprintf(stderr, "[vem setup] S_D slots: row-sorted %ld, moment-major %ld stored entries\n", pad_sorted,
                 pad_moment);
-      if ((double)pad_moment <= 1.03 * (double)pad_sorted) sslot = ms;
+      if ((double)pad_moment <= 1.03 * (double)pad_sorted || atoi(getenv("VEM_SLOT_MOMENT")) == 2) sslot = ms;
     }
     for (long i = 0; i < np; ++i) sslot_old[i] = permp[sslot[i]];
   }

@@ -95,17 +95,21 @@ def test_block_reg_m_apply_parity(name):
     sv.close()
 
 
-@pytest.mark.parametrize("name", ["C5t", "C5s"])
-def test_block_reg_m_solve_parity(name):
+@pytest.mark.parametrize("name,kin", [("C5t", 1e-8), ("C5s", 1e-8), ("C2s", 1e-14)])
+def test_block_reg_m_solve_parity(name, kin):
     """The C5-type meshes (pairs, anisotropic K with jumps) converge with kind 5 where the
     diag(M) Block-Reg stagnates; u and p within 1e-8 of the oracle's solve, outer count
-    within +-2, true residual <= 1e-10 recomputed on the host."""
+    within +-2, true residual <= 1e-10 recomputed on the host.  C2s (Kuhn tets, K = I): the
+    inner tolerance the K solve needs is problem-dependent (R24): with the default
+    1e-8 every K solve hits its step cap on this mesh, with 1e-14 kind 5 needs 25 outer
+    iterations where kind 2 needs 140."""
     s = system(name)
     cfg = configs.CONFIGS[name]
     eps = configs.eps_for(s)
-    ref = O.solve(s.M, s.B, s.rhs, O.PRECOND_BLOCK_REG_M, 1e-10, cfg.restart, eps=eps, block=s.layout.n_p_dof)
+    ref = O.solve(s.M, s.B, s.rhs, O.PRECOND_BLOCK_REG_M, 1e-10, cfg.restart, eps=eps, block=s.layout.n_p_dof,
+                  k_inner_rtol=kin)
     assert ref.converged
-    sv = solver_for(s, restart=cfg.restart)
+    sv = solver_for(s, restart=cfg.restart, k_inner_rtol=kin)
     res = sv.solve(torch.from_numpy(s.rhs).cuda(), 1e-10, 10000, pkg.PRECOND_BLOCK_REG_M)
     r = res.report
     print(f"{name} kind 5: gpu {r['iterations']} outer / {r['k_iterations']} K / {r['inner_iterations']} inner; "

@@ -22,7 +22,10 @@ for name in ("C1", "C3s", "C2s", "C4s", "C5t"):
     kinds = (1, 2, 3, 4, 5) if s.layout.n_p_dof == 1 else (1, 2, 5)
     for kind in kinds:
         sv.precond_apply(kind, x)
-        r = sv.solve(torch.from_numpy(s.rhs).cuda(), 1e-10, 40 if (name == "C5t" and kind == 2) else 2000, kind)
+        # bounded where the default tolerances are not meant to converge (kind 2 on the C5 type;
+        # kind 5 with k_inner_rtol = 1e-8 on the tets / k = 2 cubes, R24)
+        cap = 40 if ((name == "C5t" and kind == 2) or (kind == 5 and name in ("C2s", "C4s"))) else 2000
+        r = sv.solve(torch.from_numpy(s.rhs).cuda(), 1e-10, cap, kind)
         print(name, kind, r.report["status_name"], r.report["iterations"], flush=True)
     sv.set_options(inner_precond=0)
     r = sv.solve(torch.from_numpy(s.rhs).cuda(), 1e-10, 40, 2)
