@@ -266,17 +266,16 @@ struct GatherK {
 __global__ void __launch_bounds__(256) k_kmul(long nu, Sell A, const double *__restrict__ kx,
                                               const double *__restrict__ wdiag, double inv_eps,
                                               double *__restrict__ q, double *part, const int *gate) {
+  __shared__ double sh[32];
   if (!*gate) return;
   const long row = (long)blockIdx.x * blockDim.x + threadIdx.x;
-  double v = 0.0;
+  double v[1] = {0.0};
   if (row < nu) {
     const double qi = sell_dot(A, row, GatherK{nu, inv_eps, kx, wdiag});
     q[row] = qi;
-    v = kx[row] * qi;
+    v[0] = kx[row] * qi;
   }
-  // one partial per warp (no block barrier, cf. k_pcg_spmv_p); k_k_alpha sums 8 gridDim.x of them
-  v = warp_sum(v);
-  if ((threadIdx.x & 31) == 0) part[(size_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5)] = v;
+  store_partials<1>(v, sh, part);
 }
 __global__ void __launch_bounds__(1024) k_k_alpha(int nblk, const double *__restrict__ part, DevState *st) {
   __shared__ double sh[32];

@@ -1110,12 +1110,11 @@ __global__ void __launch_bounds__(256) k_pcg_spmv_p(long n, Sell S, const double
     q[row] = qi;
     v[0] = pi * qi;
   }
-  if (split) {
-    // partials only, one per WARP (no block barrier: a CTA retires warp by warp instead of
-    // holding its slots until its longest rows finish; ncu R2_04: 14% of the stalls were
-    // the barrier); k_pcg_alpha sums the 8 gridDim.x partials in a fixed order
-    const double w = warp_sum(v[0]);
-    if ((threadIdx.x & 31) == 0) part[(size_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5)] = w;
+  if (split) {   // partials only; k_pcg_alpha reduces them (no fence / atomic tail here).  One partial
+    // per warp instead of per block was tried (R2_05, R2_09): the pass itself did not change and
+    // the one-block sum of 8x the partials cost 20 us more
+    block_sum_n<1>(v, sh);
+    if (threadIdx.x == 0) part[blockIdx.x] = v[0];
     return;
   }
   block_sum_n<1>(v, sh);

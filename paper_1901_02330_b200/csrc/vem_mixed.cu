@@ -653,7 +653,7 @@ int enqueue_pcg_steps(Ctx *c, int nsteps) {
         const int g = grid_for(c->np);
         k_pcg_spmv_p<<<g, NT, 0, c->stream>>>(c->np, sellS(c), c->wdiag, c->eps, c->pp0, c->pq, c->part,
                                               c->counter, c->st, c->pcg_split);
-        if (c->pcg_split) k_pcg_alpha<<<1, 1024, 0, c->stream>>>(g * (NT / 32), c->part, c->st);
+        if (c->pcg_split) k_pcg_alpha<<<1, 1024, 0, c->stream>>>(g, c->part, c->st);
       }
       {
         TimeScope ts(c, VEM_K_PCG_VEC, bytes_pcg_vec(c) + 8.0 * c->np * c->nb);
@@ -1070,7 +1070,7 @@ int enqueue_pcgm_steps(Ctx *c, int nsteps) {
       TimeScope ts(c, VEM_K_PCG_SPMV, 12.0 * c->nnzS + 32.0 * c->np);
       k_pcg_spmv_p<<<g, NT, 0, c->stream>>>(c->np, sellS(c), c->wdiag, c->eps, c->pp0, c->pq, c->part, c->counter,
                                             c->st, 1);
-      k_pcg_alpha<<<1, 1024, 0, c->stream>>>(g * (NT / 32), c->part, c->st);
+      k_pcg_alpha<<<1, 1024, 0, c->stream>>>(g, c->part, c->st);
     }
     {
       TimeScope ts(c, VEM_K_PCG_VEC, 48.0 * c->np);
@@ -1196,7 +1196,7 @@ int enqueue_block_reg_m(Ctx *c, const double *v, const double *scale, double *z,
       launch_spmv(c, nu, np, (const double *)c->kx, c->kx, nullptr, 0, gate_k(c));   // kx[nu:] = B p
       const int g = grid_for(nu);
       k_kmul<<<g, NT, 0, c->stream>>>(nu, sellA(c), c->kx, c->wdiag, inv_eps, c->kq, c->part, gate_k(c));
-      k_k_alpha<<<1, 1024, 0, c->stream>>>(g * (NT / 32), c->part, c->st);
+      k_k_alpha<<<1, 1024, 0, c->stream>>>(g, c->part, c->st);
     }
     {
       TimeScope ts(c, VEM_K_PRECOND_VEC, 48.0 * nu);
