@@ -447,3 +447,20 @@ def test_block_reg_m_gmres_vs_lu_c5t():
         assert np.abs(r.x[sl] - xd[sl]).max() <= 1e-8 * np.abs(xd[sl]).max()
     r2 = O.solve(s.M, s.B, s.rhs, O.PRECOND_BLOCK_REG, 1e-10, 50, eps=eps, block=s.layout.n_p_dof, maxit=100)
     assert not r2.converged
+
+
+@pytest.mark.parametrize("name", ["P1s", "P2s"])
+def test_paper_mode_gmres_vs_lu(name):
+    """Paper mode (the paper's BDM-type space, pressure P_{k-1}): the oracle's
+    preconditioned GMRES reaches the LU solution with both preconditioners (and with the
+    V-cycle Block-Schur where the pressure block is scalar, k = 1)."""
+    s = configs.CONFIGS[name].build()
+    eps = configs.eps_for(s)
+    nb = s.layout.n_p_dof
+    xd = O.dense_solve(s.M, s.B, s.rhs)
+    nu = s.layout.n_u
+    for kind in (1, 2) + ((3,) if nb == 1 else ()):
+        r = O.solve(s.M, s.B, s.rhs, kind, 1e-10, 50, eps=eps, block=nb)
+        assert r.converged, (name, kind)
+        for sl in (slice(0, nu), slice(nu, None)):
+            assert np.abs(r.x[sl] - xd[sl]).max() <= 1e-8 * np.abs(xd[sl]).max(), (name, kind)

@@ -314,3 +314,92 @@ def test_class_templates_recombine_to_the_assembled_system():
     import pytest
     with pytest.raises(ValueError):
         class_templates(configs.CONFIGS["C2s"].make_mesh(), 1)
+
+
+# ---------------------------------------------------------------------------
+# Paper mode: the paper's own BDM-type space, gradient moments over
+# M_{k-1} \ M_0, divergence and pressure in P_{k-1}
+# ---------------------------------------------------------------------------
+def test_paper_mode_dof_totals_from_the_assembler():
+    """The assembler's own layout in paper mode reproduces the paper's Cube-mesh DOF totals
+    (Tables 1 and 4, tests/golden/paper_cube_dofs.txt) up to the single mean-value
+    multiplier the paper's Neumann problem adds: N_u + N_p + 1 = dofs."""
+    path = os.path.join(os.path.dirname(__file__), "golden", "paper_cube_dofs.txt")
+    rows = [l.split()[:3] for l in open(path) if l.strip() and not l.startswith("#")]
+    for NP, k, dofs in rows:
+        NP, k, dofs = int(NP), int(k), int(dofs)
+        n = round(NP ** (1 / 3))
+        if k > 2:
+            continue   # k = 3 is outside BASELINE's orders
+        nkd = poly.dim_pk_3d(k - 1)
+        lay = assemble.Layout(k, poly.dim_pk_2d(k), (nkd - 1) + len(poly.generators(k)), nkd,
+                              3 * n * n * (n + 1), NP)
+        assert lay.n_u + lay.n_p + 1 == dofs
+    # and the layout formula above is what build_system uses (small meshes, assembled for real)
+    for n, k, want in ((8, 2, 19585), (4, 1, None), (3, 2, None)):
+        s = assemble.build_system(mesh.cube_mesh(n), k, paper_mode=True)
+        nkd = poly.dim_pk_3d(k - 1)
+        assert (s.layout.n_int_dof, s.layout.n_p_dof) == ((nkd - 1) + len(poly.generators(k)), nkd)
+        assert s.M.shape == (s.layout.n_u, s.layout.n_u) and s.B.shape == (s.layout.n_p, s.layout.n_u)
+        if want:
+            assert s.n + 1 == want   # Table 4, first row (N_P = 512, k = 2): 19,585
+
+
+@pytest.mark.parametrize("k", [1, 2])
+def test_paper_mode_projection_and_divergence(k):
+    """Unisolvence and the commuting divergence of the BDM-type local space: Pi @ D = I on
+    [P_k]^3, and Div(interp(v)) = the analytic divergence of v in [P_k]^3 (which lies in P_{k-1})."""
+    for name, m in _meshes():
+        for cls in m.classes:
+            o = local.local_operators(cls.rep(), k, k - 1)
+            PD = np.einsum("eil,elj->eij", o["Pi"], o["D"])
+            assert np.abs(PD - np.eye(PD.shape[1])).max() < 1e-9, (name, cls.name)
+        g = m.classes[-1].rep()
+        o = local.local_operators(g, k, k - 1)
+        alphas = poly.multi_indices_3d(k)
+        im = poly.index_map_3d(k)
+        nk, nkd = len(alphas), o["nkd"]
+        h = g["h"][0]
+        coef = RNG.normal(size=3 * nk)
+        dv = np.zeros(nk)
+        for c in range(3):
+            for a, al in enumerate(alphas):
+                if al[c]:
+                    am = list(al); am[c] -= 1
+                    dv[im[tuple(am)]] += coef[c * nk + a] * al[c] / h
+        assert np.abs(dv[nkd:]).max() == 0.0            # div [P_k]^3 is in P_{k-1}
+        got = o["Div"][0] @ (o["D"][0] @ coef)
+        assert got.shape == (nkd,)
+        assert np.abs(got - dv[:nkd]).max() < 1e-9 * max(1, np.abs(dv).max()), name
+
+
+@pytest.mark.parametrize("name,k", [("kuhn", 1), ("kuhn", 2), ("cube", 2), ("pairs", 1)])
+def test_paper_mode_M_spd_B_full_rank(name, k):
+    m = {"kuhn": lambda: mesh.kuhn_mesh(2, seed=3), "pairs": lambda: mesh.pair_mesh(4, seed=5, block=2),
+         "cube": lambda: mesh.cube_mesh(3)}[name]()
+    s = assemble.build_system(m, k, paper_mode=True)
+    M = s.M.toarray()
+    assert np.abs(M - M.T).max() <= 1e-12 * np.abs(M).max()
+    np.linalg.cholesky(0.5 * (M + M.T))
+    SD = (s.B @ sp.diags(1 / s.M.diagonal()) @ s.B.T).toarray()
+    np.linalg.cholesky(SD)
+    assert np.linalg.matrix_rank(s.B.toarray()) == s.layout.n_p
+
+
+@pytest.mark.parametrize("kind,k,ns", [("cube", 1, (4, 8)), ("cube", 2, (2, 4)), ("kuhn", 1, (2, 4))])
+def test_paper_mode_convergence_rates_and_conservation(kind, k, ns):
+    """The paper's estimates for its own space (Remark, P:823-837): the pressure in P_{k-1}
+    converges like h^k; local conservation B u_h = f_h holds element by element.
+    (One more refinement, run once: cube k = 1 rates (e_u, e_p) = (1.99, 1.01), cube k = 2
+    (3.03, 1.96), Kuhn k = 1 (1.87, 0.95): Pi^0_k u_h converges like h^{k+1}.)"""
+    errs = []
+    for n in ns:
+        m = {"cube": lambda: mesh.cube_mesh(n), "kuhn": lambda: mesh.kuhn_mesh(n, seed=2)}[kind]()
+        s = assemble.build_system(m, k, keep_local=True, paper_mode=True)
+        u, p = _direct(s)
+        assert np.abs(s.B @ u - s.f).max() <= 1e-10 * np.abs(s.f).max()
+        errs.append(assemble.l2_errors(s, u, p))
+    errs = np.array(errs)
+    rates = np.log2(errs[:-1] / errs[1:])
+    assert k - 0.25 <= rates[-1][1] <= k + 0.45, rates        # e_p ~ h^k
+    assert rates[-1][0] >= k - 0.25, rates                    # e_u at least h^k

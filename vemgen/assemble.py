@@ -165,7 +165,7 @@ def class_template(mesh, cls, ops, k: int, source=None) -> dict:
         B_e[bi, bj] = Bt[bi, bj]
         f_e = -|P| Hinv F_e."""
     nf = poly.dim_pk_2d(k)
-    nk = poly.dim_pk_3d(k)
+    nk = ops["nkd"]                      # pressure / divergence space P_kd (kd = k, or k - 1 in paper mode)
     n_int = (nk - 1) + poly.dim_gperp(k)
     E = cls.cell_ids.shape[0]
     fd = (cls.face_ids[:, :, None] * nf + np.arange(nf)[None, None, :]).reshape(E, -1)
@@ -182,8 +182,8 @@ def class_template(mesh, cls, ops, k: int, source=None) -> dict:
     mask = (A[0] != 0).any(axis=0) | (S[0] != 0)
     ii, jj = np.nonzero(mask)
     bi, bj = np.nonzero(Bt[0])
-    F = source_moments(cls, k, source)
-    Hinv = np.linalg.inv(ops["Hp"])
+    F = source_moments(cls, k, source)[:, :nk]
+    Hinv = np.linalg.inv(ops["Hp"][:, :nk, :nk])
     return dict(L=L, P=P, ii=ii, jj=jj, A=np.stack([A[0, c][ii, jj] for c in range(3)]), S=S[0][ii, jj],
                 coef=np.concatenate([invK, sP[:, None]], axis=1), bi=bi, bj=bj, B=Bt[0][bi, bj],
                 F=F, Hinv=np.broadcast_to(Hinv, (E, nk, nk))[0], vol=cls.vol)
@@ -274,10 +274,16 @@ def class_templates(mesh, k: int, source=None) -> list:
     return out
 
 
-def build_system(mesh, k: int, source=None, gD=None, keep_local=False) -> System:
-    """Assemble M, B, g, f for mesh at order k (RT-type, reading R1)."""
+def build_system(mesh, k: int, source=None, gD=None, keep_local=False, paper_mode=False) -> System:
+    """Assemble M, B, g, f for mesh at order k (RT-type, reading R1).  paper_mode: the
+    paper's own BDM-type space (gradient moments over M_{k-1} \\ M_0, divergence and pressure
+    in P_{k-1}, k >= 1) with this build's pressure-Dirichlet
+    boundary condition (R5): the paper's DOF total minus its mean-value multiplier."""
     nf = poly.dim_pk_2d(k)
-    nk = poly.dim_pk_3d(k)
+    kd = k - 1 if paper_mode else k
+    if kd < 0:
+        raise ValueError("paper mode needs k >= 1")
+    nk = poly.dim_pk_3d(kd)
     n_int = (nk - 1) + poly.dim_gperp(k)
     lay = Layout(k, nf, n_int, nk, mesh.n_faces, mesh.n_cells)
     Nu, Np = lay.n_u, lay.n_p
@@ -286,7 +292,7 @@ def build_system(mesh, k: int, source=None, gD=None, keep_local=False) -> System
     local_keep = []
     for cls in mesh.classes:
         E = cls.cell_ids.shape[0]
-        ops = local_operators(cls.rep(), k)
+        ops = local_operators(cls.rep(), k, kd)
         if cls.congruent:
             t = class_template(mesh, cls, ops, k, source)
             L, P, ii, jj, bi, bj = t["L"], t["P"], t["ii"], t["jj"], t["bi"], t["bj"]
@@ -318,8 +324,8 @@ def build_system(mesh, k: int, source=None, gD=None, keep_local=False) -> System
             br.append(np.broadcast_to(P[:, :, None], Bt.shape)[nzb])
             bc.append(np.broadcast_to(L[:, None, :], Bt.shape)[nzb])
             bv.append(Bt[nzb])
-            F = source_moments(cls, k, source)
-            Hinv = np.linalg.inv(ops["Hp"])
+            F = source_moments(cls, k, source)[:, :nk]
+            Hinv = np.linalg.inv(ops["Hp"][:, :nk, :nk])
             fP = -cls.vol[:, None] * np.einsum("eab,eb->ea", np.broadcast_to(Hinv, (E, nk, nk)), F)
         f[P.reshape(-1)] = fP.reshape(-1)
         if keep_local:
@@ -345,7 +351,8 @@ def pressure_coeffs(system: System, p_mom: np.ndarray):
     out = []
     for cls, ops, L, P in system.local:
         E = cls.cell_ids.shape[0]
-        Hinv = np.broadcast_to(np.linalg.inv(ops["Hp"]), (E,) + ops["Hp"].shape[1:])
+        nkd = ops["nkd"]
+        Hinv = np.broadcast_to(np.linalg.inv(ops["Hp"][:, :nkd, :nkd]), (E, nkd, nkd))
         out.append((cls, cls.vol[:, None] * np.einsum("eab,eb->ea", Hinv, p_mom[P])))
     return out
 
@@ -368,9 +375,10 @@ def l2_errors(system: System, u: np.ndarray, p: np.ndarray, K=None):
         Pi = np.broadcast_to(ops["Pi"], (E,) + ops["Pi"].shape[1:])
         cu = np.einsum("eil,el->ei", Pi, u[L])                     # (E, 3 nk)
         uh = np.stack([np.einsum("eqa,ea->eq", m, cu[:, c * nk:(c + 1) * nk]) for c in range(3)], -1)
-        Hinv = np.broadcast_to(np.linalg.inv(ops["Hp"]), (E, nk, nk))
+        nkd = ops["nkd"]
+        Hinv = np.broadcast_to(np.linalg.inv(ops["Hp"][:, :nkd, :nkd]), (E, nkd, nkd))
         cp = cls.vol[:, None] * np.einsum("eab,eb->ea", Hinv, p[P])
-        ph = np.einsum("eqa,ea->eq", m, cp)
+        ph = np.einsum("eqa,ea->eq", m[..., :nkd], cp)
         ue = exact_u(pts, K)
         pe = exact_p(pts)
         eu2 += float(np.einsum("eq,eqd->", w, (ue - uh) ** 2))

@@ -53,6 +53,7 @@ class Config:
     block: int = 0     # K block size (cubes) / pairing block (pairs)
     seed: int = 0
     describe: str = ""
+    paper: bool = False   # the paper's own BDM-type space (pressure P_{k-1}), SURVEY.md N3
 
     def make_mesh(self):
         if self.kind == "cube":
@@ -66,7 +67,7 @@ class Config:
         raise ValueError(self.kind)
 
     def build(self, keep_local=False):
-        return build_system(self.make_mesh(), self.k, keep_local=keep_local)
+        return build_system(self.make_mesh(), self.k, keep_local=keep_local, paper_mode=self.paper)
 
 
 CONFIGS = {
@@ -88,7 +89,18 @@ CONFIGS = {
     # C5-type at 6^3 (two K blocks per axis): the size at which the oracle finishes the
     # kind-5 solve (PCG on M + B^T (eps W)^-1 B inside FGMRES, R24) in seconds
     "C5t": Config("C5t", "pairs", 6, 1, (BLOCK_REG,), 50, block=3, seed=5),
+    # paper mode (N3): the paper's BDM-type space on cube grids, K = I (its Tables 1 and 4 use Cube
+    # meshes at k = 1, 2), with this build's Dirichlet pressure data (R5)
+    "P1s": Config("P1s", "cube", 6, 1, (BLOCK_SCHUR, BLOCK_REG), 50, paper=True,
+                  describe="6^3 cubes, paper-mode k=1 (pressure P0)"),
+    "P2s": Config("P2s", "cube", 4, 2, (BLOCK_SCHUR, BLOCK_REG), 50, paper=True,
+                  describe="4^3 cubes, paper-mode k=2 (pressure P1)"),
 }
+
+
+def paper_cube(n: int, k: int) -> Config:
+    """Cube n^3 in paper mode at order k (the meshes of PAPER.md Table 4: n = 8, 16, 20, 24, 28 at k = 2)."""
+    return Config(f"paper-cube{n}-k{k}", "cube", n, k, (BLOCK_SCHUR, BLOCK_REG), 50, paper=True)
 
 
 def eps_for(system) -> float:

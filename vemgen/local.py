@@ -41,8 +41,12 @@ def face_coords(f, pts):
                     axis=-1) / f.h[:, None, None]
 
 
-def local_operators(g: dict, k: int) -> dict:
-    """Compute, for the batch of cells described by g (see CellClass.rep):
+def local_operators(g: dict, k: int, kd: int | None = None) -> dict:
+    """kd = order of the divergence / pressure space: k (RT-type, reading R1, the default) or
+    k - 1 (the paper's own BDM-type space: gradient moments over M_{k-1} \\ M_0, div v and
+    pressure in P_{k-1}; SURVEY.md N3 "paper mode").
+
+    Compute, for the batch of cells described by g (see CellClass.rep):
       Hp    (E, n_k, n_k)     int_P m_a m_b                       (monomial mass)
       Div   (E, n_k, n_loc)   chi -> coefficients of div v in M_k
       Pi    (E, 3 n_k, n_loc) chi -> coefficients of Pi^0_k v in [M_k]^3
@@ -55,10 +59,13 @@ def local_operators(g: dict, k: int) -> dict:
     idx1 = poly.index_map_3d(k + 1)
     betas = poly.multi_indices_2d(k)
     nk, nk1, nf = len(alphas), len(alphas1), len(betas)
+    kd = k if kd is None else kd
+    assert kd in (k, k - 1) and kd >= 0
+    nkd = poly.dim_pk_3d(kd)          # graded-lex order: the first nkd monomials span P_kd
     gens = poly.generators(k)
     gen_idx = {gg: i for i, gg in enumerate(gens)}
     nF = len(g["faces"])
-    ngrad = nk - 1
+    ngrad = nkd - 1
     ncross = len(gens)
     nloc = nF * nf + ngrad + ncross
     off_grad = nF * nf
@@ -92,21 +99,21 @@ def local_operators(g: dict, k: int) -> dict:
         Bnd[:, :, lf * nf:(lf + 1) * nf] += sig[:, None, None] * np.einsum("eab,eac->ebc", Phi, CF)
         facedata.append((fp, fw, mf, np.broadcast_to(f.normal, (E, 3)), area))
 
-    # divergence: Hp d = r, r_a = -[a != 0] (|P|/h_P) chi^grad_a + Bnd[a]
-    r = Bnd[:, :nk, :].copy()
-    for a in range(1, nk):
+    # divergence in P_kd: Hp d = r, r_a = -[a != 0] (|P|/h_P) chi^grad_a + Bnd[a], a in M_kd
+    r = Bnd[:, :nkd, :].copy()
+    for a in range(1, nkd):
         r[:, a, off_grad + a - 1] -= vol / hP
-    Div = np.linalg.solve(Hp, r)
+    Div = np.linalg.solve(Hp[:, :nkd, :nkd], r)
 
     # G[b] . chi = int_P v . grad m_b, b in M_{k+1}, |b| >= 1
     G = np.zeros((E, nk1, nloc))
     for b, beta in enumerate(alphas1):
         if sum(beta) == 0:
             continue
-        if sum(beta) <= k:
+        if sum(beta) <= kd:
             G[:, b, off_grad + b - 1] = vol / hP
-        else:
-            G[:, b] = -np.einsum("ea,eal->el", Hk_k1[:, :, b], Div) + Bnd[:, b]
+        else:   # by parts with div v in P_kd
+            G[:, b] = -np.einsum("ea,eal->el", Hk_k1[:, :nkd, b], Div) + Bnd[:, b]
 
     # R rows: int_P v . (e_c m_a) via Props 1-3 and Prop. inTermsOfGPerpBasis
     R = np.zeros((E, 3 * nk, nloc))
@@ -129,7 +136,7 @@ def local_operators(g: dict, k: int) -> dict:
             D[:, lf * nf:(lf + 1) * nf, c * nk:(c + 1) * nk] = nrm[:, c, None, None] * base
     imap = poly.index_map_3d(k)
     mvk = mv[..., :nk]
-    for a in range(1, nk):
+    for a in range(1, nkd):
         alpha = alphas[a]
         for c in range(3):
             if alpha[c] == 0:
@@ -150,7 +157,7 @@ def local_operators(g: dict, k: int) -> dict:
                             Pi[:, c * nk:(c + 1) * nk]) for c in range(3)], axis=1)
     IDP = np.eye(nloc)[None] - np.einsum("eij,ejl->eil", D, Pi)
     S = np.einsum("eki,ekj->eij", IDP, IDP)
-    return dict(Hp=Hp, Div=Div, Pi=Pi, D=D, A=A, S=S, nloc=nloc, nk=nk, nf=nf,
+    return dict(Hp=Hp, Div=Div, Pi=Pi, D=D, A=A, S=S, nloc=nloc, nk=nk, nkd=nkd, nf=nf,
                 n_int=ngrad + ncross, vol=vol, h=hP)
 
 
