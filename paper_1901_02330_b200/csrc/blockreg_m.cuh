@@ -3,7 +3,7 @@
 //   * MG-PCG: the inner PCG on S_eps = S_D + eps W preconditioned by one V-cycle of S_eps
 //     (reading R23; oracle/amg.py SchurMG, oracle/solver.py pcg).  n_p_dof = 1: the
 //     aggregation V-cycle of amg_apply.cuh on the S_eps hierarchy.  n_p_dof > 1: a p-multigrid
-//     whose smoother is the element-block-Jacobi Chebyshev(3) on [2/30, 2] (k_mg_blk,
+//     whose smoother is the element-block-Jacobi Chebyshev(2) on [2/6, 2] (k_mg_blk,
 //     k_seps_resid) and whose coarse space is the element-mean moment (k_mg_inject,
 //     k_mg_prolong) with the aggregation V-cycle on S_eps[0::n_p, 0::n_p].
 //   * K-PCG (precond kind 5, reading R24; oracle/solver.py pcg_k): PCG on the paper's

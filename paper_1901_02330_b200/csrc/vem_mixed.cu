@@ -766,9 +766,13 @@ int run_pcg(Ctx *c, int64_t *inner_its) {
 constexpr double AMG_THETA = 0.08, AMG_THETA_COARSE = 0.04, AMG_RATIO = 30.0, AMG_STAGNATION = 0.75;
 constexpr int AMG_SA_LEVELS = 1;   // levels with the smoothed prolongator (oracle/amg.py SA_LEVELS)
 constexpr int AMG_COARSE_SIZE = 2048, AMG_MAX_LEVELS = 12, AMG_DEGREE = 3, AMG_COARSE_DEGREE = 32;
+// p-multigrid smoother of the inner V-cycle at n_p_dof > 1 (oracle/amg.py P_DEGREE, P_RATIO; R23)
+constexpr int MG_P_DEGREE = 2;
+constexpr double MG_P_RATIO = 6.0;
 
-void amg_cheb_coeffs(double lmax, int degree, double &inv_theta, std::vector<double> &c1, std::vector<double> &c2) {
-  const double b = lmax, a = lmax / AMG_RATIO;
+void amg_cheb_coeffs(double lmax, int degree, double &inv_theta, std::vector<double> &c1, std::vector<double> &c2,
+                     double ratio = AMG_RATIO) {
+  const double b = lmax, a = lmax / ratio;
   const double theta = 0.5 * (b + a), delta = 0.5 * (b - a), sigma = theta / delta;
   double rho = 1.0 / sigma;
   inv_theta = 1.0 / theta;
@@ -1002,17 +1006,17 @@ int enqueue_schur_mg(Ctx *c, const int *gate) {
   const long np = c->np, ne = np / c->nb;
   double it;
   std::vector<double> c1, c2;
-  amg_cheb_coeffs(2.0, AMG_DEGREE, it, c1, c2);   // lambda_max(D_B^-1 S_eps) <= 2 (R15)
+  amg_cheb_coeffs(2.0, MG_P_DEGREE, it, c1, c2, MG_P_RATIO);   // lambda_max(D_B^-1 S_eps) <= 2 (R15)
   const Sell S = sellS(c);
   const double blk_bytes = 8.0 * np * (4 + c->nb);
-  auto smooth = [&](const double *b, int acc) {   // mg_z (+)= C_3(b)
+  auto smooth = [&](const double *b, int acc) {   // mg_z (+)= C(b), Chebyshev(MG_P_DEGREE)
     {
       TimeScope ts(c, VEM_K_PRECOND_VEC, blk_bytes);
       dispatch_nb<MgBlkL>(c->nb, c, b, (const double *)nullptr, c->cd0, c->mg_z, 0.0, it, 1, acc, gate);
     }
     double *dold = c->cd0, *dnew = c->cd1;
     const double *rb = b;
-    for (int i = 1; i < AMG_DEGREE; ++i) {
+    for (int i = 1; i < MG_P_DEGREE; ++i) {
       {
         const bool smp = c->opts.timing == 2 && c->capturing && c->mg_samp_a && i == 1 && !acc;
         if (smp) cudaEventRecordWithFlags(c->mg_samp_a, c->stream, cudaEventRecordExternal);
