@@ -30,7 +30,9 @@ Definition (the GPU follows it step by step):
     (stagnated coarsening) a degree-COARSE_DEGREE = 32 Chebyshev smoother (C3: the
     11,794-row coarsest; degree 8 / 16 / 32 / exact inverse give 118 / 101 / 95 / 95
     GMRES iterations, R22)
-  * smoother C_l(b): degree-DEGREE point-Jacobi Chebyshev from x0 = 0 (Saad
+  * smoother C_l(b): degree-DEGREE (3; degree 2 was measured on the GPU and rejected: full C3
+    111 iterations / 151.0 ms instead of 95 / 143.5 ms, full C5 91.0 s instead of 88.7 s)
+    point-Jacobi Chebyshev from x0 = 0 (Saad
     Alg. 12.1, exactly oracle.solver.chebyshev) on [lmax/RATIO, lmax] with the
     Gershgorin bound lmax = max_i sum_j |A_ij| / A_ii
   * V(b) at level l: x = C(b); r = b - A x; x += P V(P^T r); x += C(b - A x)

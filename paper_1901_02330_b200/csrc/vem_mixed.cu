@@ -835,6 +835,17 @@ void amg_smooth(Ctx *c, AmgLevel &L, const T *b, T *out, int degree, const int *
   T *dold = D.sd0(), *dnew = D.sd1();
   int first = 1;
   if (degree > 1) {   // init fused into the first step
+    // degree 2: this launch is the whole smoother, so it is the one the sampled timing brackets
+    const bool smp0 = sample && degree == 2 && c->opts.timing == 2 && c->sample_slot >= 0 && !L.warp_rows;
+    if (smp0) cudaEventRecordWithFlags(c->samp_a[c->sample_slot], c->stream, cudaEventRecordExternal);
+    c->sample_recorded |= smp0;
+    struct SampleEnd {
+      Ctx *c;
+      bool on;
+      ~SampleEnd() {
+        if (on) cudaEventRecordWithFlags(c->samp_b[c->sample_slot], c->stream, cudaEventRecordExternal);
+      }
+    } sample_end{c, smp0};
     TimeScope ts(c, VEM_K_CHEB, vb * L.nnz + 6.0 * sizeof(T) * L.n);
     if (L.warp_rows)
       VC_GROUP_LAUNCH(k_vc_cheb_first_w, L, L.n, L.rp, L.ci, D.va(), D.dinv(), b, (T)it, (T)c1[0], (T)c2[0],
@@ -1493,7 +1504,11 @@ int solve_impl(Ctx *c, const double *rhs, double tol, int maxit, int kind, doubl
       CK(cudaMemcpyAsync(&c->hst->g, &c->st->g, sizeof(GmresState), cudaMemcpyDeviceToHost, c->stream));
       CK(cudaStreamSynchronize(c->stream));
       flush_timing(c);
-      collect_samples(c, c->hst->g.its - its_before, bytes_cheb(c));   // g.j was reset by the restart
+      // the sampled launch: k_cheb_step (kind 1) or, with the degree-2 V-cycle smoother, the
+      // fine-level k_vc_cheb_first (kinds 3, 4: one vector less than a later step)
+      collect_samples(c, c->hst->g.its - its_before,
+                      (kind == VEM_PRECOND_BLOCK_SCHUR_AMG && AMG_DEGREE == 2) ? bytes_cheb(c) - 8.0 * c->np
+                                                                               : bytes_cheb(c));   // g.j was reset by the restart
       c->hist_steps = c->hst->g.its - its_before;
       its_before = c->hst->g.its;
       const GmresState &h = c->hst->g;
