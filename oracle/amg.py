@@ -61,6 +61,7 @@ COARSE_DEGREE = 32
 STAGNATION = 0.75
 P_DEGREE = 2       # smoother of the p-multigrid (SchurMG, n_p > 1): Chebyshev(P_DEGREE) on [2/P_RATIO, 2]
 P_RATIO = 6.0
+P_COARSE_DEGREE = 8   # Chebyshev degree of a non-dense coarsest level of the SchurMG hierarchy
 KEY_INDEX_BITS = 30
 ROOT_KEY = np.int64(np.iinfo(np.int64).max)
 
@@ -184,7 +185,8 @@ class Level:
 class AMG:
     """Aggregation V-cycle hierarchy for an SPD matrix (point Jacobi smoothing)."""
 
-    def __init__(self, A, theta=THETA, coarse_size=COARSE_SIZE, max_levels=MAX_LEVELS):
+    def __init__(self, A, theta=THETA, coarse_size=COARSE_SIZE, max_levels=MAX_LEVELS, coarse_degree=None):
+        self.coarse_degree = coarse_degree   # None: the module's COARSE_DEGREE (kinds 3, 4)
         self.levels = []
         A = A.tocsr()
         while True:
@@ -225,7 +227,7 @@ class AMG:
         if level == len(self.levels) - 1:
             if self.coarse_inv is not None:
                 return self.coarse_inv @ b
-            return self.smooth(lev, b, COARSE_DEGREE)
+            return self.smooth(lev, b, COARSE_DEGREE if self.coarse_degree is None else self.coarse_degree)
         x = self.smooth(lev, b)
         r = b - lev.A @ x
         if lev.P is not None:
@@ -262,19 +264,23 @@ class SchurMG:
           S_c   = R S R^T = S[0::n_p, 0::n_p], solved by one V-cycle of AMG(S_c)
           V(b)  : x = C(b); r = b - S x; x[0::n_p] += AMG(S_c).vcycle(r[0::n_p]);
                   x += C(b - S x)
+      * a non-dense coarsest level of either hierarchy (stagnated coarsening: the 18,380-row
+        coarsest of C5's mean-moment block) is smoothed by Chebyshev(P_COARSE_DEGREE = 8), not
+        the 32 of kind 3: inside a PCG that runs to a tolerance the coarsest solve hardly
+        matters (C5-type 96^3, steps to 1e-8: degree 32 / 16 / 8 / 4 -> 22 / 22 / 23 / 28)
     """
 
-    def __init__(self, S, nb, DBinv=None):
+    def __init__(self, S, nb, DBinv=None, max_levels=MAX_LEVELS):
         self.S = S.tocsr()
         self.nb = nb
         if nb == 1:
-            self.amg = AMG(self.S)
+            self.amg = AMG(self.S, coarse_degree=P_COARSE_DEGREE, max_levels=max_levels)
         else:
             from .solver import block_jacobi_inv
             self.DBinv = block_jacobi_inv(self.S, nb) if DBinv is None else DBinv
             self.Sc = self.S[0::nb, 0::nb].tocsr()
             self.Sc.sort_indices()
-            self.amg = AMG(self.Sc)
+            self.amg = AMG(self.Sc, coarse_degree=P_COARSE_DEGREE, max_levels=max_levels)
 
     def smooth(self, b):
         return chebyshev(self.S, self.DBinv, b, P_DEGREE, 2.0, P_RATIO)

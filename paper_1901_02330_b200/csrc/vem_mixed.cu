@@ -81,6 +81,7 @@ struct AmgHier {
   double *cinv = nullptr;      // dense inverse of the coarsest level
   float *cinv_f = nullptr;     // its FP32 copy (kind 4)
   bool dense = false;
+  int coarse_degree = 32;      // Chebyshev degree of a non-dense coarsest level
 };
 
 // level data of the V-cycle in precision T
@@ -769,6 +770,7 @@ constexpr int AMG_COARSE_SIZE = 2048, AMG_MAX_LEVELS = 12, AMG_DEGREE = 3, AMG_C
 // p-multigrid smoother of the inner V-cycle at n_p_dof > 1 (oracle/amg.py P_DEGREE, P_RATIO; R23)
 constexpr int MG_P_DEGREE = 2;
 constexpr double MG_P_RATIO = 6.0;
+constexpr int MG_COARSE_DEGREE = 8;   // non-dense coarsest level of the S_eps hierarchy (P_COARSE_DEGREE)
 
 void amg_cheb_coeffs(double lmax, int degree, double &inv_theta, std::vector<double> &c1, std::vector<double> &c2,
                      double ratio = AMG_RATIO) {
@@ -941,7 +943,7 @@ void amg_vcycle(Ctx *c, AmgHier &H, size_t l, const int *gate) {
     } else if (L.vc_ok) {
       amg_coarse_cluster<T>(c, L, gate);
     } else {
-      amg_smooth<T>(c, L, D.b(), D.x(), c->amg_coarse_degree, gate);
+      amg_smooth<T>(c, L, D.b(), D.x(), H.coarse_degree, gate);
     }
     return;
   }
@@ -2721,6 +2723,7 @@ int upload_impl(Ctx *c, const vem_csr *M, const vem_csr *B, const vem_csr *W, do
     L0.dinv = c->dSinv;
     L0.lmax = c->lmax;
     L0.owns_matrix = false;
+    c->amg.coarse_degree = c->amg_coarse_degree;
     int rr = build_amg(c, c->amg, L0, c->sdiag, true);
     if (rr) return rr;
     rr = build_amg_f32(c);
@@ -2747,6 +2750,7 @@ int upload_impl(Ctx *c, const vem_csr *M, const vem_csr *B, const vem_csr *W, do
     L0.dinv = c->se_dinv;
     int rr = build_sell(c, L0.n, L0.rp, L0.ci, L0.va, &L0.soff, &L0.sci, &L0.sva, &L0.nnz_sell);
     if (rr) return rr;
+    c->amge.coarse_degree = getenv("VEM_MG_COARSE_DEGREE") ? atoi(getenv("VEM_MG_COARSE_DEGREE")) : MG_COARSE_DEGREE;
     rr = build_amg(c, c->amge, L0, c->se_diag, c->nb == 1);
     if (rr) return rr;
     if (c->nb == 1) {

@@ -122,3 +122,31 @@ def test_block_reg_m_solve_parity(name, kin):
     x = np.concatenate([res.u.cpu().numpy(), res.p.cpu().numpy()])
     assert np.linalg.norm(s.rhs - O.spmv_saddle(s.M, s.B, x)) <= 1e-10 * np.linalg.norm(s.rhs) * 1.0001
     sv.close()
+
+
+@pytest.mark.parametrize("case", ["C3m", "P24"])
+def test_inner_hierarchy_chebyshev_coarsest(monkeypatch, case):
+    """VEM_AMG_MAX_LEVELS=2 leaves a coarsest level above 2048 rows, which the S_eps hierarchy
+    smooths with Chebyshev(8) (oracle/amg.py P_COARSE_DEGREE) instead of a dense inverse: the form
+    full C5's stagnated 18,380-row coarsest level runs.  C3m: n_p_dof = 1 (3,643-row coarsest);
+    P24: the 24^3 C5-type mesh, n_p_dof = 4 (5,853-row coarsest of the mean-moment block)."""
+    from oracle.amg import SchurMG
+    monkeypatch.setenv("VEM_AMG_MAX_LEVELS", "2")
+    cfg = (configs.Config("C3m", "cube", 32, 0, (2,), 50, block=4, seed=3) if case == "C3m"
+           else configs.Config("P24", "pairs", 24, 1, (2,), 50, block=3, seed=5))
+    s = cfg.build()
+    eps = configs.eps_for(s)
+    nb = s.layout.n_p_dof
+    P = O.Preconditioner(O.PRECOND_BLOCK_REG, s.M, s.B, eps=eps, block=nb)
+    P.inner_prec = SchurMG(P.Seps, nb, max_levels=2)
+    assert len(P.inner_prec.amg.levels) == 2 and P.inner_prec.amg.coarse_inv is None
+    sv = solver_for(s)
+    assert sv.inner_amg_levels() == [(lv.A.shape[0], lv.A.nnz) for lv in P.inner_prec.amg.levels]
+    v = RNG.normal(size=s.n)
+    z, its = sv.precond_apply(pkg.PRECOND_BLOCK_REG, torch.from_numpy(v).cuda())
+    zo = P.apply(v)
+    nu = s.layout.n_u
+    print(f"{case}: inner steps gpu {its} oracle {P.inner_iterations}")
+    assert abs(its - P.inner_iterations) <= 2
+    assert rel_inf(z.cpu().numpy()[:nu], zo[:nu]) <= 1e-8
+    sv.close()
