@@ -496,7 +496,8 @@ def main():
         ach = d["bytes"] / (d["ms"] / 1e3) / 1e9
         agg = per[dom]
         roof = {"bound": "hbm", "kernel": dom, "achieved": round(ach, 1), "peak": hbm, "unit": "GB/s",
-                "frac": round(ach / hbm, 4), "traffic": ncu_traffic(dom), "peak_source": peak_kind,
+                "frac": round(ach / hbm, 4), "frac_of_nominal_8TBps": round(ach / 8000.0, 4),
+                "traffic": ncu_traffic(dom), "peak_source": peak_kind,
                 "bytes_per_launch": d["bytes"] / d["launches"], "avg_launch_us": 1e3 * d["ms"] / d["launches"],
                 "launches_timed": d["launches"], "source": src,
                 # the same class over every launch of the breakdown run, and its share of that run
