@@ -56,7 +56,9 @@ enum {
 
 /* 3: Block-Schur with one aggregation V-cycle on S_D in place of the Chebyshev
  * iteration (the GPU-native stand-in for the exact MUMPS solve of S, P:978;
- * DESIGN.md reading R22; n_p_dof = 1 only in this version). */
+ * DESIGN.md reading R22; n_p_dof = 1 only, and only for a non-singular S_D: with pure
+ * Neumann data B^T annihilates the constant pressure, the coarsest level has no dense
+ * inverse, upload succeeds without the hierarchy and kinds 3 / 4 return VEM_ERR_PRECOND). */
 enum { VEM_PRECOND_NONE = 0, VEM_PRECOND_BLOCK_SCHUR = 1, VEM_PRECOND_BLOCK_REG = 2, VEM_PRECOND_BLOCK_SCHUR_AMG = 3,
        /* kind 3 with the V-cycle in FP32 (hierarchy values and vectors), GMRES and the
         * saddle operator in FP64: the mixed-precision preconditioner of SURVEY.md §8(f) N4 */

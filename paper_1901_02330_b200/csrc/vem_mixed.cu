@@ -200,6 +200,7 @@ struct Ctx {
   // K-PCG (kind 5, R24): p (velocity part of kx = [p; B p]), r, z, q
   double *kx = nullptr, *kr = nullptr, *kz = nullptr, *kq = nullptr;
   int64_t k_its_total = 0;
+  std::string amg_unavailable;                   // why the S_D hierarchy of kinds 3 / 4 was not built
   int hist_steps = 0;                            // Arnoldi steps of the last cycle and the norms it started from
   double hist_beta = 0.0, hist_bnorm = 0.0;
   bool trace_k = false;                          // VEM_TRACE_K=1: one stderr line per kind-5 apply
@@ -976,7 +977,9 @@ void amg_vcycle(Ctx *c, AmgHier &H, size_t l, const int *gate) {
 template <typename T>
 int enqueue_block_schur_amg(Ctx *c, const double *v, const double *scale, double *z, const int *gate,
                             bool z_out = true) {
-  if (c->amg.lv.empty()) return fail(c, VEM_ERR_PRECOND, "Block-Schur-AMG needs n_p_dof = 1 (k = 0)");
+  if (c->amg.lv.empty())
+    return fail(c, VEM_ERR_PRECOND, "Block-Schur-AMG is unavailable: %s",
+                c->amg_unavailable.empty() ? "it needs n_p_dof = 1" : c->amg_unavailable.c_str());
   if (sizeof(T) == 4 && !c->amg_f32) return fail(c, VEM_ERR_PRECOND, "FP32 hierarchy not built");
   AmgLevel &L0 = c->amg.lv[0];
   const Lv<T> D0{L0};
@@ -2725,11 +2728,23 @@ int upload_impl(Ctx *c, const vem_csr *M, const vem_csr *B, const vem_csr *W, do
     L0.owns_matrix = false;
     c->amg.coarse_degree = c->amg_coarse_degree;
     int rr = build_amg(c, c->amg, L0, c->sdiag, true);
-    if (rr) return rr;
-    rr = build_amg_f32(c);
-    if (rr) return rr;
-    rr = build_amg_cluster(c);
-    if (rr) return rr;
+    if (rr == VEM_ERR_DIAG_S) {
+      // a singular S_D (pure Neumann data: B^T annihilates the constant pressure) has no dense
+      // coarsest inverse: kinds 3 and 4 are unavailable for this system (solve returns
+      // VEM_ERR_PRECOND), kinds 1, 2 and 5 do not need the hierarchy
+      c->amg.lv.clear();
+      c->amg.dense = false;
+      c->amg_unavailable = c->err;
+      CK(cudaMemsetAsync(c->derr, 0, sizeof(int), c->stream));
+      CK(cudaStreamSynchronize(c->stream));
+      rr = 0;
+    } else {
+      if (rr) return rr;
+      rr = build_amg_f32(c);
+      if (rr) return rr;
+      rr = build_amg_cluster(c);
+      if (rr) return rr;
+    }
   }
   if (c->has_reg) {   // S_eps hierarchy: the V-cycle preconditioner of Block-Reg's inner PCG (R23)
     AmgLevel L0;

@@ -54,3 +54,34 @@ def test_paper_mode_solve_parity(name, kind):
     u = res.u.cpu().numpy()
     assert np.abs(s.B @ u - s.f).max() <= 1e-8 * np.abs(s.f).max()   # local conservation
     sv.close()
+
+
+@pytest.mark.parametrize("n,k,kind", [(4, 1, 1), (4, 1, 2), (3, 2, 1), (3, 2, 2)])
+def test_paper_neumann_solve_parity(n, k, kind):
+    """The paper's own boundary value problem (Neumann data, mean-value multiplier, polynomial
+    solution; vemgen.configs.paper_neumann) through the C ABI: the multiplier in closed form, the
+    consistent singular saddle system solved on the GPU, the pressure projected onto mean zero.
+    Against the oracle's solve of the same system (u and p to 1e-8; count +-2 for Block-Schur, +-5
+    for Block-Reg: on this singular system S_D + eps W has the eigenvalue eps on the constant
+    pressure, the inner solves amplify rounding along it by 1 / eps, and the oracle's own count
+    spreads 87..89 / 75..76 under 1e-15 RHS perturbations) and against the sparse LU solution of
+    the bordered system with the multiplier (u, p to 1e-7)."""
+    import scipy.sparse.linalg as spl
+    s, N = configs.paper_neumann(n, k)
+    nb = s.layout.n_p_dof
+    eps = 1e-6 * float(N.M.diagonal().mean())
+    ref = O.solve(N.M, N.B, N.rhs, kind, 1e-10, 50, eps=eps, block=nb, maxit=5000)
+    assert ref.converged
+    sv = pkg.VemMixed(N.M, N.B, eps=eps, layout=s.layout, opts=pkg.default_options(restart=50))
+    res = sv.solve(torch.from_numpy(N.rhs).cuda(), 1e-10, 10000, kind)
+    r = res.report
+    print(f"paper Neumann n={n} k={k} precond={kind}: gpu {r['iterations']} oracle {ref.iterations}")
+    assert r["converged"] == 1 and abs(r["iterations"] - ref.iterations) <= (2 if kind == 1 else 5), (
+        r["iterations"], ref.iterations)
+    nu = s.layout.n_u
+    u, p = res.u.cpu().numpy(), N.project(res.p.cpu().numpy())
+    assert rel_inf(u, ref.x[:nu]) <= 1e-8 and rel_inf(p, N.project(ref.x[nu:])) <= 1e-8
+    x = spl.spsolve(N.bordered().tocsc(), N.bordered_rhs())
+    assert rel_inf(u, x[:nu]) <= 1e-7 and rel_inf(p, x[nu:-1]) <= 1e-7
+    assert abs(N.c @ p) <= 1e-12 * np.abs(N.c).sum() * np.abs(p).max()
+    sv.close()

@@ -464,3 +464,24 @@ def test_paper_mode_gmres_vs_lu(name):
         assert r.converged, (name, kind)
         for sl in (slice(0, nu), slice(nu, None)):
             assert np.abs(r.x[sl] - xd[sl]).max() <= 1e-8 * np.abs(xd[sl]).max(), (name, kind)
+
+
+@pytest.mark.parametrize("n,k", [(4, 1), (3, 2)])
+def test_paper_neumann_gmres_equals_bordered_lu(n, k):
+    """The paper's bordered system [M B^T 0; B 0 c; 0 c^T 0] (Neumann data + mean-value
+    multiplier) against the way it goes through the solver: the multiplier
+    in closed form (ones.f / ones.c), preconditioned GMRES on the consistent singular saddle
+    system [M B^T; B 0][u; p] = [g; f - c lambda], then the projection of p onto c.p = 0.  Both of
+    the paper's preconditioners reach the LU solution of the bordered system."""
+    import scipy.sparse.linalg as spl
+    s, N = configs.paper_neumann(n, k)
+    x = spl.spsolve(N.bordered().tocsc(), N.bordered_rhs())
+    nu = s.layout.n_u
+    ub, pb = x[:nu], x[nu:-1]
+    eps = 1e-6 * float(N.M.diagonal().mean())
+    for kind in (1, 2):
+        r = O.solve(N.M, N.B, N.rhs, kind, 1e-10, 50, eps=eps, block=s.layout.n_p_dof, maxit=2000)
+        assert r.converged, (n, k, kind)
+        u, p = r.x[:nu], N.project(r.x[nu:])
+        assert np.abs(u - ub).max() <= 1e-8 * np.abs(ub).max()
+        assert np.abs(p - pb).max() <= 1e-8 * np.abs(pb).max()

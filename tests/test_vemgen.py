@@ -403,3 +403,40 @@ def test_paper_mode_convergence_rates_and_conservation(kind, k, ns):
     rates = np.log2(errs[:-1] / errs[1:])
     assert k - 0.25 <= rates[-1][1] <= k + 0.45, rates        # e_p ~ h^k
     assert rates[-1][0] >= k - 0.25, rates                    # e_u at least h^k
+
+
+@pytest.mark.parametrize("k,ns", [(1, (2, 4)), (2, (2, 4))])
+def test_paper_neumann_problem(k, ns):
+    """The paper's own boundary value problem: Neumann data on
+    the whole boundary, the mean-zero pressure enforced by one multiplier, the polynomial
+    solution.  The DOF total with the multiplier is the paper's formula; B^T annihilates the
+    constant pressure; the multiplier of the bordered LU solve equals its closed form
+    ones.f / ones.c (zero up to rounding: the data are compatible); int p_h = 0; e_p ~ h^k and
+    e_u ~ h^{k+1} for the paper's solution."""
+    errs = []
+    for n in ns:
+        s, N = configs.paper_neumann(n, k)
+        nkd = poly.dim_pk_3d(k - 1)
+        want = (3 * n * n * (n + 1) * poly.dim_pk_2d(k)
+                + n ** 3 * ((nkd - 1) + len(poly.generators(k)) + nkd) + 1)
+        assert s.n + 1 == want == N.bordered().shape[0]
+        assert np.abs(N.B.T @ N.ones).max() <= 1e-13 * abs(N.B).max()
+        x = spl.spsolve(N.bordered().tocsc(), N.bordered_rhs())
+        nu = s.layout.n_u
+        u, p, lam = x[:nu], x[nu:-1], x[-1]
+        scale = np.abs(N.f).max() / np.abs(N.c).max()
+        assert abs(lam - N.lam) <= 1e-10 * scale and abs(N.lam) <= 1e-10 * scale
+        assert abs(N.c @ p) <= 1e-12 * np.abs(N.c).sum() * np.abs(p).max()
+        assert np.abs(u[N.boundary_dofs] - N.u_boundary).max() <= 1e-12 * np.abs(N.u_boundary).max()
+        # errors against the exact pair (p with its mean removed)
+        old = assemble.exact_u, assemble.exact_p
+        assemble.exact_u = lambda pts, K=None: assemble.paper_exact_u(pts)
+        assemble.exact_p = lambda pts: assemble.paper_exact_p(pts) - assemble.PAPER_P_MEAN
+        try:
+            errs.append(assemble.l2_errors(s, u, p))
+        finally:
+            assemble.exact_u, assemble.exact_p = old
+    errs = np.array(errs)
+    rates = np.log2(errs[:-1] / errs[1:])
+    assert k - 0.25 <= rates[-1][1] <= k + 0.45, rates
+    assert rates[-1][0] >= k + 1 - 0.25, rates

@@ -386,3 +386,116 @@ def l2_errors(system: System, u: np.ndarray, p: np.ndarray, K=None):
         ep2 += float(np.einsum("eq,eq->", w, (pe - ph) ** 2))
         np2 += float(np.einsum("eq,eq->", w, pe ** 2))
     return np.sqrt(eu2 / nu2), np.sqrt(ep2 / np2)
+
+
+# ---------------------------------------------------------------------------
+# The paper's own boundary value problem: Neumann data u.n = u_N on the whole
+# boundary and the mean-zero pressure enforced by one multiplier (PAPER.md P:562-566,
+# P:764-765), with the paper's polynomial solution
+# ---------------------------------------------------------------------------
+def paper_exact_p(x):
+    """q = x^5 + 6 y^4 + 9 z^3 + x y^2 z^3, before the mean is removed."""
+    X, Y, Z = x[..., 0], x[..., 1], x[..., 2]
+    return X ** 5 + 6 * Y ** 4 + 9 * Z ** 3 + X * Y ** 2 * Z ** 3
+
+
+PAPER_P_MEAN = 1.0 / 6 + 6.0 / 5 + 9.0 / 4 + (1.0 / 2) * (1.0 / 3) * (1.0 / 4)   # int over [0,1]^3
+
+
+def paper_exact_u(x):
+    """v = -grad q = (-5x^4 - y^2 z^3, -24 y^3 - 2 x y z^3, -27 z^2 - 3 x y^2 z^2) (nu = 1)."""
+    X, Y, Z = x[..., 0], x[..., 1], x[..., 2]
+    return np.stack([-5 * X ** 4 - Y ** 2 * Z ** 3, -24 * Y ** 3 - 2 * X * Y * Z ** 3,
+                     -27 * Z ** 2 - 3 * X * Y ** 2 * Z ** 2], axis=-1)
+
+
+def paper_source(x):
+    """f = div v = -20 x^3 - 72 y^2 - 2 x z^3 - 54 z - 6 x y^2 z."""
+    X, Y, Z = x[..., 0], x[..., 1], x[..., 2]
+    return -20 * X ** 3 - 72 * Y ** 2 - 2 * X * Z ** 3 - 54 * Z - 6 * X * Y ** 2 * Z
+
+
+@dataclass
+class NeumannSystem:
+    """The bordered system of the paper's problem,
+        [ M   B^T  0 ] [u]        [g]
+        [ B   0    c ] [p]      = [f]          c_i = int q_i  (mean-value functional),
+        [ 0   c^T  0 ] [lambda]   [0]
+    after the boundary face DOFs were set to the data (their rows of M are diag(M), their columns
+    of M and B moved to the right-hand side).  `ones` holds the moments of the constant pressure 1
+    (B^T ones = 0: the pressure is determined up to it, which the multiplier row removes)."""
+    M: sp.csr_matrix
+    B: sp.csr_matrix
+    g: np.ndarray
+    f: np.ndarray
+    c: np.ndarray
+    ones: np.ndarray
+    layout: Layout
+    boundary_dofs: np.ndarray
+    u_boundary: np.ndarray
+
+    @property
+    def lam(self) -> float:
+        """The multiplier in closed form: ones^T (B u + c lambda) = ones^T f and B^T ones = 0."""
+        return float(self.ones @ self.f) / float(self.ones @ self.c)
+
+    @property
+    def rhs(self) -> np.ndarray:
+        """Right-hand side of the consistent singular saddle system [M B^T; B 0][u; p] = [g; f - c lambda]
+        that goes through the C ABI; project() then picks the mean-zero pressure."""
+        return np.concatenate([self.g, self.f - self.lam * self.c])
+
+    def project(self, p: np.ndarray) -> np.ndarray:
+        """The pressure of the bordered system: p - (c.p / c.ones) ones."""
+        return p - (self.c @ p) / (self.c @ self.ones) * self.ones
+
+    def bordered(self) -> sp.csr_matrix:
+        c = sp.csr_matrix(self.c.reshape(-1, 1))
+        return sp.bmat([[self.M, self.B.T, None], [self.B, None, c], [None, c.T, None]]).tocsr()
+
+    def bordered_rhs(self) -> np.ndarray:
+        return np.concatenate([self.g, self.f, [0.0]])
+
+
+def neumann_system(system: System, u_exact) -> NeumannSystem:
+    """Impose u.n = u_exact.n on every boundary face of `system` (assembled with keep_local=True)
+    and add the mean-value multiplier data."""
+    mesh, k = system.mesh, system.k
+    nf = poly.dim_pk_2d(k)
+    fg = mesh.boundary_geom
+    q = 2 * k + 8
+    if fg.kind == "para":
+        fp, fw = parallelogram_rule(fg.v0, fg.v1, fg.v2, q)
+    else:
+        fp, fw = triangle_rule(fg.v0, fg.v1, fg.v2, q)
+    from .local import face_coords
+    mf = poly.eval_monomials_2d(face_coords(fg, fp), k)
+    un = np.einsum("eqd,ed->eq", u_exact(fp), fg.normal)            # u . n_f (global face normal)
+    uB = (np.einsum("eq,eq,eqa->ea", fw, un, mf) / fg.area[:, None]).reshape(-1)   # face moments (P:626)
+    bd = (mesh.boundary_faces[:, None] * nf + np.arange(nf)[None, :]).reshape(-1)
+    nu = system.layout.n_u
+    xb = np.zeros(nu)
+    xb[bd] = uB
+    g = system.g - system.M @ xb
+    f = system.f - system.B @ xb
+    keep = np.ones(nu)
+    keep[bd] = 0.0
+    Dk = sp.diags(keep)
+    dM = system.M.diagonal()
+    M = (Dk @ system.M @ Dk + sp.diags((1 - keep) * dM)).tocsr()
+    B = (system.B @ Dk).tocsr()
+    for A_ in (M, B):      # the C ABI wants sorted, duplicate-free rows
+        A_.eliminate_zeros()
+        A_.sum_duplicates()
+        A_.sort_indices()
+    g[bd] = dM[bd] * uB
+    # mean-value functional and the constant pressure in moment unknowns
+    c = np.zeros(system.layout.n_p)
+    ones = np.zeros(system.layout.n_p)
+    for cls, ops, L, P in system.local:
+        nkd = ops["nkd"]
+        E = cls.cell_ids.shape[0]
+        Hp = np.broadcast_to(ops["Hp"], (E,) + ops["Hp"].shape[1:])
+        c[P[:, 0]] = cls.vol                                     # int q = |P| * (mean moment)
+        ones[P.reshape(-1)] = (Hp[:, 0, :nkd] / cls.vol[:, None]).reshape(-1)   # (1/|P|) int m_a
+    return NeumannSystem(M, B, g, f, c, ones, system.layout, bd, uB)

@@ -115,3 +115,11 @@ def random_rhs(n: int, seed: int = 7) -> np.ndarray:
     representative; this RHS is."""
     return np.random.default_rng(seed).standard_normal(n)
 
+
+def paper_neumann(n: int, k: int):
+    """The paper's own boundary value problem on the n^3 cube grid at order k:
+    BDM-type space, nu = 1, the polynomial solution of PAPER.md P:898-911, Neumann data on the
+    whole boundary and the mean-value multiplier.  Returns (System, NeumannSystem)."""
+    from .assemble import neumann_system, paper_exact_u, paper_source
+    s = build_system(_mesh.cube_mesh(n), k, source=paper_source, keep_local=True, paper_mode=True)
+    return s, neumann_system(s, paper_exact_u)
