@@ -122,6 +122,12 @@ typedef struct {
                              Woodbury preconditioner of the PCG on K (default 1e-8: errors of
                              that solve are amplified by lambda(S_D) / eps in K)            */
   int32_t mg_chunk;       /* MG-PCG steps per host convergence poll (default 2)             */
+  int32_t basis_f32;      /* 1: compressed Krylov basis: every basis vector is
+                             the float32 rounding of the vector Arnoldi produced, used as such by
+                             every reader; the CGS kernels stream the float copy (half the bytes),
+                             all arithmetic stays FP64, and the true-residual restart recovers the
+                             full accuracy (a cycle reduces the residual by about 1e-6 at most, so
+                             solves that converged inside one cycle need one more); 0 (default) */
 } vem_opts;
 
 typedef struct {

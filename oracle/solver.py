@@ -302,7 +302,7 @@ class GmresResult:
     history: list
 
 
-def gmres(matvec, precond, b, rtol=1e-10, restart=30, maxit=10000, flexible=False, reorth=1):
+def gmres(matvec, precond, b, rtol=1e-10, restart=30, maxit=10000, flexible=False, reorth=1, basis32=False):
     """Right-preconditioned restarted GMRES(m) (flexible=True: FGMRES(m), which
     stores Z_j = P^-1 v_j), x0 = 0, classical Gram-Schmidt applied twice
     (CGS2; reorth=0: once, CGS1), Givens rotations.  Follows SURVEY.md §8(c) O8:
@@ -310,6 +310,13 @@ def gmres(matvec, precond, b, rtol=1e-10, restart=30, maxit=10000, flexible=Fals
       h_{j+1,j} <= 1e-14 ||A z_j||; at cycle end x += P^-1 (V y) (or Z y), the
       true residual r = b - A x is recomputed and the solve stops only if
       ||r|| <= rtol * beta.  `iterations` counts Arnoldi steps.
+
+    basis32 (traffic-reduced Krylov: a compressed basis): every basis
+    vector is the float32 rounding of the vector Arnoldi produced, fl32(r) / beta and
+    fl32(w) / ||fl32(w)||, used as such everywhere (preconditioner input, dot products,
+    updates, the combination at the cycle end), all arithmetic staying in float64; the
+    Arnoldi relation then holds up to 6e-8 per step and the true-residual restart
+    (iterative refinement) recovers the full accuracy.
     """
     n = b.shape[0]
     x = np.zeros(n)
@@ -332,7 +339,7 @@ def gmres(matvec, precond, b, rtol=1e-10, restart=30, maxit=10000, flexible=Fals
         sn = np.zeros(m)
         g = np.zeros(m + 1)
         g[0] = beta
-        V[0] = r / beta
+        V[0] = (r.astype(np.float32).astype(np.float64) if basis32 else r) / beta
         j_done = 0
         conv = False
         for j in range(m):
@@ -350,6 +357,8 @@ def gmres(matvec, precond, b, rtol=1e-10, restart=30, maxit=10000, flexible=Fals
                 H[:j + 1, j] = h1 + h2
             else:
                 H[:j + 1, j] = h1
+            if basis32:
+                w = w.astype(np.float32).astype(np.float64)
             hn = np.linalg.norm(w)
             H[j + 1, j] = hn
             for i in range(j):
@@ -400,7 +409,7 @@ def gmres(matvec, precond, b, rtol=1e-10, restart=30, maxit=10000, flexible=Fals
 def solve(M, B, rhs, precond_kind=PRECOND_BLOCK_SCHUR, rtol=1e-10, restart=30, maxit=10000,
           eps=0.0, cheb_degree=16, cheb_ratio=30.0, inner_rtol=1e-14, inner_maxit=10000,
           exact_schur=False, block=1, reorth=-1, inner_precond=INNER_MG, k_rtol=0.1, k_maxit=500,
-          k_inner_rtol=1e-8):
+          k_inner_rtol=1e-8, basis32=False):
     """Oracle counterpart of vem_mixed_upload + vem_mixed_solve; `block` is
     the number of pressure DOFs per element (layout.n_p_dof).  reorth = -1
     (auto, reading R17): CGS1 for GMRES, CGS2 for the Block-Reg
@@ -410,7 +419,7 @@ def solve(M, B, rhs, precond_kind=PRECOND_BLOCK_SCHUR, rtol=1e-10, restart=30, m
     P = Preconditioner(precond_kind, M, B, cheb_degree, cheb_ratio, eps, inner_rtol, inner_maxit,
                        exact_schur, block=block, inner_precond=inner_precond, k_rtol=k_rtol, k_maxit=k_maxit,
                        k_inner_rtol=k_inner_rtol)
-    res = gmres(lambda x: spmv_saddle(M, B, x), P.apply, rhs, rtol, restart, maxit, P.flexible, reorth)
+    res = gmres(lambda x: spmv_saddle(M, B, x), P.apply, rhs, rtol, restart, maxit, P.flexible, reorth, basis32)
     res.inner_iterations = P.inner_iterations
     res.k_iterations = P.k_iterations
     res.inner_failed = P.inner_failed

@@ -45,7 +45,7 @@ class vem_opts(C.Structure):
                 ("timing", C.c_int32), ("pcg_chunk", C.c_int32), ("reorth", C.c_int32),
                 ("l2_persist", C.c_int32), ("reorder", C.c_int32), ("inner_precond", C.c_int32),
                 ("k_maxit", C.c_int32), ("k_rtol", C.c_double), ("k_inner_rtol", C.c_double),
-                ("mg_chunk", C.c_int32)]
+                ("mg_chunk", C.c_int32), ("basis_f32", C.c_int32)]
 
 
 class vem_solve_report(C.Structure):

@@ -657,6 +657,137 @@ __global__ void __launch_bounds__(256) k_update(long n, const double *__restrict
   }
 }
 
+// ---------------------------------------------------------------------------
+// Compressed Krylov basis (opts.basis_f32: traffic-reduced Krylov):
+// every basis vector is the float32 rounding of the vector Arnoldi produced.  V (FP64) keeps
+// the rounded values for its other readers (preconditioner input, SpMV, k_combine), V32 is
+// the float copy the CGS kernels stream: 4 bytes per basis entry instead of 8.  Same
+// arithmetic as k_mdot / k_update otherwise (FP64 accumulation, same reductions).
+// ---------------------------------------------------------------------------
+__global__ void __launch_bounds__(256) k_mdot32(long n, const float *__restrict__ V32, long ldv, int nv,
+                                                int with_norm, const double *__restrict__ w, double *part,
+                                                unsigned *counter, DevState *st, int pass) {
+  __shared__ double sh[32 * VEM_DOT_CHUNK];
+  if (!st->g.active) return;
+  const int nout = nv + (with_norm ? 1 : 0);
+  const int c0 = blockIdx.y * VEM_DOT_CHUNK;
+  const int nb = gridDim.x, b = blockIdx.x;
+  double acc[VEM_DOT_CHUNK];
+#pragma unroll
+  for (int c = 0; c < VEM_DOT_CHUNK; ++c) acc[c] = 0.0;
+  const float *vp[VEM_DOT_CHUNK];
+#pragma unroll
+  for (int c = 0; c < VEM_DOT_CHUNK; ++c) vp[c] = V32 + (size_t)min(c0 + c, nv - 1) * ldv;
+  // two consecutive entries per thread (float2 / double2 loads: 8 bytes per basis vector and
+  // thread in flight, as in the FP64 kernel); ldv and the vectors are 1 KB-aligned
+  const long n2 = n >> 1;
+  const int nvc = min(VEM_DOT_CHUNK, nv - c0);              // basis vectors of this chunk (block-uniform)
+  const bool has_norm = with_norm && nv >= c0 && nv < c0 + VEM_DOT_CHUNK;   // the w.w slot lives here
+  double accn = 0.0;
+  for (long i = (long)b * blockDim.x + threadIdx.x; i < n2; i += (long)nb * blockDim.x) {
+    const double2 wi = reinterpret_cast<const double2 *>(w)[i];
+    float2 vv[VEM_DOT_CHUNK];
+#pragma unroll
+    for (int c = 0; c < VEM_DOT_CHUNK; ++c)
+      if (c < nvc) vv[c] = reinterpret_cast<const float2 *>(vp[c])[i];
+#pragma unroll
+    for (int c = 0; c < VEM_DOT_CHUNK; ++c)
+      if (c < nvc) acc[c] = fma((double)vv[c].y, wi.y, fma((double)vv[c].x, wi.x, acc[c]));
+    if (has_norm) accn = fma(wi.y, wi.y, fma(wi.x, wi.x, accn));
+  }
+  if ((n & 1) && b == 0 && threadIdx.x == 0) {   // odd tail
+    const double wi = w[n - 1];
+#pragma unroll
+    for (int c = 0; c < VEM_DOT_CHUNK; ++c)
+      if (c < nvc) acc[c] = fma((double)vp[c][n - 1], wi, acc[c]);
+    if (has_norm) accn = fma(wi, wi, accn);
+  }
+  if (has_norm) {
+#pragma unroll
+    for (int c = 0; c < VEM_DOT_CHUNK; ++c)
+      if (c0 + c == nv) acc[c] = accn;
+  }
+  block_sum_n<VEM_DOT_CHUNK>(acc, sh);
+  if (threadIdx.x == 0) {
+    double *dst = part + ((size_t)blockIdx.y * nb + b) * VEM_DOT_CHUNK;
+#pragma unroll
+    for (int c = 0; c < VEM_DOT_CHUNK; ++c) dst[c] = acc[c];
+  }
+  if (elect_last_block(counter)) {
+    __shared__ double tot[VEM_MAXM + 2];
+    reduce_partials<VEM_DOT_CHUNK>(part, nb, nout, tot);
+    if (threadIdx.x == 0) {
+      for (int o = 0; o < nv; ++o) {
+        const double h = st->vscale[o] * tot[o];
+        st->coef[o] = h * st->vscale[o];
+        st->h1[o] = (pass == 1) ? h : st->h1[o] + h;
+      }
+      if (with_norm) st->g.wnorm0 = sqrt(tot[nv]);
+      *counter = 0u;
+    }
+  }
+}
+
+// w -= sum coef_o V32_o; the final pass (with_norm) rounds w to float32, stores the float copy as
+// basis vector j + 1 and takes the norm of the ROUNDED vector (h_{j+1,j} = ||fl32(w)||)
+__global__ void __launch_bounds__(256) k_update32(long n, const float *__restrict__ V32, long ldv, int nv,
+                                                  double *__restrict__ w, float *__restrict__ w32, int with_norm,
+                                                  double *part, unsigned *counter, DevState *st, int j) {
+  __shared__ double sh[32];
+  __shared__ double cf[VEM_MAXM + 1];
+  if (!st->g.active) return;
+  for (int o = threadIdx.x; o < nv; o += blockDim.x) cf[o] = st->coef[o];
+  __syncthreads();
+  double v[1] = {0.0};
+  const long n2 = n >> 1;   // two consecutive entries per thread (float2 / double2)
+  for (long i = (long)blockIdx.x * blockDim.x + threadIdx.x; i < n2; i += (long)gridDim.x * blockDim.x) {
+    double2 wi = reinterpret_cast<double2 *>(w)[i];
+    for (int o = 0; o < nv; ++o) {
+      const float2 vv = reinterpret_cast<const float2 *>(V32 + (size_t)o * ldv)[i];
+      wi.x = fma(-cf[o], (double)vv.x, wi.x);
+      wi.y = fma(-cf[o], (double)vv.y, wi.y);
+    }
+    if (with_norm) {
+      const float2 wf = make_float2((float)wi.x, (float)wi.y);
+      reinterpret_cast<float2 *>(w32)[i] = wf;
+      wi = make_double2((double)wf.x, (double)wf.y);
+    }
+    reinterpret_cast<double2 *>(w)[i] = wi;
+    v[0] += wi.x * wi.x + wi.y * wi.y;
+  }
+  if ((n & 1) && blockIdx.x == 0 && threadIdx.x == 0) {   // odd tail
+    double wi = w[n - 1];
+    for (int o = 0; o < nv; ++o) wi = fma(-cf[o], (double)V32[(size_t)o * ldv + n - 1], wi);
+    if (with_norm) {
+      const float wf = (float)wi;
+      w32[n - 1] = wf;
+      wi = (double)wf;
+    }
+    w[n - 1] = wi;
+    v[0] += wi * wi;
+  }
+  if (!with_norm) return;
+  block_sum_n<1>(v, sh);
+  if (threadIdx.x == 0) part[blockIdx.x] = v[0];
+  if (elect_last_block(counter)) {
+    __shared__ double tot;
+    reduce_partials<1>(part, gridDim.x, 1, &tot);
+    if (threadIdx.x == 0) {
+      givens_column(st, j, sqrt(tot));
+      *counter = 0u;
+    }
+  }
+}
+
+// first basis vector of a cycle: r -> fl32(r) in place, float copy to V32_0 (beta stays ||r||)
+__global__ void k_round_basis(long n, double *__restrict__ v, float *__restrict__ v32) {
+  for (long i = (long)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (long)gridDim.x * blockDim.x) {
+    const float f = (float)v[i];
+    v32[i] = f;
+    v[i] = (double)f;
+  }
+}
+
 // y = R^-1 g (back substitution on the rotated Hessenberg), coef_i = y_i * scale_i
 __global__ void k_backsolve(DevState *st, int use_vscale) {
   if (threadIdx.x != 0 || blockIdx.x != 0) return;

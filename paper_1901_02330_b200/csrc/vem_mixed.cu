@@ -149,6 +149,7 @@ struct Ctx {
   int pdl = 1;                                   // programmatic dependent launch of the V-cycle kernels
   int mdot_slots = 0;                            // >0: k_mdot grid = one full wave of this many resident CTAs
   int update_slots = 0;                          // >0: k_update grid = one full wave (VEM_UPDATE_WAVE)
+  int mdot32_slots = 0, update32_slots = 0;      // the same for the compressed-basis kernels
   bool pdl_skip = false;                         // next launch follows an event record: plain edge
   int amg_cluster = 0;                           // coarsest smoother as one cluster launch (VEM_AMG_CLUSTER=1;
                                                  // off by default: slower than the per-step launches)
@@ -182,6 +183,7 @@ struct Ctx {
   double *dMinv = nullptr, *dSinv = nullptr, *dSepsinv = nullptr, *wdiag = nullptr, *sdiag = nullptr;
   // work vectors
   double *V = nullptr, *Z = nullptr;
+  float *V32 = nullptr;                 // float copy of the basis (opts.basis_f32; the CGS kernels read it)
   int zcap = 0;
   double *x = nullptr, *b = nullptr, *z = nullptr, *t = nullptr;
   double *cr = nullptr, *cd0 = nullptr, *cd1 = nullptr, *cx = nullptr;           // Chebyshev
@@ -1317,6 +1319,19 @@ int enqueue_arnoldi_step(Ctx *c, int kind, int j, int64_t *inner_its) {
     // one full wave of resident CTAs over all chunks (a fixed 2 CTAs/SM per chunk leaves the
     // short-basis steps at a quarter of the SM slots and the long ones at 1.75 waves)
     dim3 grid(c->mdot_slots > 0 ? std::max(c->mdot_slots / nchunk, 1) : gx, nchunk);
+    if (c->opts.basis_f32) {   // compressed basis: the CGS kernels stream the float copy (N4)
+      {
+        TimeScope ts(c, VEM_K_DOT, c->n * (4.0 * nv + 8.0));
+        dim3 grid32(c->mdot32_slots > 0 ? std::max(c->mdot32_slots / nchunk, 1) : gx, nchunk);
+        k_mdot32<<<grid32, NT, 0, c->stream>>>(c->n, c->V32, c->ldv, nv, pass == 1 ? 1 : 0, w, c->part, c->counter,
+                                               c->st, pass);
+      }
+      TimeScope ts(c, VEM_K_UPDATE, c->n * (4.0 * nv + 16.0 + (pass == npass ? 4.0 : 0.0)));
+      k_update32<<<c->update32_slots > 0 ? c->update32_slots : gx * 2, NT, 0, c->stream>>>(
+          c->n, c->V32, c->ldv, nv, w, c->V32 + (size_t)(j + 1) * c->ldv, pass == npass ? 1 : 0, c->part, c->counter,
+          c->st, j);
+      continue;
+    }
     {
       TimeScope ts(c, VEM_K_DOT, bytes_vecs(c, nv + 1));
       k_mdot<<<grid, NT, 0, c->stream>>>(c->n, c->V, c->ldv, nv, pass == 1 ? 1 : 0, w, c->part, c->counter, c->st,
@@ -1355,6 +1370,7 @@ int enqueue_cycle_end(Ctx *c, int kind, int64_t *inner_its) {
     TimeScope ts(c, VEM_K_SPMV, bytes_spmv(c) + 8.0 * c->n);
     launch_residual(c, c->x, c->b, c->V, 1);
   }
+  if (c->opts.basis_f32) k_round_basis<<<grid_stream(c, c->n), NT, 0, c->stream>>>(c->n, c->V, c->V32);
   CKL();
   return 0;
 }
@@ -1384,6 +1400,10 @@ int ensure_work(Ctx *c, int kind) {
   if (!c->V) {
     DA(c->V, (size_t)(m + 1) * c->ldv);
     CK(cudaMemsetAsync(c->V, 0, (size_t)(m + 1) * c->ldv * sizeof(double), c->stream));
+  }
+  if (c->opts.basis_f32 && !c->V32) {
+    DA(c->V32, (size_t)(m + 1) * c->ldv);
+    CK(cudaMemsetAsync(c->V32, 0, (size_t)(m + 1) * c->ldv * sizeof(float), c->stream));
   }
   if (is_flexible(kind) && c->zcap < m) {
     if (c->Z) dfree(c, c->Z);
@@ -1457,6 +1477,7 @@ int solve_impl(Ctx *c, const double *rhs, double tol, int maxit, int kind, doubl
   CK(cudaStreamSynchronize(c->stream));
   // beta0 = ||b||; V0 = b
   launch_residual(c, nullptr, c->b, c->V, 0);
+  if (c->opts.basis_f32) k_round_basis<<<grid_stream(c, c->n), NT, 0, c->stream>>>(c->n, c->V, c->V32);
   CKL();
   CK(cudaMemcpyAsync(&c->hst->g, &c->st->g, sizeof(GmresState), cudaMemcpyDeviceToHost, c->stream));
   CK(cudaStreamSynchronize(c->stream));
@@ -2506,6 +2527,13 @@ int upload_impl(Ctx *c, const vem_csr *M, const vem_csr *B, const vem_csr *W, do
     int occ = 0;
     if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_update, NT, 0) == cudaSuccess && occ > 0)
       c->update_slots = occ * c->sm_count;
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_update32, NT, 0) == cudaSuccess && occ > 0)
+      c->update32_slots = occ * c->sm_count;
+  }
+  if (c->mdot_slots > 0) {
+    int occ = 0;
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_mdot32, NT, 0) == cudaSuccess && occ > 0)
+      c->mdot32_slots = occ * c->sm_count;
   }
 
   // raw uploads (freed after the merged formats are built)
@@ -2951,6 +2979,7 @@ void vem_mixed_default_options(vem_opts *o) {
   o->k_rtol = 0.1;
   o->k_inner_rtol = 1e-8;
   o->mg_chunk = 2;
+  o->basis_f32 = 0;
 }
 
 static int validate_opts(Ctx *c, const vem_opts *o) {
@@ -2963,6 +2992,7 @@ static int validate_opts(Ctx *c, const vem_opts *o) {
   if (o->inner_precond < 0 || o->inner_precond > 1) return fail(c, VEM_ERR_INVALID, "inner_precond must be 0 or 1");
   if (o->k_maxit < 1 || !(o->k_rtol > 0.0) || !(o->k_inner_rtol > 0.0) || o->mg_chunk < 1)
     return fail(c, VEM_ERR_INVALID, "bad kind-5 / MG-PCG options");
+  if (o->basis_f32 < 0 || o->basis_f32 > 1) return fail(c, VEM_ERR_INVALID, "basis_f32 must be 0 or 1");
   return 0;
 }
 
@@ -3308,6 +3338,8 @@ int vem_mixed_set_options(vem_ctx *h, const vem_opts *o) {
   if (realloc_v) {
     if (c->V) dfree(c, c->V);
     c->V = nullptr;
+    if (c->V32) dfree(c, c->V32);
+    c->V32 = nullptr;
     if (c->Z) dfree(c, c->Z);
     c->Z = nullptr;
     c->zcap = 0;

@@ -482,6 +482,35 @@ def test_fixed_grid_cgs_fallback(monkeypatch):
     sv.close()
 
 
+@pytest.mark.parametrize("name,kind", [("C1", 1), ("C3s", 1), ("C3s", 3), ("C2s", 1), ("C3s", 2)])
+def test_compressed_basis_parity(name, kind):
+    """opts.basis_f32 (traffic-reduced Krylov): the basis vectors are the
+    float32 roundings of the Arnoldi vectors, the CGS kernels stream the float copy.  Same
+    definition in the oracle (gmres(basis32=True)): count +-2, u and p to 1e-8 of the oracle's
+    compressed-basis solve AND of its full-precision solve (the restart recovers the accuracy)."""
+    s = system(name)
+    cfg = configs.CONFIGS[name]
+    eps = configs.eps_for(s)
+    nb = s.layout.n_p_dof
+    ref = O.solve(s.M, s.B, s.rhs, kind, 1e-10, cfg.restart, eps=eps, block=nb, basis32=True)
+    full = O.solve(s.M, s.B, s.rhs, kind, 1e-10, cfg.restart, eps=eps, block=nb)
+    assert ref.converged
+    sv = solver_for(s, restart=cfg.restart, basis_f32=1)
+    res = sv.solve(torch.from_numpy(s.rhs).cuda(), 1e-10, 10000, kind)
+    r = res.report
+    log_counts(test="compressed_basis", config=name, precond=kind, gpu=r["iterations"], oracle=ref.iterations,
+               oracle_fp64_basis=full.iterations)
+    assert r["converged"] == 1 and abs(r["iterations"] - ref.iterations) <= 2, (r["iterations"], ref.iterations)
+    nu = s.layout.n_u
+    for x in (ref.x, full.x):
+        assert rel_inf(res.u.cpu().numpy(), x[:nu]) <= 1e-8 and rel_inf(res.p.cpu().numpy(), x[nu:]) <= 1e-8
+    # switching back restores the full-precision basis
+    sv.set_options(basis_f32=0)
+    res2 = sv.solve(torch.from_numpy(s.rhs).cuda(), 1e-10, 10000, kind)
+    assert abs(res2.report["iterations"] - full.iterations) <= 2
+    sv.close()
+
+
 def test_solve_host_matches_device_and_is_deterministic():
     s = system("C3s")
     sv = solver_for(s, restart=50)
