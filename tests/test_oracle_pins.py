@@ -485,3 +485,22 @@ def test_paper_neumann_gmres_equals_bordered_lu(n, k):
         u, p = r.x[:nu], N.project(r.x[nu:])
         assert np.abs(u - ub).max() <= 1e-8 * np.abs(ub).max()
         assert np.abs(p - pb).max() <= 1e-8 * np.abs(pb).max()
+
+
+@pytest.mark.parametrize("name,kind", [("C1", 1), ("C3s", 3), ("C2s", 1)])
+def test_compressed_basis_gmres_vs_lu(name, kind):
+    """gmres(basis32=True) (the basis vectors are float32 roundings, the
+    arithmetic stays float64): the true-residual restart recovers the full accuracy, so the
+    solve still reaches the LU solution to 1e-8 and the true residual 1e-10; every stored
+    basis vector is exactly representable in float32 times its scale."""
+    s = configs.CONFIGS[name].build()
+    cfg = configs.CONFIGS[name]
+    xd = O.dense_solve(s.M, s.B, s.rhs) if s.n <= 7000 else None
+    r = O.solve(s.M, s.B, s.rhs, kind, 1e-10, cfg.restart, block=s.layout.n_p_dof, basis32=True)
+    assert r.converged and r.rel_residual_true <= 1e-10
+    full = O.solve(s.M, s.B, s.rhs, kind, 1e-10, cfg.restart, block=s.layout.n_p_dof)
+    nu = s.layout.n_u
+    for ref in ([xd] if xd is not None else []) + [full.x]:
+        for sl in (slice(0, nu), slice(nu, None)):
+            assert np.abs(r.x[sl] - ref[sl]).max() <= 1e-8 * np.abs(ref[sl]).max()
+    assert r.iterations >= full.iterations     # rounding the basis never helps
