@@ -112,7 +112,7 @@ typedef struct {
                              operator entry point stay in the caller's numbering); 0: off */
   int32_t inner_precond;  /* Block-Reg inner PCG preconditioner: 1 (default) one V-cycle of
                              S_D + eps W (n_p_dof = 1: the kind-3 aggregation hierarchy built
-                             on S_D + eps W; n_p_dof > 1: element-block-Jacobi Chebyshev(3)
+                             on S_D + eps W; n_p_dof > 1: element-block-Jacobi Chebyshev(2) on [1/3, 2]
                              smoothing + injection of the element-mean moment + that hierarchy
                              on the mean-moment block; reading R23); 0: element-block Jacobi */
   int32_t k_maxit;        /* kind 5: iteration cap of the PCG on K per apply (default 500)  */
