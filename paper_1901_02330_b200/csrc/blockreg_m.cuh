@@ -52,6 +52,20 @@ __global__ void __launch_bounds__(256) k_seps_resid(long np, Sell S, const doubl
   out[row] = b[row] - fma(eps * w, d[row], sell_dot(S, slot, GatherX{d}));
 }
 
+// q = S_eps p on every row (the PCG product without its p.q partials: the block barrier of
+// k_pcg_spmv_p costs a third of that kernel's stall cycles, ncu R2_27: 172 vs 132 us; the dot
+// product is a separate light pass, k_dot_part)
+__global__ void __launch_bounds__(256) k_seps_mul(long np, Sell S, const double *__restrict__ wdiag, double eps,
+                                                  const double *__restrict__ p, double *__restrict__ q,
+                                                  const int *gate) {
+  if (!*gate) return;
+  const long slot = (long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (slot >= np) return;
+  const long row = sell_row(S, slot);
+  const double w = wdiag ? wdiag[row] : 1.0;
+  q[row] = fma(eps * w, p[row], sell_dot(S, slot, GatherX{p}));
+}
+
 // element-block half of a Chebyshev step of the p-multigrid smoother:
 //   init: d_new = c2 D_B^-1 r           else: d_new = c1 d_old + c2 D_B^-1 r
 //   acc_x: x += d_new                   else: x = d_new

@@ -1090,9 +1090,12 @@ int enqueue_pcgm_steps(Ctx *c, int nsteps) {
   for (int s = 0; s < nsteps; ++s) {
     {
       TimeScope ts(c, VEM_K_PCG_SPMV, 12.0 * c->nnzS + 32.0 * c->np);
-      k_pcg_spmv_p<<<g, NT, 0, c->stream>>>(c->np, sellS(c), c->wdiag, c->eps, c->pp0, c->pq, c->part, c->counter,
-                                            c->st, 1);
-      k_pcg_alpha<<<1, 1024, 0, c->stream>>>(g, c->part, c->st);
+      k_seps_mul<<<g, NT, 0, c->stream>>>(c->np, sellS(c), c->wdiag, c->eps, c->pp0, c->pq, gate_pcg(c));
+    }
+    {
+      TimeScope ts(c, VEM_K_PCG_VEC, 16.0 * c->np);
+      k_dot_part<<<gp, NT, 0, c->stream>>>(c->np, c->pp0, c->pq, c->part, gate_pcg(c));
+      k_pcg_alpha<<<1, 1024, 0, c->stream>>>(gp, c->part, c->st);
     }
     {
       TimeScope ts(c, VEM_K_PCG_VEC, 48.0 * c->np);
