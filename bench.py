@@ -337,10 +337,11 @@ def secondary_c3(pkg, torch, steps=3):
     sv = pkg.VemMixed(s.M, s.B, eps=0.0, layout=s.layout, opts=pkg.default_options(restart=cfg.restart))
     rhs = torch.from_numpy(s.rhs).cuda()
     out = {"workload": f"C3: {cfg.describe}", "n_dofs": s.n}
-    for kind in (3, 4, 30):
-        if kind == 30:   # kind 3 with the compressed (float32) Krylov basis, SURVEY.md §8(f) N4
+    for kind in (3, 4, 30, 40):
+        if kind >= 30:   # kinds 3 / 4 with the compressed (float32) Krylov basis, SURVEY.md §8(f) N4
             sv.set_options(basis_f32=1)
-            kind_arg, label = 3, "block_schur amg v-cycle (kind 3) with the float32-compressed Krylov basis"
+            kind_arg = kind // 10
+            label = KIND_NAMES[kind_arg] + ", float32-compressed Krylov basis (opts.basis_f32)"
         else:
             kind_arg, label = kind, KIND_NAMES[kind]
         for _ in range(2):
@@ -356,7 +357,7 @@ def secondary_c3(pkg, torch, steps=3):
         for r in reps:
             check_full(r, cfg.rtol, f"C3 kind {kind}")
         ms = a.elapsed_time(b) / steps
-        out["kind3_basis_f32" if kind == 30 else f"kind{kind}"] = {
+        out[f"kind{kind_arg}_basis_f32" if kind >= 30 else f"kind{kind}"] = {
                               "precond": label, "time_to_solution_ms": round(ms, 2),
                               "iterations": reps[-1]["iterations"], "solves_per_s": round(1e3 / ms, 3),
                               "gmres_it_per_s": round(reps[-1]["iterations"] / (ms / 1e3), 1),
